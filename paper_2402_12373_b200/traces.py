@@ -1,0 +1,295 @@
+"""Traces, specifications and the trace-file format (the input model either side of the hot path).
+
+A trace is a sequence of characters; a character is an int bitmask over the alphabet's
+propositions.  Contract follows the reference's `traces.py` (paths relative to
+/root/reference/pkg/src/ltllearn/): `Alphabet` `traces.py:23-53`, `Specification`
+`traces.py:56-106` (per-side de-duplication keeping first occurrences, P and N disjoint, row order
+= positives then negatives), suffix table `traces.py:145-172`, file format `traces.py:180-253`.
+
+Unlike the reference (tuples of tuples, <= 64 traces of <= 63 positions) a specification here is
+backed by one padded ``uint16[R, Lmax]`` character matrix plus a length vector, so that 2^21
+traces can be de-duplicated, censused and bit-packed with vectorised numpy / device code; the
+tuple views `pos` / `neg` / `traces` are materialised lazily for small inputs.
+"""
+from __future__ import annotations
+
+import warnings
+from typing import Iterable, Sequence
+
+import numpy as np
+
+Trace = tuple
+
+
+class TraceFormatError(ValueError):
+    pass
+
+
+class Alphabet:
+    __slots__ = ("names",)
+
+    def __init__(self, names: Sequence[str]):
+        names = tuple(names)
+        if not names:
+            raise ValueError("alphabet must be non-empty")
+        if len(set(names)) != len(names):
+            raise ValueError("proposition names must be unique")
+        for n in names:
+            if n in ("X", "F", "G", "U") or not n or not all(c.isalnum() or c == "_" for c in n):
+                raise ValueError(f"invalid proposition name {n!r}")
+        object.__setattr__(self, "names", names)
+
+    def __setattr__(self, *_):
+        raise AttributeError("immutable")
+
+    @staticmethod
+    def default(size: int) -> "Alphabet":
+        return Alphabet(tuple(f"p{i}" for i in range(size)))
+
+    @property
+    def size(self) -> int:
+        return len(self.names)
+
+    @property
+    def n_chars(self) -> int:
+        return 1 << len(self.names)
+
+    def index_of(self, name: str):
+        try:
+            return self.names.index(name)
+        except ValueError:
+            return None
+
+    def __eq__(self, other):
+        return isinstance(other, Alphabet) and other.names == self.names
+
+    def __hash__(self):
+        return hash(self.names)
+
+    def __repr__(self):
+        return f"Alphabet({self.names})"
+
+
+def _as_matrix(traces: Iterable) -> tuple[np.ndarray, np.ndarray]:
+    rows = [np.asarray(tr, dtype=np.int64).reshape(-1) for tr in traces]
+    lengths = np.array([len(r) for r in rows], dtype=np.int64)
+    width = int(lengths.max()) if len(rows) else 0
+    chars = np.zeros((len(rows), max(width, 1)), dtype=np.uint16)
+    for k, r in enumerate(rows):
+        if len(r):
+            if r.min() < 0:
+                raise ValueError("trace characters must be non-negative bitmasks")
+            if r.max() > 0xFFFF:
+                raise ValueError("at most 16 propositions are supported")
+            chars[k, : len(r)] = r
+    return chars, lengths
+
+
+def _row_keys(chars: np.ndarray, lengths: np.ndarray, width: int) -> np.ndarray:
+    """One opaque bytes-like key per trace: (length, padded characters)."""
+    R = len(lengths)
+    key = np.zeros((R, width + 1), dtype=np.uint16)
+    key[:, 0] = lengths  # lengths < 65536 checked by callers
+    key[:, 1 : 1 + chars.shape[1]] = chars
+    return np.ascontiguousarray(key).view(np.dtype((np.void, key.dtype.itemsize * (width + 1)))).reshape(R)
+
+
+def _first_occurrences(keys: np.ndarray) -> np.ndarray:
+    _, first = np.unique(keys, return_index=True)
+    return np.sort(first)
+
+
+class Specification:
+    """Disjoint positive / negative trace sets in a fixed, meaningful order (it is the row order
+    of every characteristic matrix: positives first)."""
+
+    def __init__(self, pos=(), neg=(), *, _arrays=None):
+        if _arrays is None:
+            pc, pl = _as_matrix(pos)
+            nc, nl = _as_matrix(neg)
+        else:
+            pc, pl, nc, nl = _arrays
+        self._build(pc, pl, nc, nl)
+
+    @staticmethod
+    def from_arrays(pos_chars, pos_lengths, neg_chars, neg_lengths) -> "Specification":
+        """Array form: ``chars[k, j]`` is character j of trace k (entries at j >= length ignored)."""
+        pc = np.ascontiguousarray(pos_chars, dtype=np.uint16).reshape(len(pos_lengths), -1)
+        nc = np.ascontiguousarray(neg_chars, dtype=np.uint16).reshape(len(neg_lengths), -1)
+        return Specification(_arrays=(pc, np.asarray(pos_lengths, dtype=np.int64), nc, np.asarray(neg_lengths, dtype=np.int64)))
+
+    def _build(self, pc, pl, nc, nl):
+        width = max(pc.shape[1] if len(pl) else 1, nc.shape[1] if len(nl) else 1, 1)
+        if max(int(pl.max()) if len(pl) else 0, int(nl.max()) if len(nl) else 0) > 0xFFFF:
+            raise ValueError("traces longer than 65535 positions are not supported")
+
+        def clean(chars, lengths):
+            full = np.zeros((len(lengths), width), dtype=np.uint16)
+            if len(lengths):
+                full[:, : chars.shape[1]] = chars
+                full[np.arange(width)[None, :] >= lengths[:, None]] = 0  # canonical padding
+            return full
+
+        pc, nc = clean(pc, pl), clean(nc, nl)
+        sides = []
+        for name, chars, lengths in (("positive", pc, pl), ("negative", nc, nl)):
+            if len(lengths):
+                keys = _row_keys(chars, lengths, width)
+                keep = _first_occurrences(keys)
+                if len(keep) != len(lengths):
+                    warnings.warn(f"{len(lengths) - len(keep)} duplicate {name} trace(s) dropped", stacklevel=4)
+                chars, lengths, keys = chars[keep], lengths[keep], keys[keep]
+            else:
+                keys = np.zeros(0, dtype=np.dtype((np.void, 2 * (width + 1))))
+            sides.append((chars, lengths, keys))
+        (pc, pl, pk), (nc, nl, nk) = sides
+        if len(pk) and len(nk):
+            clash = np.isin(pk, nk)
+            if clash.any():
+                i = int(np.argmax(clash))
+                j = int(np.argmax(nk == pk[i]))
+                raise ValueError(f"trace occurs on both sides (positive #{i}, negative #{j})")
+        self.n_pos = len(pl)
+        self.n_neg = len(nl)
+        self.chars = np.concatenate([pc, nc], axis=0) if (len(pl) + len(nl)) else np.zeros((0, width), np.uint16)
+        self.lengths = np.concatenate([pl, nl]).astype(np.int64)
+        self._tuples = None
+
+    # -- views -------------------------------------------------------------------------
+    @property
+    def size(self) -> int:
+        return self.n_pos + self.n_neg
+
+    @property
+    def max_len(self) -> int:
+        return int(self.lengths.max()) if len(self.lengths) else 0
+
+    def _materialise(self):
+        if self._tuples is None:
+            self._tuples = tuple(
+                tuple(int(c) for c in self.chars[r, : self.lengths[r]]) for r in range(self.size)
+            )
+        return self._tuples
+
+    @property
+    def traces(self) -> tuple:
+        return self._materialise()
+
+    @property
+    def pos(self) -> tuple:
+        return self._materialise()[: self.n_pos]
+
+    @property
+    def neg(self) -> tuple:
+        return self._materialise()[self.n_pos :]
+
+    def char_width(self) -> int:
+        top = int(np.bitwise_or.reduce(self.chars, axis=None)) if self.chars.size else 0
+        return max(1, top.bit_length())
+
+    def positive_char_census(self) -> tuple[int, int]:
+        """(#positions, #set proposition bits) over the positive traces -- all that the
+        closed-form overfit cost needs."""
+        pc = self.chars[: self.n_pos]
+        n_positions = int(self.lengths[: self.n_pos].sum())
+        bits = np.unpackbits(pc.view(np.uint8), axis=None)
+        return n_positions, int(bits.sum())
+
+    def __repr__(self):
+        return f"Specification(|P|={self.n_pos}, |N|={self.n_neg}, max_len={self.max_len})"
+
+
+# ---------------------------------------------------------------------------------- suffix table
+
+
+class SuffixTable:
+    """One representative (row, offset) per distinct non-empty suffix, in first-occurrence scan
+    order (row-major).  Only its size decides whether fingerprints can be exact (<= 126), so the
+    scan stops as soon as ``limit`` distinct suffixes have been seen: ``count`` is then
+    ``limit + 1`` ("too many") and the projection is meaningless.  (Reference `traces.py:145-172`
+    scans everything, O(R*L^2); every non-empty trace is its own suffix, so R > limit + 1 traces
+    already decide the question.)"""
+
+    __slots__ = ("count", "rows", "offsets", "complete")
+
+    def __init__(self, count, rows, offsets, complete):
+        self.count, self.rows, self.offsets, self.complete = count, tuple(rows), tuple(offsets), complete
+
+    @staticmethod
+    def from_spec(spec: Specification, limit: int | None = None) -> "SuffixTable":
+        if limit is not None and int(np.count_nonzero(spec.lengths)) > limit:
+            return SuffixTable(limit + 1, (), (), False)
+        seen = set()
+        rows, offs = [], []
+        for r, tr in enumerate(spec.traces):
+            for j in range(len(tr)):
+                suf = tr[j:]
+                if suf not in seen:
+                    seen.add(suf)
+                    rows.append(r)
+                    offs.append(j)
+                    if limit is not None and len(seen) > limit:
+                        return SuffixTable(limit + 1, (), (), False)
+        return SuffixTable(len(seen), rows, offs, True)
+
+
+# ---------------------------------------------------------------------------------- file format
+# One trace per line, positions separated by ';', each position a comma-separated 0/1 vector
+# over the alphabet; a '---' line separates positives from negatives; later sections ignored.
+
+
+def _parse_line(line: str, line_no: int, width):
+    chars = []
+    for token in line.split(";"):
+        bits = token.split(",")
+        if width is None:
+            width = len(bits)
+        elif len(bits) != width:
+            raise TraceFormatError(f"line {line_no}: expected {width} propositions, found {len(bits)}")
+        char = 0
+        for p, b in enumerate(bits):
+            b = b.strip()
+            if b == "1":
+                char |= 1 << p
+            elif b != "0":
+                raise TraceFormatError(f"line {line_no}: bad proposition value {b!r}")
+        chars.append(char)
+    return tuple(chars), width
+
+
+def load_spec(path) -> tuple[Specification, Alphabet]:
+    sections: list[list] = [[]]
+    width = None
+    with open(path, "r", encoding="utf-8") as fh:
+        for line_no, raw in enumerate(fh, start=1):
+            line = raw.strip()
+            if not line:
+                continue
+            if line == "---":
+                sections.append([])
+                continue
+            tr, width = _parse_line(line, line_no, width)
+            sections[-1].append(tr)
+    if len(sections) < 2:
+        raise TraceFormatError("missing '---' separator between trace blocks")
+    if len(sections) > 2:
+        warnings.warn(f"{path}: ignoring {len(sections) - 2} extra '---' section(s)")
+    if width is None:
+        raise TraceFormatError("empty trace file")
+    return Specification(tuple(sections[0]), tuple(sections[1])), Alphabet.default(width)
+
+
+def format_trace(tr, width: int) -> str:
+    return ";".join(",".join("1" if (int(c) >> p) & 1 else "0" for p in range(width)) for c in tr)
+
+
+def save_spec(spec: Specification, path, alphabet: Alphabet | None = None) -> None:
+    width = alphabet.size if alphabet is not None else spec.char_width()
+    if (spec.lengths == 0).any():
+        raise TraceFormatError("the trace file format cannot carry empty traces")
+    with open(path, "w", encoding="utf-8") as fh:
+        for tr in spec.pos:
+            fh.write(format_trace(tr, width) + "\n")
+        fh.write("---\n")
+        for tr in spec.neg:
+            fh.write(format_trace(tr, width) + "\n")
