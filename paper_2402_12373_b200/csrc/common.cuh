@@ -1,0 +1,181 @@
+// common.cuh -- shared device/host definitions for the B200 screening core (sm_100a only).
+//
+// Data layout in HBM:
+//   * characteristic matrices ("entries") are stored in GROUPS of 32 entries, word-major inside a
+//     group:  word k (k = row*W + w, 0 <= k < n = R*W) of entry e lives at
+//         cms[((e >> 5) * n + k) * 32 + (e & 31)]
+//     so the 32 lanes of a warp that own the 32 entries of a group read/write one aligned 256-byte
+//     line per word (fully coalesced, 8 sectors), and 4 consecutive entries' copies of one word are
+//     one aligned 32-byte sector (the left-operand register tile is one 256-bit broadcast load).
+//   * the uniqueness set is an open-addressing table of 32-byte slots {lo, hi, rank, pad}: one
+//     DRAM sector per probe.  key = 126-bit fingerprint (top 2 bits of hi always 0, reference
+//     kernels.py:35), EMPTY key = all ones.  rank = global enumeration rank of the candidate that
+//     owns the key (atomicMin => "lowest enumeration rank wins" = the sequential reference's
+//     first-wins admission, _speedups.pyx:245-262), ~0 = key present but not a member.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+typedef unsigned long long u64;
+typedef unsigned int u32;
+typedef long long i64;
+
+// opcodes (reference formula.py:13-20); 0 doubles as "identity" for add_entry / fingerprint_of.
+enum { OP_IDENT = 0, OP_NOT = 1, OP_AND = 2, OP_OR = 3, OP_NEXT = 4, OP_FINALLY = 5, OP_GLOBALLY = 6, OP_UNTIL = 7 };
+enum { VAR_GATHER = 0, VAR_MUELLER = 1, VAR_FKP = 2 };
+enum { PIECE_UNARY = 0, PIECE_RECT = 1, PIECE_TRI = 2 };
+enum { MODE_INSERT = 0, MODE_FP_ONLY = 1, MODE_LOOKUP = 2 };
+
+#define LTL_GROUP 32
+#define LTL_NONE 0xFFFFFFFFu
+#define LTL_RANK_NONE 0xFFFFFFFFFFFFFFFFull
+#define LTL_CTA 256
+
+// fingerprint constants (reference kernels.py:28-35)
+#define K_MIX1 0xBF58476D1CE4E5B9ull
+#define K_MIX2 0x94D049BB133111EBull
+#define K_STEP 0x9E3779B97F4A7C15ull
+#define K_FOLD0 0xC2B2AE3D27D4EB4Full
+#define K_FOLD1 0x9E3779B185EBCA87ull
+#define K_SEED0 0x243F6A8885A308D3ull
+#define K_SEED1 0x13198A2E03707344ull
+#define K_HI_CLEAR 0x3FFFFFFFFFFFFFFFull
+
+struct __align__(32) Slot {
+    u64 lo, hi;  // key (16-byte aligned: one ATOMG.CAS.128)
+    u64 rank;    // owner's global enumeration rank
+    u64 pad;
+};
+
+// One run of candidates inside a chunk, in enumeration order (host: Chunker in core.cu).
+struct Piece {
+    int op;
+    int kind;          // PIECE_*
+    i64 i0, i1;        // left / only operand entry range [i0, i1)
+    i64 j0, j1;        // right operand entry range [j0, j1); TRI: columns (i, j1) for row i
+    i64 cbase;         // chunk-local rank of this piece's first candidate
+    u32 tile_base;     // first CTA of this piece in the launch
+    u32 tiles_j;       // CTAs per i-tile row
+    i64 ti0, tj0;      // first i-tile index (i0 / TI) and first j group (j0 >> 5)
+};
+
+// One deposit of the "bits" fingerprints (gather / fkp): take ((word[k] >> rsh) & mask) and OR it
+// into the 128-bit fingerprint at bit position pos (reference _speedups.pyx:188-195, 205-222).
+struct Deposit {
+    u32 k;
+    u32 rsh;
+    u64 mask;
+    u32 pos;
+    u32 pad;
+};
+
+// Device-resident control block of one chunk.
+struct Ctl {
+    u64 solver_c;   // min chunk-local rank whose error count <= err_max (atomicMin), ~0 if none
+    u64 oom_c;      // chunk-local rank of the first new unique that does not fit the budget, ~0 if none
+    u64 total;      // winners below the cutoff
+    u64 fp_hi, fp_lo;  // MODE_FP_ONLY / MODE_LOOKUP result for single-candidate queries
+    u64 found;
+    u64 pad[2];
+};
+
+struct ScreenParams {
+    const u64* cms;       // entry store (group layout)
+    const u64* masks;     // n words
+    const Piece* pieces;
+    int n_pieces;
+    int R, W, n_pos, err_max;
+    i64 n;                // words per entry
+    int variant, mask_k, n_dep;
+    const Deposit* deps;
+    int mode, check_solve;
+    Slot* table;
+    u64 table_mask;
+    u64 gbase;            // global rank of chunk-local rank 0
+    u32* slot;            // per candidate: contender slot / NONE   (phase A out, resolve in/out)
+    u64* fp_out;          // MODE_FP_ONLY: 2 words per candidate (hi, lo), may be null
+    Ctl* ctl;
+    // phase B
+    u64* cms_out;         // same buffer as cms (entries >= n_base are written)
+    i64 n_base;           // entry index of destination 0
+    unsigned char* rec_op;
+    int* rec_lhs;
+    int* rec_rhs;
+    u64 cutoff;           // candidates with chunk-local rank >= cutoff are ignored
+};
+
+__host__ __device__ __forceinline__ u64 mix64(u64 x) {  // reference kernels.py:50-57
+    x ^= x >> 30;
+    x *= K_MIX1;
+    x ^= x >> 27;
+    x *= K_MIX2;
+    x ^= x >> 31;
+    return x;
+}
+
+__host__ __device__ __forceinline__ size_t cm_index(i64 e, i64 n, i64 k) {
+    return ((size_t)(e >> 5) * (size_t)n + (size_t)k) * LTL_GROUP + (size_t)(e & 31);
+}
+
+#ifdef __CUDACC__
+// ---- 128-bit key helpers -----------------------------------------------------------------
+struct Key128 {
+    u64 lo, hi;
+};
+
+__device__ __forceinline__ Key128 ld_key(const Slot* s) {
+    Key128 k;
+    asm volatile("ld.global.cg.v2.u64 {%0, %1}, [%2];" : "=l"(k.lo), "=l"(k.hi) : "l"(s) : "memory");
+    return k;
+}
+
+__device__ __forceinline__ Key128 cas_key(Slot* s, Key128 cmp, Key128 val) {
+    Key128 old;
+    asm volatile(
+        "{\n\t.reg .b128 c, v, o;\n\t"
+        "mov.b128 c, {%2, %3};\n\t"
+        "mov.b128 v, {%4, %5};\n\t"
+        "atom.global.cas.b128 o, [%6], c, v;\n\t"
+        "mov.b128 {%0, %1}, o;\n\t}"
+        : "=l"(old.lo), "=l"(old.hi)
+        : "l"(cmp.lo), "l"(cmp.hi), "l"(val.lo), "l"(val.hi), "l"(s)
+        : "memory");
+    return old;
+}
+
+__device__ __forceinline__ u64 slot_hash(u64 hi, u64 lo) { return mix64(lo ^ (hi * K_STEP)); }
+
+// Find the slot of key (inserting it if absent).  Keys never change once written, so a stale
+// EMPTY read only costs one extra CAS.
+__device__ __forceinline__ u64 table_find_or_claim(Slot* table, u64 mask, u64 hi, u64 lo) {
+    u64 s = slot_hash(hi, lo) & mask;
+    const Key128 empty = {~0ull, ~0ull};
+    const Key128 mine = {lo, hi};
+    while (true) {
+        Key128 k = ld_key(table + s);
+        if (k.hi == hi && k.lo == lo) return s;
+        if (k.hi == ~0ull) {
+            Key128 old = cas_key(table + s, empty, mine);
+            if (old.hi == ~0ull || (old.hi == hi && old.lo == lo)) return s;
+        }
+        s = (s + 1) & mask;
+    }
+}
+
+// Lookup only: slot index or ~0.
+__device__ __forceinline__ u64 table_find(const Slot* table, u64 mask, u64 hi, u64 lo) {
+    u64 s = slot_hash(hi, lo) & mask;
+    while (true) {
+        Key128 k = ld_key(table + s);
+        if (k.hi == hi && k.lo == lo) return s;
+        if (k.hi == ~0ull) return ~0ull;
+        s = (s + 1) & mask;
+    }
+}
+
+__device__ __forceinline__ u64 ld_rank(const Slot* s) {
+    u64 r;
+    asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(r) : "l"(&s->rank) : "memory");
+    return r;
+}
+#endif
