@@ -1,0 +1,152 @@
+/*
+ * ltl_core.h -- C ABI of the B200 screening core (libltlcore.so).
+ *
+ * This is the drop-in boundary for the hot path of the reference learner: the object returned by
+ *   ltllearn.kernels.make_core(masks, n_pos, err_max, variant, proj_rows, proj_offs, fkp_bits, mask_k,
+ *                              budget_bytes, backend)                       (reference kernels.py:140-172)
+ * whose contract is spelled out by the reference's two interchangeable cores,
+ *   ltllearn._speedups.Core   (reference _speedups.pyx:61-380, Cython/C++)  and
+ *   ltllearn._kernels_py.PyCore (reference _kernels_py.py:32-281).
+ * Every entry point below names the reference member it replaces.  Paths are relative to
+ * /root/reference/pkg/src/ltllearn/.
+ *
+ * Conventions
+ *   - plain C types only; all buffers are HOST pointers owned by the caller; the core copies in / out.
+ *   - a characteristic matrix (CM) is uint64[R*W], row-major (word w of row r at cm[r*W + w]); trace
+ *     position j of a row lives in word j/64 at bit 63 - j%64.  W == 1 is exactly the reference's uint64[R].
+ *   - every function returns LTL_OK (0) or a negative LTL_ERR_* code; the message for the last failure
+ *     on a handle is available from ltl_core_last_error().  No exception crosses the ABI.
+ *   - a handle is single-threaded and not re-entrant (like the reference core, which holds the GIL).
+ *   - the library talks to the GPU only; there is no CPU fallback.  Without a usable CUDA device
+ *     ltl_core_create() fails with LTL_ERR_CUDA.
+ */
+#ifndef LTL_CORE_H
+#define LTL_CORE_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define LTL_ABI_VERSION 1
+
+#if defined(__GNUC__)
+#define LTL_API __attribute__((visibility("default")))
+#else
+#define LTL_API
+#endif
+
+/* status codes of the screening calls: reference kernels.py:43-45 */
+#define LTL_S_DONE 0
+#define LTL_S_SOLVED 1
+#define LTL_S_OOM 2
+
+/* fingerprint variants: reference kernels.py:39-41 */
+#define LTL_V_GATHER 0
+#define LTL_V_MUELLER 1
+#define LTL_V_FKP 2
+
+/* error codes */
+#define LTL_OK 0
+#define LTL_ERR_ARG (-1)        /* bad argument (the reference raises ValueError / IndexError) */
+#define LTL_ERR_CUDA (-2)       /* CUDA runtime / driver failure, no device */
+#define LTL_ERR_BUDGET (-3)     /* add_entry over the logical budget (the reference raises CoreOOM, _speedups.pyx:275-276) */
+#define LTL_ERR_DEVICE_OOM (-4) /* device memory exhausted before the logical budget */
+
+typedef struct ltl_core ltl_core;
+
+/* One run of candidates of a cost level, in enumeration order (reference enumerator.py:271-296 dispatches
+ * exactly these to screen_unary / screen_binary, chunked):  op applied to left entries [a0, a1) and, for
+ * binary ops, right entries [b0, b1); b0 = b1 = -1 for unary ops; tri != 0 restricts to right index >
+ * left index (reference _speedups.pyx:367). */
+typedef struct ltl_segment {
+    int32_t op;
+    int32_t tri;
+    int64_t a0, a1;
+    int64_t b0, b1;
+} ltl_segment;
+
+/* kernel classes for ltl_core_kernel_stats */
+#define LTL_K_SCREEN 0      /* evaluate + check + fingerprint + file in the uniqueness table ("phase A") */
+#define LTL_K_FINALIZE 1    /* row-split runs only: combine partial fingerprints */
+#define LTL_K_RESOLVE 2     /* which candidate owns its fingerprint */
+#define LTL_K_SCAN 3        /* ordered compaction offsets */
+#define LTL_K_EMIT 4        /* records of the winners */
+#define LTL_K_MATERIALIZE 5 /* append the winners' matrices ("phase B") */
+#define LTL_K_REHASH 6
+#define LTL_K_PURGE 7
+#define LTL_K_MISC 8        /* import / export / record fix-ups */
+#define LTL_K_COUNT 9
+
+LTL_API int ltl_abi_version(void);
+
+/* Number of CUDA devices visible, or a negative LTL_ERR_* code. */
+LTL_API int ltl_device_count(void);
+
+/* Constructor: reference _speedups.pyx:79-111 (Core.__cinit__) / kernels.py:140-172 (make_core).
+ * masks: uint64[R*W] length masks.  proj_rows/proj_offs (n_proj <= 126 pairs): gather projection
+ * (row, position).  fkp_bits: per-row prefix width of the fkp variant.  mask_k: low fingerprint bits
+ * cleared.  budget_bytes: logical budget, entry_bytes = 8*R*W + 16 (reference _speedups.pyx:100).
+ * Differences by design: no R <= 64 limit, W up to 16 words per row. */
+LTL_API int ltl_core_create(const uint64_t* masks, int R, int W, int n_pos, int err_max, int variant,
+                    const int32_t* proj_rows, const int32_t* proj_offs, int n_proj, int fkp_bits, int mask_k,
+                    uint64_t budget_bytes, int device, ltl_core** out);
+LTL_API void ltl_core_destroy(ltl_core* h);
+LTL_API const char* ltl_core_last_error(const ltl_core* h); /* h may be NULL: last create() failure */
+
+/* add_entry: reference _speedups.pyx:264-277.  *index_out = new entry index, or -1 if the fingerprint is
+ * already present.  Returns LTL_ERR_BUDGET where the reference raises CoreOOM.  No solve check. */
+LTL_API int ltl_core_add_entry(ltl_core* h, const uint64_t* cm, int op, int lhs, int rhs, int64_t* index_out);
+
+/* screen_unary / screen_binary: reference _speedups.pyx:337-355 / 357-380.  Candidates are treated
+ * strictly in enumeration order; *status is LTL_S_*; (*li, *ri) are the solving operands or -1. */
+LTL_API int ltl_core_screen_unary(ltl_core* h, int op, int64_t c0, int64_t c1, int* status, int64_t* li, int64_t* ri);
+LTL_API int ltl_core_screen_binary(ltl_core* h, int op, int64_t a0, int64_t a1, int64_t b0, int64_t b1, int tri, int* status,
+                           int64_t* li, int64_t* ri);
+
+/* One whole cost level: the segment list of reference enumerator.py:271-296 (_run_level_core) in one call.
+ * Equivalent to calling screen_* on every segment in order and stopping at the first status != DONE;
+ * *seg_index is the segment of the solving candidate (or -1). */
+LTL_API int ltl_core_run_level(ltl_core* h, const ltl_segment* segs, int n_segs, int* status, int* seg_index, int64_t* li,
+                       int64_t* ri);
+
+/* contains / fingerprint_of: reference _speedups.pyx:279-287 / 233-241 (hi has its top 2 bits clear). */
+LTL_API int ltl_core_contains(ltl_core* h, const uint64_t* cm, int* found);
+LTL_API int ltl_core_fingerprint_of(ltl_core* h, const uint64_t* cm, uint64_t* hi, uint64_t* lo);
+
+/* get_cm / get_record / export_cms: reference _speedups.pyx:117-137.  export_* copy entries
+ * [first, first + count); cms_out is uint64[count][R*W] row-major. */
+LTL_API int ltl_core_get_cm(ltl_core* h, int64_t idx, uint64_t* out);
+LTL_API int ltl_core_get_record(ltl_core* h, int64_t idx, int* op, int* lhs, int* rhs);
+LTL_API int ltl_core_export_cms(ltl_core* h, int64_t first, int64_t count, uint64_t* cms_out);
+LTL_API int ltl_core_export_records(ltl_core* h, int64_t first, int64_t count, int8_t* op, int32_t* lhs, int32_t* rhs);
+
+/* Fingerprints of stored entries [first, first + count) (set-parity checks; reference fingerprint_of over
+ * export_cms). */
+LTL_API int ltl_core_entry_fingerprints(ltl_core* h, int64_t first, int64_t count, uint64_t* hi, uint64_t* lo);
+
+/* out[0..4] = n_entries, bytes_used, offered, admitted, duplicates: reference _speedups.pyx:68, 113-115. */
+LTL_API int ltl_core_counters(ltl_core* h, uint64_t out[5]);
+
+/* Tuning / measurement (no reference counterpart).
+ * options: "chunk_candidates" (candidates per device pass), "profile" (1: time every kernel with CUDA
+ * events on the launching stream), "max_split" (cap on row splits), "force_split" (tests). */
+LTL_API int ltl_core_set_option(ltl_core* h, const char* name, int64_t value);
+/* Accumulated per kernel class since creation / the last reset: launches, device milliseconds (profile
+ * mode only), algorithmic bytes and candidates / entries processed. */
+LTL_API int ltl_core_kernel_stats(ltl_core* h, int kernel_class, uint64_t* launches, double* ms, double* alg_bytes,
+                          uint64_t* units);
+LTL_API int ltl_core_reset_kernel_stats(ltl_core* h);
+/* The CUDA stream (cudaStream_t) every kernel and copy of this handle is issued on, for CUDA-event timing. */
+LTL_API int ltl_core_stream(ltl_core* h, void** stream_out);
+/* out[0..1] = bytes copied host->device / device->host by this handle so far. */
+LTL_API int ltl_core_transfer_stats(ltl_core* h, uint64_t out[2]);
+/* out[0..5] = effective entry capacity, device bytes mapped for matrices, table slots, chunk candidates,
+ * 1 if the store uses virtual-memory growth, words per matrix */
+LTL_API int ltl_core_info(ltl_core* h, uint64_t out[6]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LTL_CORE_H */

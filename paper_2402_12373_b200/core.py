@@ -1,0 +1,306 @@
+"""ctypes face of `csrc/libltlcore.so` -- the B200 screening core behind the reference's core contract.
+
+`CudaCore` has the members of the reference's interchangeable cores (`_speedups.Core`,
+`/root/reference/pkg/src/ltllearn/_speedups.pyx:61-380`; contract `_kernels_py.py:32-281`):
+``add_entry, contains, fingerprint_of, get_cm, get_record, export_cms, screen_unary, screen_binary`` and the
+counters ``n_entries, bytes_used, offered, admitted, duplicates`` -- same argument meaning, same status
+codes, same exceptions (`ValueError` for misuse, `CoreOOM` from ``add_entry``) -- plus ``run_level``
+(one call per cost level instead of one per chunk, reference `enumerator.py:271-296`).
+`make_core` mirrors `kernels.make_core` (`kernels.py:140-172`).
+
+There is no CPU fallback: if the shared library is missing or no CUDA device is visible, `make_core`
+raises `BackendUnavailable`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from typing import Sequence
+
+import numpy as np
+
+from .errors import BackendUnavailable, CoreError, CoreOOM
+
+S_DONE, S_SOLVED, S_OOM = 0, 1, 2
+V_GATHER, V_MUELLER, V_FKP = 0, 1, 2
+MAX_WORDS_PER_ROW = 16
+
+ERR_ARG, ERR_CUDA, ERR_BUDGET, ERR_DEVICE_OOM = -1, -2, -3, -4
+KERNEL_CLASSES = ("screen", "finalize", "resolve", "scan", "emit", "materialize", "rehash", "purge", "misc")
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "csrc", "libltlcore.so")
+
+
+class Segment(C.Structure):
+    _fields_ = [("op", C.c_int32), ("tri", C.c_int32), ("a0", C.c_int64), ("a1", C.c_int64), ("b0", C.c_int64),
+                ("b1", C.c_int64)]
+
+
+_lib = None
+
+
+def load_library():
+    """Load libltlcore.so (never builds it: `python -m paper_2402_12373_b200.build` does)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise BackendUnavailable(f"{LIB_PATH} is missing: run `python -m paper_2402_12373_b200.build` "
+                                 "(there is no CPU fallback)")
+    try:
+        L = C.CDLL(LIB_PATH)
+    except OSError as exc:  # pragma: no cover
+        raise BackendUnavailable(f"cannot load {LIB_PATH}: {exc}") from None
+    u64p, i32p, i64p, ip = C.POINTER(C.c_uint64), C.POINTER(C.c_int32), C.POINTER(C.c_int64), C.POINTER(C.c_int)
+    vp = C.c_void_p
+    L.ltl_abi_version.restype = C.c_int
+    L.ltl_device_count.restype = C.c_int
+    L.ltl_core_create.argtypes = [u64p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, i32p, i32p, C.c_int, C.c_int,
+                                  C.c_int, C.c_uint64, C.c_int, C.POINTER(vp)]
+    L.ltl_core_destroy.argtypes = [vp]
+    L.ltl_core_destroy.restype = None
+    L.ltl_core_last_error.argtypes = [vp]
+    L.ltl_core_last_error.restype = C.c_char_p
+    L.ltl_core_add_entry.argtypes = [vp, u64p, C.c_int, C.c_int, C.c_int, i64p]
+    L.ltl_core_screen_unary.argtypes = [vp, C.c_int, C.c_int64, C.c_int64, ip, i64p, i64p]
+    L.ltl_core_screen_binary.argtypes = [vp, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int, ip, i64p,
+                                         i64p]
+    L.ltl_core_run_level.argtypes = [vp, C.POINTER(Segment), C.c_int, ip, ip, i64p, i64p]
+    L.ltl_core_contains.argtypes = [vp, u64p, ip]
+    L.ltl_core_fingerprint_of.argtypes = [vp, u64p, u64p, u64p]
+    L.ltl_core_get_cm.argtypes = [vp, C.c_int64, u64p]
+    L.ltl_core_get_record.argtypes = [vp, C.c_int64, ip, ip, ip]
+    L.ltl_core_export_cms.argtypes = [vp, C.c_int64, C.c_int64, u64p]
+    L.ltl_core_export_records.argtypes = [vp, C.c_int64, C.c_int64, C.POINTER(C.c_int8), i32p, i32p]
+    L.ltl_core_entry_fingerprints.argtypes = [vp, C.c_int64, C.c_int64, u64p, u64p]
+    L.ltl_core_counters.argtypes = [vp, u64p]
+    L.ltl_core_set_option.argtypes = [vp, C.c_char_p, C.c_int64]
+    L.ltl_core_kernel_stats.argtypes = [vp, C.c_int, u64p, C.POINTER(C.c_double), C.POINTER(C.c_double), u64p]
+    L.ltl_core_reset_kernel_stats.argtypes = [vp]
+    L.ltl_core_info.argtypes = [vp, u64p]
+    L.ltl_core_stream.argtypes = [vp, C.POINTER(vp)]
+    L.ltl_core_transfer_stats.argtypes = [vp, u64p]
+    for name in ("ltl_core_create", "ltl_core_add_entry", "ltl_core_screen_unary", "ltl_core_screen_binary",
+                 "ltl_core_run_level", "ltl_core_contains", "ltl_core_fingerprint_of", "ltl_core_get_cm",
+                 "ltl_core_get_record", "ltl_core_export_cms", "ltl_core_export_records",
+                 "ltl_core_entry_fingerprints", "ltl_core_counters", "ltl_core_set_option", "ltl_core_kernel_stats",
+                 "ltl_core_reset_kernel_stats", "ltl_core_info", "ltl_core_stream", "ltl_core_transfer_stats"):
+        getattr(L, name).restype = C.c_int
+    _lib = L
+    return L
+
+
+def device_count() -> int:
+    n = load_library().ltl_device_count()
+    return max(n, 0)
+
+
+def _u64(a: np.ndarray):
+    return a.ctypes.data_as(C.POINTER(C.c_uint64))
+
+
+class CudaCore:
+    """Device-resident screening core (matrices, records, uniqueness table live in HBM)."""
+
+    def __init__(self, masks, n_pos, err_max, variant, proj_rows: Sequence[int] = (), proj_offs: Sequence[int] = (),
+                 fkp_bits=0, mask_k=0, budget_bytes=2 << 30, *, words_per_row=1, device=0, chunk_candidates=None,
+                 profile=False):
+        L = load_library()
+        m = np.ascontiguousarray(masks, dtype=np.uint64).reshape(-1)
+        W = int(words_per_row)
+        if W < 1 or W > MAX_WORDS_PER_ROW:
+            raise ValueError(f"words_per_row must lie in [1, {MAX_WORDS_PER_ROW}]")
+        if len(m) == 0 or len(m) % W:
+            raise ValueError("masks length must be a positive multiple of words_per_row")
+        pr = np.ascontiguousarray(list(proj_rows), dtype=np.int32)
+        po = np.ascontiguousarray(list(proj_offs), dtype=np.int32)
+        if len(pr) != len(po):
+            raise ValueError("proj_rows and proj_offs differ in length")
+        if len(pr) > 126:
+            raise ValueError("projection wider than the fingerprint")  # reference `_speedups.pyx:92-93`
+        self.R, self.W, self.n = len(m) // W, W, len(m)
+        self._L = L
+        self._h = C.c_void_p()
+        i32p = C.POINTER(C.c_int32)
+        rc = L.ltl_core_create(_u64(m), self.R, W, int(n_pos), int(err_max), int(variant), pr.ctypes.data_as(i32p),
+                               po.ctypes.data_as(i32p), len(pr), int(fkp_bits), int(mask_k), int(budget_bytes),
+                               int(device), C.byref(self._h))
+        if rc:
+            msg = (L.ltl_core_last_error(None) or b"").decode()
+            self._h = None
+            if rc == ERR_ARG:
+                raise ValueError(msg)
+            if rc == ERR_CUDA:
+                raise BackendUnavailable(f"CUDA core unavailable: {msg} (there is no CPU fallback)")
+            raise CoreError(msg)
+        if chunk_candidates is not None:
+            self.set_option("chunk_candidates", chunk_candidates)
+        if profile:
+            self.set_option("profile", 1)
+
+    # -- lifetime ----------------------------------------------------------------------
+    def close(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            self._L.ltl_core_destroy(h)
+
+    __del__ = close
+
+    def _check(self, rc):
+        if rc == 0:
+            return
+        msg = (self._L.ltl_core_last_error(self._h) or b"").decode()
+        if rc == ERR_BUDGET:
+            raise CoreOOM(msg)
+        if rc == ERR_ARG:
+            raise ValueError(msg)
+        raise CoreError(f"[{rc}] {msg}")
+
+    def _cm(self, cm) -> np.ndarray:
+        a = np.ascontiguousarray(cm, dtype=np.uint64).reshape(-1)
+        if len(a) != self.n:
+            raise ValueError(f"expected {self.n} words, got {len(a)}")
+        return a
+
+    # -- counters ----------------------------------------------------------------------
+    def counters(self):
+        """(n_entries, bytes_used, offered, admitted, duplicates) -- reference `_speedups.pyx:68, 113-115`."""
+        out = np.zeros(5, dtype=np.uint64)
+        self._check(self._L.ltl_core_counters(self._h, _u64(out)))
+        return [int(v) for v in out]
+
+    n_entries = property(lambda s: s.counters()[0])
+    bytes_used = property(lambda s: s.counters()[1])
+    offered = property(lambda s: s.counters()[2])
+    admitted = property(lambda s: s.counters()[3])
+    duplicates = property(lambda s: s.counters()[4])
+
+    # -- contract ----------------------------------------------------------------------
+    def add_entry(self, cm, op, lhs, rhs) -> int:
+        idx = C.c_int64()
+        self._check(self._L.ltl_core_add_entry(self._h, _u64(self._cm(cm)), int(op), int(lhs), int(rhs), C.byref(idx)))
+        return int(idx.value)
+
+    def contains(self, cm) -> bool:
+        found = C.c_int()
+        self._check(self._L.ltl_core_contains(self._h, _u64(self._cm(cm)), C.byref(found)))
+        return bool(found.value)
+
+    def fingerprint_of(self, cm) -> int:
+        hi, lo = C.c_uint64(), C.c_uint64()
+        self._check(self._L.ltl_core_fingerprint_of(self._h, _u64(self._cm(cm)), C.byref(hi), C.byref(lo)))
+        return int(hi.value) << 64 | int(lo.value)
+
+    def get_cm(self, idx) -> np.ndarray:
+        out = np.empty(self.n, dtype=np.uint64)
+        rc = self._L.ltl_core_get_cm(self._h, int(idx), _u64(out))
+        if rc == ERR_ARG:
+            raise IndexError((self._L.ltl_core_last_error(self._h) or b"").decode())
+        self._check(rc)
+        return out
+
+    def get_record(self, idx):
+        op, lhs, rhs = C.c_int(), C.c_int(), C.c_int()
+        rc = self._L.ltl_core_get_record(self._h, int(idx), C.byref(op), C.byref(lhs), C.byref(rhs))
+        if rc == ERR_ARG:
+            raise IndexError((self._L.ltl_core_last_error(self._h) or b"").decode())
+        self._check(rc)
+        return op.value, lhs.value, rhs.value
+
+    def export_cms(self, first=0, count=None) -> np.ndarray:
+        n = self.n_entries
+        count = n - first if count is None else count
+        out = np.empty((count, self.n), dtype=np.uint64)
+        if count:
+            self._check(self._L.ltl_core_export_cms(self._h, int(first), int(count), _u64(out)))
+        return out
+
+    def export_records(self, first=0, count=None):
+        n = self.n_entries
+        count = n - first if count is None else count
+        op = np.empty(count, dtype=np.int8)
+        lhs = np.empty(count, dtype=np.int32)
+        rhs = np.empty(count, dtype=np.int32)
+        if count:
+            self._check(self._L.ltl_core_export_records(self._h, int(first), int(count),
+                                                        op.ctypes.data_as(C.POINTER(C.c_int8)),
+                                                        lhs.ctypes.data_as(C.POINTER(C.c_int32)),
+                                                        rhs.ctypes.data_as(C.POINTER(C.c_int32))))
+        return op, lhs, rhs
+
+    def entry_fingerprints(self, first=0, count=None):
+        n = self.n_entries
+        count = n - first if count is None else count
+        hi = np.empty(count, dtype=np.uint64)
+        lo = np.empty(count, dtype=np.uint64)
+        if count:
+            self._check(self._L.ltl_core_entry_fingerprints(self._h, int(first), int(count), _u64(hi), _u64(lo)))
+        return hi, lo
+
+    def screen_unary(self, op, c0, c1):
+        st, li, ri = C.c_int(), C.c_int64(), C.c_int64()
+        self._check(self._L.ltl_core_screen_unary(self._h, int(op), int(c0), int(c1), C.byref(st), C.byref(li),
+                                                  C.byref(ri)))
+        return st.value, li.value, ri.value
+
+    def screen_binary(self, op, a0, a1, b0, b1, tri):
+        st, li, ri = C.c_int(), C.c_int64(), C.c_int64()
+        self._check(self._L.ltl_core_screen_binary(self._h, int(op), int(a0), int(a1), int(b0), int(b1),
+                                                   int(bool(tri)), C.byref(st), C.byref(li), C.byref(ri)))
+        return st.value, li.value, ri.value
+
+    def run_level(self, segments):
+        """Screen a whole cost level.  ``segments``: iterable of objects with ``op, a0, a1, b0, b1, tri``
+        in enumeration order.  Returns ``(status, segment_index, li, ri)``."""
+        segments = list(segments)
+        arr = (Segment * max(1, len(segments)))()
+        for k, s in enumerate(segments):
+            arr[k] = Segment(int(s.op), int(bool(s.tri)), int(s.a0), int(s.a1), int(s.b0), int(s.b1))
+        st, seg, li, ri = C.c_int(), C.c_int(), C.c_int64(), C.c_int64()
+        self._check(self._L.ltl_core_run_level(self._h, arr, len(segments), C.byref(st), C.byref(seg), C.byref(li),
+                                               C.byref(ri)))
+        return st.value, seg.value, li.value, ri.value
+
+    # -- tuning / measurement ------------------------------------------------------------
+    def set_option(self, name: str, value: int):
+        self._check(self._L.ltl_core_set_option(self._h, name.encode(), int(value)))
+
+    def kernel_stats(self) -> dict:
+        out = {}
+        for k, name in enumerate(KERNEL_CLASSES):
+            launches, units = C.c_uint64(), C.c_uint64()
+            ms, nbytes = C.c_double(), C.c_double()
+            self._check(self._L.ltl_core_kernel_stats(self._h, k, C.byref(launches), C.byref(ms), C.byref(nbytes),
+                                                      C.byref(units)))
+            out[name] = {"launches": int(launches.value), "ms": float(ms.value), "alg_bytes": float(nbytes.value),
+                         "units": int(units.value)}
+        return out
+
+    def reset_kernel_stats(self):
+        self._check(self._L.ltl_core_reset_kernel_stats(self._h))
+
+    def stream_handle(self) -> int:
+        """The cudaStream_t all work of this core is issued on (for CUDA-event timing by the caller)."""
+        out = C.c_void_p()
+        self._check(self._L.ltl_core_stream(self._h, C.byref(out)))
+        return int(out.value or 0)
+
+    def transfer_stats(self) -> tuple[int, int]:
+        """(host->device bytes, device->host bytes) copied so far."""
+        out = np.zeros(2, dtype=np.uint64)
+        self._check(self._L.ltl_core_transfer_stats(self._h, _u64(out)))
+        return int(out[0]), int(out[1])
+
+    def info(self) -> dict:
+        out = np.zeros(6, dtype=np.uint64)
+        self._check(self._L.ltl_core_info(self._h, _u64(out)))
+        keys = ("capacity_entries", "matrix_bytes_mapped", "table_slots", "chunk_candidates", "vmm", "words_per_matrix")
+        return {k: int(v) for k, v in zip(keys, out)}
+
+
+def make_core(masks, n_pos, err_max, variant, proj_rows=(), proj_offs=(), fkp_bits=0, mask_k=0,
+              budget_bytes=2 << 30, *, words_per_row=1, device=0, **options) -> CudaCore:
+    """The drop-in for reference `kernels.make_core` (`kernels.py:140-172`): always the CUDA core."""
+    return CudaCore(masks, n_pos, err_max, variant, proj_rows, proj_offs, fkp_bits, mask_k, budget_bytes,
+                    words_per_row=words_per_row, device=device, **options)

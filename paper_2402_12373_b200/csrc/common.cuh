@@ -5,8 +5,7 @@
 //     group:  word k (k = row*W + w, 0 <= k < n = R*W) of entry e lives at
 //         cms[((e >> 5) * n + k) * 32 + (e & 31)]
 //     so the 32 lanes of a warp that own the 32 entries of a group read/write one aligned 256-byte
-//     line per word (fully coalesced, 8 sectors), and 4 consecutive entries' copies of one word are
-//     one aligned 32-byte sector (the left-operand register tile is one 256-bit broadcast load).
+//     line per word (fully coalesced, 8 sectors).
 //   * the uniqueness set is an open-addressing table of 32-byte slots {lo, hi, rank, pad}: one
 //     DRAM sector per probe.  key = 126-bit fingerprint (top 2 bits of hi always 0, reference
 //     kernels.py:35), EMPTY key = all ones.  rank = global enumeration rank of the candidate that
@@ -29,7 +28,10 @@ enum { MODE_INSERT = 0, MODE_FP_ONLY = 1, MODE_LOOKUP = 2 };
 #define LTL_GROUP 32
 #define LTL_NONE 0xFFFFFFFFu
 #define LTL_RANK_NONE 0xFFFFFFFFFFFFFFFFull
-#define LTL_CTA 256
+#define LTL_WARPS_PER_CTA 8
+#define LTL_CTA (32 * LTL_WARPS_PER_CTA)
+#define LTL_MAX_W 16
+#define LTL_SPLIT_ROWS 64  // row-split granularity: 64 rows = a whole number of 64-word hash blocks
 
 // fingerprint constants (reference kernels.py:28-35)
 #define K_MIX1 0xBF58476D1CE4E5B9ull
@@ -47,20 +49,32 @@ struct __align__(32) Slot {
     u64 pad;
 };
 
-// One run of candidates inside a chunk, in enumeration order (host: Chunker in core.cu).
+// One run of candidates inside a chunk, in enumeration order (host: plan_chunk in core.cu).
+//   UNARY: candidates op(i),      i in [i0, i1)                 rank = cbase + (i - i0)
+//   RECT : candidates op(i, j),   i in [i0, i1), j in [j0, j1)  rank = cbase + (i - i0)*(j1 - j0) + (j - j0)
+//   TRI  : candidates op(i, j),   i in [i0, i1), j in (i, j1)   rank = cbase + T(i - i0) + (j - i - 1),
+//          T(q) = q*m - q*(q-1)/2 with m = j1 - 1 - i0  (reference _speedups.pyx:364-368: i ascending, then j)
+// Warp tiles: 32 lanes run over one 32-entry storage group of the "lane operand" (j, or i for
+// UNARY / swapped RECT), and up to `ti` consecutive entries of the other operand are applied per lane.
 struct Piece {
     int op;
-    int kind;          // PIECE_*
-    i64 i0, i1;        // left / only operand entry range [i0, i1)
-    i64 j0, j1;        // right operand entry range [j0, j1); TRI: columns (i, j1) for row i
-    i64 cbase;         // chunk-local rank of this piece's first candidate
-    u32 tile_base;     // first CTA of this piece in the launch
-    u32 tiles_j;       // CTAs per i-tile row
-    i64 ti0, tj0;      // first i-tile index (i0 / TI) and first j group (j0 >> 5)
+    int kind;       // PIECE_*
+    int swap;       // RECT only: lanes run over the left operand i, row tiles over j
+    int ti;         // max rows per warp tile (1..4)
+    int seg;        // index of the caller's segment this piece belongs to
+    int pad;
+    i64 i0, i1;
+    i64 j0, j1;
+    i64 cbase;      // chunk-local rank of this piece's first candidate
+    i64 count;      // candidates in this piece
+    i64 tile_base;  // first warp tile of this piece in the launch
+    i64 tiles_lane; // lane groups spanned
+    i64 lane_g0;    // first lane group (entry index >> 5)
 };
 
-// One deposit of the "bits" fingerprints (gather / fkp): take ((word[k] >> rsh) & mask) and OR it
+// One deposit of the "bits" fingerprints (gather / fkp): take ((word[k] >> rsh) & mask) and add it
 // into the 128-bit fingerprint at bit position pos (reference _speedups.pyx:188-195, 205-222).
+// Deposits target disjoint bit ranges, so integer addition == bitwise or.
 struct Deposit {
     u32 k;
     u32 rsh;
@@ -71,37 +85,48 @@ struct Deposit {
 
 // Device-resident control block of one chunk.
 struct Ctl {
-    u64 solver_c;   // min chunk-local rank whose error count <= err_max (atomicMin), ~0 if none
-    u64 oom_c;      // chunk-local rank of the first new unique that does not fit the budget, ~0 if none
-    u64 total;      // winners below the cutoff
+    u64 solver_c;      // min chunk-local rank whose error count <= err_max (atomicMin), ~0 if none
+    u64 oom_c;         // chunk-local rank of the first new unique that does not fit the budget, ~0 if none
+    u64 total;         // winners below the solver cutoff
     u64 fp_hi, fp_lo;  // MODE_FP_ONLY / MODE_LOOKUP result for single-candidate queries
     u64 found;
     u64 pad[2];
 };
 
 struct ScreenParams {
-    const u64* cms;       // entry store (group layout)
-    const u64* masks;     // n words
+    const u64* cms;  // entry store (group layout)
+    const u64* masks;  // n words
     const Piece* pieces;
     int n_pieces;
     int R, W, n_pos, err_max;
-    i64 n;                // words per entry
+    i64 n;  // words per entry
+    i64 total_tiles;
+    int nsplit;        // row splits (gridDim.y); > 1 => partial sums go to acc_*, k_finalize completes
+    int rows_per_split;  // multiple of LTL_SPLIT_ROWS
     int variant, mask_k, n_dep;
     const Deposit* deps;
     int mode, check_solve;
     Slot* table;
     u64 table_mask;
-    u64 gbase;            // global rank of chunk-local rank 0
-    u32* slot;            // per candidate: contender slot / NONE   (phase A out, resolve in/out)
-    u64* fp_out;          // MODE_FP_ONLY: 2 words per candidate (hi, lo), may be null
+    u64 gbase;  // global rank of chunk-local rank 0
+    u32* slot;  // per candidate: contender slot / NONE
+    u64* fp_out;  // MODE_FP_ONLY: 2 words per candidate (hi, lo)
+    u64* acc_s0;  // nsplit > 1: per-candidate partial sums
+    u64* acc_s1;
+    u32* acc_err;
     Ctl* ctl;
-    // phase B
-    u64* cms_out;         // same buffer as cms (entries >= n_base are written)
-    i64 n_base;           // entry index of destination 0
-    unsigned char* rec_op;
-    int* rec_lhs;
-    int* rec_rhs;
-    u64 cutoff;           // candidates with chunk-local rank >= cutoff are ignored
+};
+
+struct MaterializeParams {
+    u64* cms;  // reads entries < n_base, writes entries [n_base, n_base + count)
+    const u64* masks;
+    int R, W;
+    i64 n;
+    i64 n_base, count;
+    const unsigned char* rec_op;
+    const int* rec_lhs;
+    const int* rec_rhs;
+    int nsplit, rows_per_split;
 };
 
 __host__ __device__ __forceinline__ u64 mix64(u64 x) {  // reference kernels.py:50-57
@@ -116,6 +141,9 @@ __host__ __device__ __forceinline__ u64 mix64(u64 x) {  // reference kernels.py:
 __host__ __device__ __forceinline__ size_t cm_index(i64 e, i64 n, i64 k) {
     return ((size_t)(e >> 5) * (size_t)n + (size_t)k) * LTL_GROUP + (size_t)(e & 31);
 }
+
+// T(q) of the TRI rank formula.
+__host__ __device__ __forceinline__ u64 tri_before(u64 q, u64 m) { return q * m - ((q * (q - 1)) >> 1); }
 
 #ifdef __CUDACC__
 // ---- 128-bit key helpers -----------------------------------------------------------------
@@ -178,4 +206,6 @@ __device__ __forceinline__ u64 ld_rank(const Slot* s) {
     asm volatile("ld.global.cg.u64 %0, [%1];" : "=l"(r) : "l"(&s->rank) : "memory");
     return r;
 }
+
+__device__ __forceinline__ u64 ld_nc(const u64* p) { return __ldg(p); }
 #endif

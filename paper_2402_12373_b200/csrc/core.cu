@@ -1,0 +1,1359 @@
+// core.cu -- host side of the B200 screening core + the small bookkeeping kernels + the C ABI
+// (include/ltl_core.h).  The two hot kernels live in screen.cuh.
+//
+// One "chunk" (<= chunk_candidates candidates, consecutive in enumeration order) runs as
+//   k_screen      every candidate: evaluate, count errors, fingerprint, claim its table slot with
+//                 atomicMin(rank)                                   (reference _speedups.pyx:364-379)
+//   k_resolve     a candidate is admitted iff its rank is the one left in the slot  (first-wins)
+//   k_scan/k_emit ordered compaction: winners get consecutive entry indices in rank order and their
+//                 (op, lhs, rhs) records                            (reference _speedups.pyx:255-262)
+//   k_materialize winners' matrices are re-evaluated and appended to the store
+// so that entry order, records and counters equal the sequential reference's.
+#include <cuda.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/ltl_core.h"
+#include "screen.cuh"
+
+// ------------------------------------------------------------------------------------------------
+// per-W launchers (screen_inst.cu)
+
+#define LTL_DECL_W(N)                                                                                  \
+    extern "C" void ltl_launch_screen_w##N(const ScreenParams&, bool, dim3, cudaStream_t);             \
+    extern "C" void ltl_launch_materialize_w##N(const MaterializeParams&, dim3, cudaStream_t);
+LTL_DECL_W(1) LTL_DECL_W(2) LTL_DECL_W(3) LTL_DECL_W(4) LTL_DECL_W(5) LTL_DECL_W(6) LTL_DECL_W(7) LTL_DECL_W(8)
+LTL_DECL_W(9) LTL_DECL_W(10) LTL_DECL_W(11) LTL_DECL_W(12) LTL_DECL_W(13) LTL_DECL_W(14) LTL_DECL_W(15) LTL_DECL_W(16)
+#undef LTL_DECL_W
+
+static const screen_launch_fn SCREEN_FN[LTL_MAX_W + 1] = {
+    nullptr, ltl_launch_screen_w1, ltl_launch_screen_w2, ltl_launch_screen_w3, ltl_launch_screen_w4,
+    ltl_launch_screen_w5, ltl_launch_screen_w6, ltl_launch_screen_w7, ltl_launch_screen_w8, ltl_launch_screen_w9,
+    ltl_launch_screen_w10, ltl_launch_screen_w11, ltl_launch_screen_w12, ltl_launch_screen_w13,
+    ltl_launch_screen_w14, ltl_launch_screen_w15, ltl_launch_screen_w16};
+static const materialize_launch_fn MATERIALIZE_FN[LTL_MAX_W + 1] = {
+    nullptr, ltl_launch_materialize_w1, ltl_launch_materialize_w2, ltl_launch_materialize_w3,
+    ltl_launch_materialize_w4, ltl_launch_materialize_w5, ltl_launch_materialize_w6, ltl_launch_materialize_w7,
+    ltl_launch_materialize_w8, ltl_launch_materialize_w9, ltl_launch_materialize_w10, ltl_launch_materialize_w11,
+    ltl_launch_materialize_w12, ltl_launch_materialize_w13, ltl_launch_materialize_w14, ltl_launch_materialize_w15,
+    ltl_launch_materialize_w16};
+
+// ------------------------------------------------------------------------------------------------
+// bookkeeping kernels
+
+#define RES_CTA 1024
+
+template <bool MUELLER>
+__global__ void k_finalize(const __grid_constant__ ScreenParams p, u64 total) {
+    u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (c >= total) return;
+    finish_candidate<MUELLER>(p, c, p.acc_s0[c], p.acc_s1[c], p.acc_err[c]);
+}
+
+// winner flags (one bit per candidate) + winners per 1024-candidate block
+__global__ void __launch_bounds__(RES_CTA) k_resolve(const u32* __restrict__ slot, const Slot* __restrict__ table,
+                                                     u64 gbase, u64 total, const Ctl* __restrict__ ctl,
+                                                     u32* __restrict__ flagw, u32* __restrict__ blocksum) {
+    __shared__ u32 cnt;
+    const u64 limit = min(total, ctl->solver_c);  // nothing at or above the first solver is admitted
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    const u64 c = (u64)blockIdx.x * RES_CTA + threadIdx.x;
+    bool win = false;
+    if (c < limit) {
+        u32 s = slot[c];
+        if (s != LTL_NONE) win = ld_rank(table + s) == gbase + c;
+    }
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, win);
+    if ((threadIdx.x & 31) == 0) {
+        flagw[c >> 5] = b;
+        if (b) atomicAdd(&cnt, __popc(b));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) blocksum[blockIdx.x] = cnt;
+}
+
+// exclusive scan of the block sums (single CTA) -> blockoff, ctl->total
+__global__ void __launch_bounds__(1024) k_scan(const u32* __restrict__ blocksum, u32 nb, u64* __restrict__ blockoff,
+                                               Ctl* ctl) {
+    __shared__ u64 wsum[32];
+    __shared__ u64 carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (u32 base = 0; base < nb; base += 1024) {
+        const u32 idx = base + threadIdx.x;
+        const u64 v = idx < nb ? blocksum[idx] : 0;
+        u64 x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            u64 y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            u64 w = wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                u64 y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+                if (lane >= o) w += y;
+            }
+            wsum[lane] = w;  // inclusive over warps
+        }
+        __syncthreads();
+        const u64 before = carry + (warp ? wsum[warp - 1] : 0) + (x - v);
+        if (idx < nb) blockoff[idx] = before;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = before + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) ctl->total = carry;
+}
+
+// winners (in rank order) -> records at entry n_base + dest; the first winner beyond the budget marks OOM
+__global__ void __launch_bounds__(RES_CTA) k_emit(const u32* __restrict__ flagw, const u64* __restrict__ blockoff,
+                                                  const Piece* __restrict__ pieces, int n_pieces, u64 total, i64 n_base,
+                                                  u64 cap_left, unsigned char* __restrict__ rec_op,
+                                                  int* __restrict__ rec_lhs, int* __restrict__ rec_rhs, Ctl* ctl) {
+    __shared__ u32 wcnt[32];
+    const u64 limit = min(total, ctl->solver_c);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const u64 c = (u64)blockIdx.x * RES_CTA + threadIdx.x;
+    const u32 fw = flagw[c >> 5];
+    if (lane == 0) wcnt[warp] = __popc(fw);
+    __syncthreads();
+    if (!((fw >> lane) & 1u) || c >= limit) return;
+    u64 dest = blockoff[blockIdx.x] + __popc(fw & ((1u << lane) - 1u));
+    for (int w = 0; w < warp; w++) dest += wcnt[w];
+    if (dest > cap_left) return;
+    if (dest == cap_left) {
+        ctl->oom_c = c;
+        return;
+    }
+    int lo = 0, hi = n_pieces - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if ((u64)pieces[mid].cbase <= c) lo = mid;
+        else hi = mid - 1;
+    }
+    const Piece pc = pieces[lo];
+    i64 i, j;
+    piece_unrank(pc, c, &i, &j);
+    const i64 e = n_base + (i64)dest;
+    rec_op[e] = (unsigned char)pc.op;
+    rec_lhs[e] = (int)i;
+    rec_rhs[e] = (int)j;
+}
+
+__global__ void k_import(const u64* __restrict__ stage, u64* __restrict__ cms, i64 e, i64 n) {
+    i64 k = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k < n) cms[cm_index(e, n, k)] = stage[k];
+}
+
+// out[(e - first) * n + k] for entries [first, first + count)
+__global__ void k_export(const u64* __restrict__ cms, i64 first, i64 count, i64 n, u64* __restrict__ out) {
+    const i64 g0 = first >> 5;
+    const i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    const i64 lane = t & 31;
+    const i64 gk = t >> 5;
+    const i64 g = gk / n, k = gk - g * n;
+    const i64 e = (g0 + g) * 32 + lane;
+    if (e >= first && e < first + count) out[(size_t)(e - first) * n + k] = cms[cm_index(e, n, k)];
+}
+
+__global__ void k_set_record(unsigned char* rec_op, int* rec_lhs, int* rec_rhs, i64 e, int op, int lhs, int rhs) {
+    rec_op[e] = (unsigned char)op;
+    rec_lhs[e] = lhs;
+    rec_rhs[e] = rhs;
+}
+
+__global__ void k_rehash(const Slot* __restrict__ old, u64 old_cap, Slot* __restrict__ fresh, u64 fresh_mask) {
+    u64 s = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= old_cap) return;
+    const Key128 k = ld_key(old + s);
+    if (k.hi == ~0ull) return;
+    u64 d = table_find_or_claim(fresh, fresh_mask, k.hi, k.lo);
+    fresh[d].rank = old[s].rank;
+}
+
+// after a solve / OOM cut: keys filed by candidates at or above the cut are not members
+__global__ void k_purge(Slot* table, u64 cap, u64 gcut) {
+    u64 s = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= cap) return;
+    if (table[s].hi == ~0ull) return;
+    u64 r = table[s].rank;
+    if (r != LTL_RANK_NONE && r >= gcut) table[s].rank = LTL_RANK_NONE;
+}
+
+// ------------------------------------------------------------------------------------------------
+// driver API (virtual memory management) through the runtime's entry-point lookup: no link-time libcuda
+
+struct DriverApi {
+    bool tried = false, ok = false;
+    CUresult (*MemAddressReserve)(CUdeviceptr*, size_t, size_t, CUdeviceptr, unsigned long long) = nullptr;
+    CUresult (*MemAddressFree)(CUdeviceptr, size_t) = nullptr;
+    CUresult (*MemCreate)(CUmemGenericAllocationHandle*, size_t, const CUmemAllocationProp*, unsigned long long) = nullptr;
+    CUresult (*MemRelease)(CUmemGenericAllocationHandle) = nullptr;
+    CUresult (*MemMap)(CUdeviceptr, size_t, size_t, CUmemGenericAllocationHandle, unsigned long long) = nullptr;
+    CUresult (*MemUnmap)(CUdeviceptr, size_t) = nullptr;
+    CUresult (*MemSetAccess)(CUdeviceptr, size_t, const CUmemAccessDesc*, size_t) = nullptr;
+    CUresult (*MemGetAllocationGranularity)(size_t*, const CUmemAllocationProp*, CUmemAllocationGranularity_flags) = nullptr;
+};
+
+static DriverApi& drv() {
+    static DriverApi d;
+    if (d.tried) return d;
+    d.tried = true;
+    if (getenv("LTL_NO_VMM")) return d;
+    bool ok = true;
+    auto get = [&](const char* name, void** fn) {
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess ||
+            !*fn)
+            ok = false;
+    };
+    get("cuMemAddressReserve", (void**)&d.MemAddressReserve);
+    get("cuMemAddressFree", (void**)&d.MemAddressFree);
+    get("cuMemCreate", (void**)&d.MemCreate);
+    get("cuMemRelease", (void**)&d.MemRelease);
+    get("cuMemMap", (void**)&d.MemMap);
+    get("cuMemUnmap", (void**)&d.MemUnmap);
+    get("cuMemSetAccess", (void**)&d.MemSetAccess);
+    get("cuMemGetAllocationGranularity", (void**)&d.MemGetAllocationGranularity);
+    cudaGetLastError();
+    d.ok = ok;
+    return d;
+}
+
+// A device buffer that grows in place: a reserved virtual range, physical memory mapped on demand
+// (180 GB of HBM is filled without ever copying the store).  Falls back to malloc + copy without VMM.
+struct GrowBuf {
+    char* base = nullptr;
+    size_t reserved = 0, mapped = 0, gran = 0;
+    bool vmm = false;
+    int device = 0;
+    std::vector<std::pair<CUmemGenericAllocationHandle, size_t>> parts;
+
+    int init(int dev, size_t max_bytes) {
+        device = dev;
+        DriverApi& d = drv();
+        if (d.ok) {
+            CUmemAllocationProp prop;
+            memset(&prop, 0, sizeof(prop));
+            prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+            prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+            prop.location.id = dev;
+            if (d.MemGetAllocationGranularity(&gran, &prop, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) == CUDA_SUCCESS && gran) {
+                size_t want = ((max_bytes + gran - 1) / gran) * gran;
+                if (want < gran) want = gran;
+                CUdeviceptr p = 0;
+                if (d.MemAddressReserve(&p, want, 0, 0, 0) == CUDA_SUCCESS) {
+                    base = (char*)p;
+                    reserved = want;
+                    vmm = true;
+                    return 0;
+                }
+            }
+        }
+        vmm = false;
+        reserved = max_bytes;
+        return 0;
+    }
+
+    // 0 ok, -1 device out of memory / failure
+    int ensure(size_t bytes, cudaStream_t stream) {
+        if (bytes <= mapped) return 0;
+        if (bytes > reserved) return -1;
+        if (vmm) {
+            DriverApi& d = drv();
+            size_t step = std::max(mapped / 4, (size_t)(64u << 20));
+            size_t target = std::max(bytes, std::min(reserved, mapped + step));
+            target = std::min(reserved, ((target + gran - 1) / gran) * gran);
+            for (int attempt = 0; attempt < 2; attempt++) {
+                size_t add = target - mapped;
+                CUmemAllocationProp prop;
+                memset(&prop, 0, sizeof(prop));
+                prop.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+                prop.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+                prop.location.id = device;
+                CUmemGenericAllocationHandle hnd;
+                if (d.MemCreate(&hnd, add, &prop, 0) == CUDA_SUCCESS) {
+                    if (d.MemMap((CUdeviceptr)(base + mapped), add, 0, hnd, 0) != CUDA_SUCCESS) {
+                        d.MemRelease(hnd);
+                        return -1;
+                    }
+                    CUmemAccessDesc acc;
+                    memset(&acc, 0, sizeof(acc));
+                    acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+                    acc.location.id = device;
+                    acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+                    if (d.MemSetAccess((CUdeviceptr)(base + mapped), add, &acc, 1) != CUDA_SUCCESS) {
+                        d.MemUnmap((CUdeviceptr)(base + mapped), add);
+                        d.MemRelease(hnd);
+                        return -1;
+                    }
+                    parts.push_back({hnd, add});
+                    mapped = target;
+                    return 0;
+                }
+                // retry with exactly what is needed
+                target = std::min(reserved, ((bytes + gran - 1) / gran) * gran);
+                if (target <= mapped) return -1;
+            }
+            return -1;
+        }
+        size_t target = std::min(reserved, std::max(bytes, std::max(mapped * 2, (size_t)(1u << 20))));
+        char* fresh = nullptr;
+        if (cudaMalloc(&fresh, target) != cudaSuccess) {
+            cudaGetLastError();
+            target = bytes;
+            if (cudaMalloc(&fresh, target) != cudaSuccess) {
+                cudaGetLastError();
+                return -1;
+            }
+        }
+        if (base) {
+            cudaMemcpyAsync(fresh, base, mapped, cudaMemcpyDeviceToDevice, stream);
+            cudaStreamSynchronize(stream);
+            cudaFree(base);
+        }
+        base = fresh;
+        mapped = target;
+        return 0;
+    }
+
+    void release() {
+        if (vmm) {
+            DriverApi& d = drv();
+            size_t off = 0;
+            for (auto& pr : parts) {
+                d.MemUnmap((CUdeviceptr)(base + off), pr.second);
+                d.MemRelease(pr.first);
+                off += pr.second;
+            }
+            parts.clear();
+            if (base) d.MemAddressFree((CUdeviceptr)base, reserved);
+        } else if (base) {
+            cudaFree(base);
+        }
+        base = nullptr;
+        mapped = reserved = 0;
+    }
+};
+
+// ------------------------------------------------------------------------------------------------
+// the core object
+
+struct KStat {
+    u64 launches = 0, units = 0;
+    double ms = 0, bytes = 0;
+};
+
+struct PendingEvent {
+    int cls;
+    cudaEvent_t a, b;
+};
+
+// a unit of enumeration before chunking
+struct Unit {
+    int kind, op, seg;
+    i64 i0, i1, j0, j1;
+};
+
+static thread_local std::string g_create_error;
+
+struct ltl_core {
+    int device = 0, R = 0, W = 0, n_pos = 0, err_max = 0, variant = 0, fkp_bits = 0, mask_k = 0;
+    i64 n = 0;
+    u64 budget = 0, entry_bytes = 0;
+    u64 cap_entries = 0;  // admissions allowed: min(logical budget, what the device can hold)
+    cudaStream_t stream = nullptr;
+    u64* d_masks = nullptr;
+    Deposit* d_deps = nullptr;
+    int n_dep = 0;
+    GrowBuf cms, rec_op, rec_lhs, rec_rhs;
+    Slot* table = nullptr;
+    u64 table_cap = 0, keys_upper = 0;
+    i64 chunk_cap = 1 << 24;
+    i64 scratch_cap = 0;
+    u32* d_slot = nullptr;
+    u32* d_flagw = nullptr;
+    u32* d_blocksum = nullptr;
+    u64* d_blockoff = nullptr;
+    u64 *d_acc_s0 = nullptr, *d_acc_s1 = nullptr;
+    u32* d_acc_err = nullptr;
+    i64 acc_cap = 0;
+    u64* d_fp = nullptr;
+    i64 fp_cap = 0;
+    Piece* d_pieces = nullptr;
+    Piece* h_pieces = nullptr;
+    int pieces_cap = 0;
+    Ctl* d_ctl = nullptr;
+    Ctl* h_ctl = nullptr;
+    u64* d_stage = nullptr;
+    u64* h_stage = nullptr;  // pinned, n words
+    u64 n_entries = 0, offered = 0, admitted = 0, duplicates = 0;
+    u64 h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic of this handle
+    int sm_count = 148;
+    int max_split = 4096, force_split = 0;
+    bool profile = false;
+    KStat stats[LTL_K_COUNT];
+    std::vector<PendingEvent> pending;
+    std::vector<cudaEvent_t> event_pool;
+    std::string err;
+
+    int fail(int code, const std::string& msg) {
+        err = msg;
+        return code;
+    }
+    int cuda_fail(cudaError_t e, const char* what) {
+        err = std::string(what) + ": " + cudaGetErrorString(e);
+        cudaGetLastError();
+        return LTL_ERR_CUDA;
+    }
+};
+
+#define CK(call)                                        \
+    do {                                                \
+        cudaError_t e_ = (call);                        \
+        if (e_ != cudaSuccess) return h->cuda_fail(e_, #call); \
+    } while (0)
+
+static cudaEvent_t get_event(ltl_core* h) {
+    if (!h->event_pool.empty()) {
+        cudaEvent_t e = h->event_pool.back();
+        h->event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+struct ScopedTimer {
+    ltl_core* h;
+    int cls;
+    cudaEvent_t a = nullptr, b = nullptr;
+    ScopedTimer(ltl_core* h_, int cls_, u64 units, double bytes) : h(h_), cls(cls_) {
+        h->stats[cls].launches++;
+        h->stats[cls].units += units;
+        h->stats[cls].bytes += bytes;
+        if (h->profile) {
+            a = get_event(h);
+            b = get_event(h);
+            cudaEventRecord(a, h->stream);
+        }
+    }
+    ~ScopedTimer() {
+        if (a) {
+            cudaEventRecord(b, h->stream);
+            h->pending.push_back({cls, a, b});
+        }
+    }
+};
+
+static void drain_events(ltl_core* h) {  // stream must be idle
+    for (auto& pe : h->pending) {
+        float ms = 0;
+        if (cudaEventElapsedTime(&ms, pe.a, pe.b) == cudaSuccess) h->stats[pe.cls].ms += ms;
+        h->event_pool.push_back(pe.a);
+        h->event_pool.push_back(pe.b);
+    }
+    h->pending.clear();
+    cudaGetLastError();
+}
+
+static int ensure_table(ltl_core* h, u64 need_keys) {
+    u64 want = 1u << 16;
+    while (want < need_keys * 2) want <<= 1;
+    if (want <= h->table_cap) return LTL_OK;
+    if (want > (1ull << 31)) return h->fail(LTL_ERR_DEVICE_OOM, "uniqueness table would exceed 2^31 slots");
+    Slot* fresh = nullptr;
+    if (cudaMalloc(&fresh, want * sizeof(Slot)) != cudaSuccess) {
+        cudaGetLastError();
+        return h->fail(LTL_ERR_DEVICE_OOM, "device memory exhausted growing the uniqueness table");
+    }
+    CK(cudaMemsetAsync(fresh, 0xFF, want * sizeof(Slot), h->stream));
+    if (h->table) {
+        {
+            ScopedTimer t(h, LTL_K_REHASH, h->table_cap, (double)h->table_cap * sizeof(Slot));
+            k_rehash<<<(unsigned)((h->table_cap + 255) / 256), 256, 0, h->stream>>>(h->table, h->table_cap, fresh, want - 1);
+        }
+        CK(cudaStreamSynchronize(h->stream));
+        drain_events(h);
+        cudaFree(h->table);
+    }
+    h->table = fresh;
+    h->table_cap = want;
+    return LTL_OK;
+}
+
+static int ensure_scratch(ltl_core* h, i64 total) {
+    if (total <= h->scratch_cap) return LTL_OK;
+    i64 cap = std::max<i64>(total, std::min<i64>(h->chunk_cap, std::max<i64>(h->scratch_cap * 4, 1 << 16)));
+    cap = ((cap + RES_CTA - 1) / RES_CTA) * RES_CTA;
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(h->d_slot);
+    cudaFree(h->d_flagw);
+    cudaFree(h->d_blocksum);
+    cudaFree(h->d_blockoff);
+    h->d_slot = nullptr;
+    h->d_flagw = h->d_blocksum = nullptr;
+    h->d_blockoff = nullptr;
+    h->scratch_cap = 0;
+    CK(cudaMalloc(&h->d_slot, (size_t)cap * 4));
+    CK(cudaMalloc(&h->d_flagw, (size_t)(cap / 32) * 4));
+    CK(cudaMalloc(&h->d_blocksum, (size_t)(cap / RES_CTA) * 4));
+    CK(cudaMalloc(&h->d_blockoff, (size_t)(cap / RES_CTA) * 8));
+    h->scratch_cap = cap;
+    return LTL_OK;
+}
+
+static int ensure_acc(ltl_core* h, i64 total) {
+    if (total <= h->acc_cap) return LTL_OK;
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(h->d_acc_s0);
+    cudaFree(h->d_acc_s1);
+    cudaFree(h->d_acc_err);
+    h->d_acc_s0 = h->d_acc_s1 = nullptr;
+    h->d_acc_err = nullptr;
+    h->acc_cap = 0;
+    i64 cap = std::max<i64>(total, 1 << 12);
+    CK(cudaMalloc(&h->d_acc_s0, (size_t)cap * 8));
+    CK(cudaMalloc(&h->d_acc_s1, (size_t)cap * 8));
+    CK(cudaMalloc(&h->d_acc_err, (size_t)cap * 4));
+    h->acc_cap = cap;
+    return LTL_OK;
+}
+
+static int ensure_pieces(ltl_core* h, int n) {
+    if (n <= h->pieces_cap) return LTL_OK;
+    int cap = std::max(n, std::max(64, h->pieces_cap * 2));
+    CK(cudaStreamSynchronize(h->stream));
+    cudaFree(h->d_pieces);
+    cudaFreeHost(h->h_pieces);
+    h->d_pieces = h->h_pieces = nullptr;
+    h->pieces_cap = 0;
+    CK(cudaMalloc(&h->d_pieces, sizeof(Piece) * cap));
+    CK(cudaMallocHost(&h->h_pieces, sizeof(Piece) * cap));
+    h->pieces_cap = cap;
+    return LTL_OK;
+}
+
+static int ensure_entries(ltl_core* h, u64 entries) {  // matrices + records for `entries` entries
+    const u64 groups = (entries + 31) / 32;
+    if (h->cms.ensure((size_t)groups * 32 * (size_t)h->n * 8, h->stream) || h->rec_op.ensure((size_t)groups * 32, h->stream) ||
+        h->rec_lhs.ensure((size_t)groups * 32 * 4, h->stream) || h->rec_rhs.ensure((size_t)groups * 32 * 4, h->stream)) {
+        cudaGetLastError();
+        return h->fail(LTL_ERR_DEVICE_OOM, "device memory exhausted growing the entry store");
+    }
+    return LTL_OK;
+}
+
+static int ensure_records(ltl_core* h, u64 entries) {
+    const u64 groups = (entries + 31) / 32;
+    if (h->rec_op.ensure((size_t)groups * 32, h->stream) || h->rec_lhs.ensure((size_t)groups * 32 * 4, h->stream) ||
+        h->rec_rhs.ensure((size_t)groups * 32 * 4, h->stream)) {
+        cudaGetLastError();
+        return h->fail(LTL_ERR_DEVICE_OOM, "device memory exhausted growing the record store");
+    }
+    return LTL_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// chunk planning
+
+static inline bool is_binary(int op) { return op == OP_AND || op == OP_OR || op == OP_UNTIL; }
+
+static void push_piece(ltl_core* h, std::vector<Piece>& pieces, i64& total, i64& tiles, const Unit& u, i64 i0, i64 i1,
+                       i64 j0, i64 j1, int kind) {
+    Piece p;
+    memset(&p, 0, sizeof(p));
+    p.op = u.op;
+    p.kind = kind;
+    p.seg = u.seg;
+    p.i0 = i0;
+    p.i1 = i1;
+    p.j0 = j0;
+    p.j1 = j1;
+    p.swap = 0;
+    p.ti = 1;
+    i64 lane_lo, lane_hi, rows;
+    if (kind == PIECE_UNARY) {
+        p.count = i1 - i0;
+        lane_lo = i0;
+        lane_hi = i1;
+        rows = 1;
+    } else if (kind == PIECE_RECT) {
+        p.count = (i1 - i0) * (j1 - j0);
+        p.swap = (i1 - i0) > (j1 - j0) ? 1 : 0;
+        lane_lo = p.swap ? i0 : j0;
+        lane_hi = p.swap ? i1 : j1;
+        rows = p.swap ? (j1 - j0) : (i1 - i0);
+    } else {
+        p.count = (i64)tri_before((u64)(i1 - i0), (u64)(j1 - 1 - i0));
+        lane_lo = i0 + 1;
+        lane_hi = j1;
+        rows = i1 - i0;
+    }
+    if (kind != PIECE_UNARY && h->W == 1 && h->variant == VAR_MUELLER) p.ti = 4;
+    p.lane_g0 = lane_lo >> 5;
+    p.tiles_lane = ((lane_hi - 1) >> 5) - p.lane_g0 + 1;
+    const i64 row_tiles = (rows + p.ti - 1) / p.ti;
+    p.cbase = total;
+    p.tile_base = tiles;
+    total += p.count;
+    tiles += row_tiles * p.tiles_lane;
+    pieces.push_back(p);
+}
+
+// Expand caller segments into rectangular / triangular / unary units (reference _speedups.pyx:364-368:
+// for row i the columns start at max(b0, i + 1) when tri).
+static int expand_segments(ltl_core* h, const ltl_segment* segs, int n_segs, std::vector<Unit>& units) {
+    const i64 ne = (i64)h->n_entries;
+    for (int s = 0; s < n_segs; s++) {
+        const ltl_segment& g = segs[s];
+        const bool unary = g.op == OP_NOT || g.op == OP_NEXT || g.op == OP_FINALLY || g.op == OP_GLOBALLY;
+        if (!unary && !is_binary(g.op)) return h->fail(LTL_ERR_ARG, "segment: unknown opcode");
+        if (g.a0 < 0 || g.a1 > ne || g.a0 > g.a1) return h->fail(LTL_ERR_ARG, "segment: left range outside the store");
+        if (unary) {
+            if (g.a1 > g.a0) units.push_back({PIECE_UNARY, g.op, s, g.a0, g.a1, -1, -1});
+            continue;
+        }
+        if (g.b0 < 0 || g.b1 > ne || g.b0 > g.b1) return h->fail(LTL_ERR_ARG, "segment: right range outside the store");
+        if (g.a1 == g.a0 || g.b1 == g.b0) continue;
+        if (!g.tri) {
+            units.push_back({PIECE_RECT, g.op, s, g.a0, g.a1, g.b0, g.b1});
+            continue;
+        }
+        const i64 rect_end = std::min(g.a1, g.b0);  // rows i < b0 see the whole right range
+        if (g.a0 < rect_end) units.push_back({PIECE_RECT, g.op, s, g.a0, rect_end, g.b0, g.b1});
+        const i64 t0 = std::max(g.a0, g.b0), t1 = std::min(g.a1, g.b1 - 1);  // row b1-1 has no column left
+        if (t0 < t1) units.push_back({PIECE_TRI, g.op, s, t0, t1, -1, g.b1});
+    }
+    return LTL_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// one chunk
+
+struct ChunkOut {
+    int status = LTL_S_DONE;
+    u64 cut_c = ~0ull;  // chunk-local rank of the solving / overflowing candidate
+    u64 admitted = 0;
+};
+
+static void choose_split(ltl_core* h, i64 tiles, int* nsplit, int* rows_per_split) {
+    int ns = 1;
+    const i64 target = (i64)h->sm_count * 16;  // warps wanted in flight
+    if (h->force_split > 0) ns = h->force_split;
+    else if (tiles < target && h->R >= 2 * LTL_SPLIT_ROWS) ns = (int)std::min<i64>((target + tiles - 1) / tiles, h->max_split);
+    const int max_ns = (h->R + LTL_SPLIT_ROWS - 1) / LTL_SPLIT_ROWS;
+    ns = std::max(1, std::min(ns, max_ns));
+    int rps = (h->R + ns - 1) / ns;
+    rps = ((rps + LTL_SPLIT_ROWS - 1) / LTL_SPLIT_ROWS) * LTL_SPLIT_ROWS;
+    *rows_per_split = rps;
+    *nsplit = (h->R + rps - 1) / rps;
+}
+
+static double screen_bytes(ltl_core* h, const std::vector<Piece>& pieces) {
+    double b = 0;
+    const double B = 8.0 * (double)h->n;
+    for (auto& p : pieces) b += (double)p.count * ((p.kind == PIECE_UNARY ? 1.0 : 2.0) * B + 16.0);
+    return b;
+}
+
+static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 tiles, int mode, bool check_solve,
+                     bool materialize, ChunkOut* out) {
+    int rc;
+    if (total <= 0) return LTL_OK;
+    if (mode == MODE_INSERT) {
+        if ((rc = ensure_table(h, h->keys_upper + (u64)total))) return rc;
+        if ((rc = ensure_scratch(h, total))) return rc;
+        const u64 room = h->cap_entries > h->n_entries ? h->cap_entries - h->n_entries : 0;
+        if ((rc = ensure_records(h, h->n_entries + std::min<u64>((u64)total, room) + 1))) return rc;
+    }
+    if ((rc = ensure_pieces(h, (int)pieces.size()))) return rc;
+    memcpy(h->h_pieces, pieces.data(), sizeof(Piece) * pieces.size());
+    CK(cudaMemcpyAsync(h->d_pieces, h->h_pieces, sizeof(Piece) * pieces.size(), cudaMemcpyHostToDevice, h->stream));
+    h->h2d_bytes += sizeof(Piece) * pieces.size();
+    CK(cudaMemsetAsync(h->d_ctl, 0xFF, 2 * sizeof(u64), h->stream));  // solver_c = oom_c = none
+    CK(cudaMemsetAsync((char*)h->d_ctl + 2 * sizeof(u64), 0, sizeof(Ctl) - 2 * sizeof(u64), h->stream));
+
+    ScreenParams p;
+    memset(&p, 0, sizeof(p));
+    p.cms = (const u64*)h->cms.base;
+    p.masks = h->d_masks;
+    p.pieces = h->d_pieces;
+    p.n_pieces = (int)pieces.size();
+    p.R = h->R;
+    p.W = h->W;
+    p.n_pos = h->n_pos;
+    p.err_max = h->err_max;
+    p.n = h->n;
+    p.total_tiles = tiles;
+    choose_split(h, tiles, &p.nsplit, &p.rows_per_split);
+    p.variant = h->variant;
+    p.mask_k = h->mask_k;
+    p.n_dep = h->n_dep;
+    p.deps = h->d_deps;
+    p.mode = mode;
+    p.check_solve = check_solve ? 1 : 0;
+    p.table = h->table;
+    p.table_mask = h->table_cap ? h->table_cap - 1 : 0;
+    p.gbase = h->offered;
+    p.slot = h->d_slot;
+    p.fp_out = mode == MODE_FP_ONLY ? h->d_fp : nullptr;
+    p.ctl = h->d_ctl;
+    if (p.nsplit > 1) {
+        if ((rc = ensure_acc(h, total))) return rc;
+        p.acc_s0 = h->d_acc_s0;
+        p.acc_s1 = h->d_acc_s1;
+        p.acc_err = h->d_acc_err;
+        CK(cudaMemsetAsync(h->d_acc_s0, 0, (size_t)total * 8, h->stream));
+        CK(cudaMemsetAsync(h->d_acc_s1, 0, (size_t)total * 8, h->stream));
+        CK(cudaMemsetAsync(h->d_acc_err, 0, (size_t)total * 4, h->stream));
+    }
+    const bool mueller = h->variant == VAR_MUELLER;
+    {
+        ScopedTimer t(h, LTL_K_SCREEN, (u64)total, screen_bytes(h, pieces));
+        dim3 grid((unsigned)((tiles + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), (unsigned)p.nsplit);
+        SCREEN_FN[h->W](p, mueller, grid, h->stream);
+    }
+    CK(cudaGetLastError());
+    if (p.nsplit > 1) {
+        ScopedTimer t(h, LTL_K_FINALIZE, (u64)total, (double)total * 36.0);
+        if (mueller) k_finalize<true><<<(unsigned)((total + 255) / 256), 256, 0, h->stream>>>(p, (u64)total);
+        else k_finalize<false><<<(unsigned)((total + 255) / 256), 256, 0, h->stream>>>(p, (u64)total);
+        CK(cudaGetLastError());
+    }
+    if (mode != MODE_INSERT) {
+        CK(cudaMemcpyAsync(h->h_ctl, h->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        h->d2h_bytes += sizeof(Ctl);
+        drain_events(h);
+        return LTL_OK;
+    }
+
+    // ---- ordered admission.  The resolve limit min(total, solver rank) is read from ctl on the device, so
+    // phase A and the three bookkeeping kernels run back to back with one host round trip per chunk.
+    const u64 room = h->cap_entries > h->n_entries ? h->cap_entries - h->n_entries : 0;
+    {
+        const unsigned nb = (unsigned)((total + RES_CTA - 1) / RES_CTA);
+        {
+            ScopedTimer t(h, LTL_K_RESOLVE, (u64)total, (double)total * 36.0);
+            k_resolve<<<nb, RES_CTA, 0, h->stream>>>(h->d_slot, h->table, h->offered, (u64)total, h->d_ctl, h->d_flagw,
+                                                      h->d_blocksum);
+        }
+        {
+            ScopedTimer t(h, LTL_K_SCAN, nb, (double)nb * 12.0);
+            k_scan<<<1, 1024, 0, h->stream>>>(h->d_blocksum, nb, h->d_blockoff, h->d_ctl);
+        }
+        {
+            ScopedTimer t(h, LTL_K_EMIT, (u64)total, (double)total * 0.125);
+            k_emit<<<nb, RES_CTA, 0, h->stream>>>(h->d_flagw, h->d_blockoff, h->d_pieces, (int)pieces.size(), (u64)total,
+                                                   (i64)h->n_entries, room, (unsigned char*)h->rec_op.base,
+                                                   (int*)h->rec_lhs.base, (int*)h->rec_rhs.base, h->d_ctl);
+        }
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(h->h_ctl, h->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        h->d2h_bytes += sizeof(Ctl);
+    }
+    const u64 solver_c = h->h_ctl->solver_c;
+    const u64 winners = h->h_ctl->total;
+    const u64 oom_c = h->h_ctl->oom_c;
+    drain_events(h);
+    const bool oom = winners > room;
+    const u64 count = oom ? room : winners;
+    if (oom && oom_c == ~0ull) return h->fail(LTL_ERR_CUDA, "internal: overflow rank missing");
+    if (count > 0 && materialize) {
+        if ((rc = ensure_entries(h, h->n_entries + count))) return rc;
+        MaterializeParams m;
+        memset(&m, 0, sizeof(m));
+        m.cms = (u64*)h->cms.base;
+        m.masks = h->d_masks;
+        m.R = h->R;
+        m.W = h->W;
+        m.n = h->n;
+        m.n_base = (i64)h->n_entries;
+        m.count = (i64)count;
+        m.rec_op = (const unsigned char*)h->rec_op.base;
+        m.rec_lhs = (const int*)h->rec_lhs.base;
+        m.rec_rhs = (const int*)h->rec_rhs.base;
+        const i64 groups = (i64)((h->n_entries + count + 31) / 32 - h->n_entries / 32);
+        choose_split(h, groups, &m.nsplit, &m.rows_per_split);
+        ScopedTimer t(h, LTL_K_MATERIALIZE, count, (double)count * (8.0 * (double)h->n + 16.0 + 9.0));
+        dim3 grid((unsigned)((groups + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), (unsigned)m.nsplit);
+        MATERIALIZE_FN[h->W](m, grid, h->stream);
+        CK(cudaGetLastError());
+    }
+    // ---- counters (reference _speedups.pyx:347-354, 372-379)
+    u64 offered_c;
+    if (oom) {
+        out->status = LTL_S_OOM;
+        out->cut_c = oom_c;
+        offered_c = oom_c + 1;
+        h->duplicates += oom_c - count;
+    } else if (solver_c != ~0ull) {
+        out->status = LTL_S_SOLVED;
+        out->cut_c = solver_c;
+        offered_c = solver_c + 1;
+        h->duplicates += solver_c - count;
+    } else {
+        offered_c = (u64)total;
+        h->duplicates += (u64)total - count;
+    }
+    out->admitted = count;
+    const u64 gbase = h->offered;
+    h->offered += offered_c;
+    h->admitted += count;
+    h->n_entries += count;
+    if (out->status != LTL_S_DONE) {
+        ScopedTimer t(h, LTL_K_PURGE, h->table_cap, (double)h->table_cap * sizeof(Slot));
+        k_purge<<<(unsigned)((h->table_cap + 255) / 256), 256, 0, h->stream>>>(h->table, h->table_cap, gbase + out->cut_c);
+        CK(cudaGetLastError());
+        h->keys_upper += (u64)total;
+    } else {
+        h->keys_upper += count;
+    }
+    return LTL_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// level driver: units -> chunks of <= chunk_cap candidates, consecutive in enumeration order
+
+static int run_units(ltl_core* h, const std::vector<Unit>& units, bool check_solve, int* status, int* seg_index,
+                     int64_t* li, int64_t* ri) {
+    *status = LTL_S_DONE;
+    *seg_index = -1;
+    *li = *ri = -1;
+    std::vector<Piece> pieces;
+    size_t ui = 0;
+    i64 row = units.empty() ? 0 : units[0].i0;  // next row (left index) of the current unit
+    i64 col = -1;                               // >= 0: next column inside a partially emitted row
+    while (ui < units.size()) {
+        pieces.clear();
+        i64 total = 0, tiles = 0;
+        const i64 cap = h->chunk_cap;
+        while (ui < units.size() && total < cap) {
+            const Unit& u = units[ui];
+            const i64 room = cap - total;
+            bool unit_done = false;
+            if (u.kind == PIECE_UNARY) {
+                const i64 take = std::min(room, u.i1 - row);
+                push_piece(h, pieces, total, tiles, u, row, row + take, -1, -1, PIECE_UNARY);
+                row += take;
+                unit_done = row == u.i1;
+            } else {
+                // columns of row `row`: [cstart, u.j1)
+                const i64 c0 = u.kind == PIECE_RECT ? u.j0 : row + 1;
+                if (col >= 0) {  // finish a partially emitted row
+                    const i64 take = std::min(room, u.j1 - col);
+                    push_piece(h, pieces, total, tiles, u, row, row + 1, col, col + take, PIECE_RECT);
+                    col += take;
+                    if (col == u.j1) {
+                        col = -1;
+                        row++;
+                    }
+                    unit_done = row == u.i1;
+                } else {
+                    i64 rows_fit;
+                    if (u.kind == PIECE_RECT) {
+                        rows_fit = std::min(u.i1 - row, room / (u.j1 - u.j0));
+                    } else {
+                        const u64 m = (u64)(u.j1 - 1 - row);
+                        i64 lo = 0, hi = u.i1 - row;
+                        while (lo < hi) {
+                            i64 mid = (lo + hi + 1) >> 1;
+                            if (tri_before((u64)mid, m) <= (u64)room) lo = mid;
+                            else hi = mid - 1;
+                        }
+                        rows_fit = lo;
+                    }
+                    if (rows_fit > 0) {
+                        if (u.kind == PIECE_RECT) push_piece(h, pieces, total, tiles, u, row, row + rows_fit, u.j0, u.j1, PIECE_RECT);
+                        else push_piece(h, pieces, total, tiles, u, row, row + rows_fit, -1, u.j1, PIECE_TRI);
+                        row += rows_fit;
+                        unit_done = row == u.i1;
+                    } else if (total == 0) {  // a single row exceeds the chunk: emit it in column runs
+                        col = c0;
+                        continue;
+                    } else {
+                        break;  // close the chunk, the row starts the next one
+                    }
+                }
+            }
+            if (unit_done) {
+                ui++;
+                if (ui < units.size()) row = units[ui].i0;
+                col = -1;
+            }
+        }
+        ChunkOut co;
+        int rc = run_chunk(h, pieces, total, tiles, MODE_INSERT, check_solve, true, &co);
+        if (rc) return rc;
+        if (co.status != LTL_S_DONE) {
+            *status = co.status;
+            if (co.status == LTL_S_SOLVED) {
+                size_t pi = 0;
+                for (size_t k = 0; k < pieces.size(); k++)
+                    if ((u64)pieces[k].cbase <= co.cut_c) pi = k;
+                i64 i, j;
+                piece_unrank(pieces[pi], co.cut_c, &i, &j);
+                *li = i;
+                *ri = j;
+                *seg_index = pieces[pi].seg;
+            }
+            return LTL_OK;
+        }
+    }
+    return LTL_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// single-matrix paths (add_entry / contains / fingerprint_of)
+
+static int stage_matrix(ltl_core* h, const uint64_t* cm, i64 e) {
+    int rc;
+    if ((rc = ensure_entries(h, (u64)e + 1))) return rc;
+    CK(cudaStreamSynchronize(h->stream));  // h_stage may still be in flight
+    memcpy(h->h_stage, cm, (size_t)h->n * 8);
+    CK(cudaMemcpyAsync(h->d_stage, h->h_stage, (size_t)h->n * 8, cudaMemcpyHostToDevice, h->stream));
+    h->h2d_bytes += (size_t)h->n * 8;
+    ScopedTimer t(h, LTL_K_MISC, 1, 16.0 * (double)h->n);
+    k_import<<<(unsigned)((h->n + 255) / 256), 256, 0, h->stream>>>(h->d_stage, (u64*)h->cms.base, e, h->n);
+    CK(cudaGetLastError());
+    return LTL_OK;
+}
+
+static int single_chunk(ltl_core* h, i64 e, int mode, ChunkOut* co) {
+    std::vector<Piece> pieces;
+    i64 total = 0, tiles = 0;
+    Unit u{PIECE_UNARY, OP_IDENT, 0, e, e + 1, -1, -1};
+    push_piece(h, pieces, total, tiles, u, e, e + 1, -1, -1, PIECE_UNARY);
+    return run_chunk(h, pieces, total, tiles, mode, false, false, co);
+}
+
+// ------------------------------------------------------------------------------------------------
+// fingerprint deposits for the bit-gathering variants
+
+static int build_deposits(ltl_core* h, const int32_t* proj_rows, const int32_t* proj_offs, int n_proj, std::vector<Deposit>& deps) {
+    if (h->variant == VAR_GATHER) {  // reference _speedups.pyx:188-195: bit b of the projection -> bit 125 - b
+        for (int b = 0; b < n_proj; b++) {
+            const int r = proj_rows[b], off = proj_offs[b];
+            if (r < 0 || r >= h->R || off < 0 || off >= 64 * h->W) return h->fail(LTL_ERR_ARG, "projection outside the matrix");
+            Deposit d;
+            d.k = (u32)(r * h->W + (off >> 6));
+            d.rsh = (u32)(63 - (off & 63));
+            d.mask = 1;
+            d.pos = (u32)(125 - b);
+            d.pad = 0;
+            deps.push_back(d);
+        }
+    } else if (h->variant == VAR_FKP) {  // reference _speedups.pyx:205-222: first fkp_bits positions of every row
+        if (h->fkp_bits < 1 || h->fkp_bits > 64) return h->fail(LTL_ERR_ARG, "fkp_bits must lie in [1, 64]");
+        int used = 0;
+        for (int r = 0; r < h->R; r++) {
+            int nb = std::min(126 - used, h->fkp_bits);
+            if (nb <= 0) break;
+            Deposit d;
+            d.k = (u32)(r * h->W);
+            d.rsh = (u32)(64 - nb);
+            d.mask = nb >= 64 ? ~0ull : ((1ull << nb) - 1ull);
+            d.pos = (u32)(126 - used - nb);
+            d.pad = 0;
+            deps.push_back(d);
+            used += nb;
+        }
+    }
+    std::stable_sort(deps.begin(), deps.end(), [](const Deposit& a, const Deposit& b) { return a.k < b.k; });
+    return LTL_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// C ABI
+
+extern "C" {
+
+int ltl_abi_version(void) { return LTL_ABI_VERSION; }
+
+int ltl_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return LTL_ERR_CUDA;
+    }
+    return n;
+}
+
+const char* ltl_core_last_error(const ltl_core* h) { return h ? h->err.c_str() : g_create_error.c_str(); }
+
+void ltl_core_destroy(ltl_core* h) {
+    if (!h) return;
+    cudaSetDevice(h->device);
+    if (h->stream) cudaStreamSynchronize(h->stream);
+    drain_events(h);
+    for (auto e : h->event_pool) cudaEventDestroy(e);
+    h->cms.release();
+    h->rec_op.release();
+    h->rec_lhs.release();
+    h->rec_rhs.release();
+    cudaFree(h->table);
+    cudaFree(h->d_masks);
+    cudaFree(h->d_deps);
+    cudaFree(h->d_slot);
+    cudaFree(h->d_flagw);
+    cudaFree(h->d_blocksum);
+    cudaFree(h->d_blockoff);
+    cudaFree(h->d_acc_s0);
+    cudaFree(h->d_acc_s1);
+    cudaFree(h->d_acc_err);
+    cudaFree(h->d_fp);
+    cudaFree(h->d_pieces);
+    cudaFree(h->d_ctl);
+    cudaFree(h->d_stage);
+    cudaFreeHost(h->h_pieces);
+    cudaFreeHost(h->h_ctl);
+    cudaFreeHost(h->h_stage);
+    if (h->stream) cudaStreamDestroy(h->stream);
+    cudaGetLastError();
+    delete h;
+}
+
+int ltl_core_create(const uint64_t* masks, int R, int W, int n_pos, int err_max, int variant, const int32_t* proj_rows,
+                    const int32_t* proj_offs, int n_proj, int fkp_bits, int mask_k, uint64_t budget_bytes, int device,
+                    ltl_core** out) {
+    if (!out) return LTL_ERR_ARG;
+    *out = nullptr;
+    auto bad = [&](const char* m) {
+        g_create_error = m;
+        return LTL_ERR_ARG;
+    };
+    if (!masks || R < 1) return bad("need at least one row");
+    if (W < 1 || W > LTL_MAX_W) return bad("words per row must lie in [1, 16]");
+    if (n_pos < 0 || n_pos > R) return bad("n_pos outside [0, R]");
+    if (variant < 0 || variant > 2) return bad("unknown fingerprint variant");
+    if (n_proj < 0 || n_proj > 126) return bad("projection wider than the fingerprint");  // reference _speedups.pyx:92-93
+    if (mask_k < 0 || mask_k > 126) return bad("mask_k outside [0, 126]");
+    if ((int64_t)R * W > (int64_t)1 << 31) return bad("matrix too large");
+    int ndev = 0;
+    cudaError_t ce = cudaGetDeviceCount(&ndev);
+    if (ce != cudaSuccess || ndev < 1) {
+        g_create_error = std::string("no usable CUDA device: ") + cudaGetErrorString(ce);
+        cudaGetLastError();
+        return LTL_ERR_CUDA;
+    }
+    if (device < 0 || device >= ndev) return bad("device index out of range");
+    ltl_core* h = new ltl_core();
+    h->device = device;
+    h->R = R;
+    h->W = W;
+    h->n = (i64)R * W;
+    h->n_pos = n_pos;
+    h->err_max = err_max;
+    h->variant = variant;
+    h->fkp_bits = fkp_bits;
+    h->mask_k = mask_k;
+    h->budget = budget_bytes;
+    h->entry_bytes = (u64)h->n * 8 + 16;  // reference _speedups.pyx:100
+    int rc = LTL_OK;
+    auto boot = [&]() -> int {
+        CK(cudaSetDevice(device));
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, device));
+        h->sm_count = prop.multiProcessorCount;
+        CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        size_t free_b = 0, total_b = 0;
+        CK(cudaMemGetInfo(&free_b, &total_b));
+        // admissions allowed by the logical budget: OOM when admitted*eb + eb > budget (reference _speedups.pyx:252-253)
+        u64 logical = h->budget / h->entry_bytes;
+        const double per_entry = 8.0 * (double)h->n + 9.0 + 2.5 * sizeof(Slot);
+        const double usable = (double)free_b * 0.92 - (double)h->chunk_cap * 8.0 - (double)(64u << 20);
+        u64 physical = usable > per_entry ? (u64)(usable / per_entry) : 0;
+        h->cap_entries = std::min<u64>(std::min(logical, physical), (1ull << 31) - 64);
+        const u64 cap_groups = (h->cap_entries + 63) / 32;
+        h->cms.init(device, (size_t)cap_groups * 32 * (size_t)h->n * 8);
+        h->rec_op.init(device, (size_t)cap_groups * 32);
+        h->rec_lhs.init(device, (size_t)cap_groups * 32 * 4);
+        h->rec_rhs.init(device, (size_t)cap_groups * 32 * 4);
+        CK(cudaMalloc(&h->d_masks, (size_t)h->n * 8));
+        CK(cudaMemcpyAsync(h->d_masks, masks, (size_t)h->n * 8, cudaMemcpyHostToDevice, h->stream));
+        h->h2d_bytes += (size_t)h->n * 8;
+        CK(cudaStreamSynchronize(h->stream));
+        std::vector<Deposit> deps;
+        int r2 = build_deposits(h, proj_rows, proj_offs, n_proj, deps);
+        if (r2) return r2;
+        h->n_dep = (int)deps.size();
+        CK(cudaMalloc(&h->d_deps, sizeof(Deposit) * std::max<size_t>(1, deps.size())));
+        if (!deps.empty()) {
+            CK(cudaMemcpyAsync(h->d_deps, deps.data(), sizeof(Deposit) * deps.size(), cudaMemcpyHostToDevice, h->stream));
+            CK(cudaStreamSynchronize(h->stream));
+        }
+        CK(cudaMalloc(&h->d_ctl, sizeof(Ctl)));
+        CK(cudaMallocHost(&h->h_ctl, sizeof(Ctl)));
+        CK(cudaMalloc(&h->d_stage, (size_t)h->n * 8));
+        CK(cudaMallocHost(&h->h_stage, (size_t)h->n * 8));
+        return ensure_table(h, 1);
+    };
+    rc = boot();
+    if (rc) {
+        g_create_error = h->err;
+        ltl_core_destroy(h);
+        return rc;
+    }
+    *out = h;
+    return LTL_OK;
+}
+
+#define ENTER(h)                              \
+    if (!(h)) return LTL_ERR_ARG;             \
+    {                                         \
+        cudaError_t e0_ = cudaSetDevice((h)->device); \
+        if (e0_ != cudaSuccess) return (h)->cuda_fail(e0_, "cudaSetDevice"); \
+    }
+
+int ltl_core_add_entry(ltl_core* h, const uint64_t* cm, int op, int lhs, int rhs, int64_t* index_out) {
+    ENTER(h);
+    if (!cm || !index_out) return h->fail(LTL_ERR_ARG, "null argument");
+    *index_out = -1;
+    const i64 e = (i64)h->n_entries;
+    int rc;
+    if ((rc = stage_matrix(h, cm, e))) return rc;
+    ChunkOut co;
+    if ((rc = single_chunk(h, e, MODE_INSERT, &co))) return rc;
+    if (co.status == LTL_S_OOM) return h->fail(LTL_ERR_BUDGET, "memory budget exhausted");
+    if (co.admitted == 1) {
+        ScopedTimer t(h, LTL_K_MISC, 1, 9.0);
+        k_set_record<<<1, 1, 0, h->stream>>>((unsigned char*)h->rec_op.base, (int*)h->rec_lhs.base, (int*)h->rec_rhs.base, e, op,
+                                             lhs, rhs);
+        CK(cudaGetLastError());
+        *index_out = e;
+    }
+    return LTL_OK;
+}
+
+int ltl_core_run_level(ltl_core* h, const ltl_segment* segs, int n_segs, int* status, int* seg_index, int64_t* li,
+                       int64_t* ri) {
+    ENTER(h);
+    if (n_segs < 0 || (n_segs && !segs) || !status || !seg_index || !li || !ri) return h->fail(LTL_ERR_ARG, "null argument");
+    std::vector<Unit> units;
+    int rc = expand_segments(h, segs, n_segs, units);
+    if (rc) return rc;
+    return run_units(h, units, true, status, seg_index, li, ri);
+}
+
+int ltl_core_screen_unary(ltl_core* h, int op, int64_t c0, int64_t c1, int* status, int64_t* li, int64_t* ri) {
+    ltl_segment s{op, 0, c0, c1, -1, -1};
+    int seg;
+    return ltl_core_run_level(h, &s, 1, status, &seg, li, ri);
+}
+
+int ltl_core_screen_binary(ltl_core* h, int op, int64_t a0, int64_t a1, int64_t b0, int64_t b1, int tri, int* status,
+                           int64_t* li, int64_t* ri) {
+    ltl_segment s{op, tri ? 1 : 0, a0, a1, b0, b1};
+    int seg;
+    return ltl_core_run_level(h, &s, 1, status, &seg, li, ri);
+}
+
+int ltl_core_contains(ltl_core* h, const uint64_t* cm, int* found) {
+    ENTER(h);
+    if (!cm || !found) return h->fail(LTL_ERR_ARG, "null argument");
+    const i64 e = (i64)h->n_entries;  // staged past the end of the store, never admitted
+    int rc;
+    if ((rc = stage_matrix(h, cm, e))) return rc;
+    ChunkOut co;
+    if ((rc = single_chunk(h, e, MODE_LOOKUP, &co))) return rc;
+    *found = h->h_ctl->found ? 1 : 0;
+    return LTL_OK;
+}
+
+int ltl_core_fingerprint_of(ltl_core* h, const uint64_t* cm, uint64_t* hi, uint64_t* lo) {
+    ENTER(h);
+    if (!cm || !hi || !lo) return h->fail(LTL_ERR_ARG, "null argument");
+    const i64 e = (i64)h->n_entries;
+    int rc;
+    if ((rc = stage_matrix(h, cm, e))) return rc;
+    ChunkOut co;
+    if ((rc = single_chunk(h, e, MODE_FP_ONLY, &co))) return rc;
+    *hi = h->h_ctl->fp_hi;
+    *lo = h->h_ctl->fp_lo;
+    return LTL_OK;
+}
+
+int ltl_core_entry_fingerprints(ltl_core* h, int64_t first, int64_t count, uint64_t* hi, uint64_t* lo) {
+    ENTER(h);
+    if (first < 0 || count < 0 || (u64)(first + count) > h->n_entries) return h->fail(LTL_ERR_ARG, "entry range outside the store");
+    if (count == 0) return LTL_OK;
+    if (!hi || !lo) return h->fail(LTL_ERR_ARG, "null argument");
+    std::vector<u64> host;
+    for (i64 done = 0; done < count;) {
+        const i64 take = std::min<i64>(count - done, 1 << 20);
+        if (take > h->fp_cap) {
+            CK(cudaStreamSynchronize(h->stream));
+            cudaFree(h->d_fp);
+            h->d_fp = nullptr;
+            h->fp_cap = 0;
+            CK(cudaMalloc(&h->d_fp, (size_t)take * 16));
+            h->fp_cap = take;
+        }
+        std::vector<Piece> pieces;
+        i64 total = 0, tiles = 0;
+        Unit u{PIECE_UNARY, OP_IDENT, 0, first + done, first + done + take, -1, -1};
+        push_piece(h, pieces, total, tiles, u, u.i0, u.i1, -1, -1, PIECE_UNARY);
+        ChunkOut co;
+        int rc = run_chunk(h, pieces, total, tiles, MODE_FP_ONLY, false, false, &co);
+        if (rc) return rc;
+        host.resize((size_t)take * 2);
+        CK(cudaMemcpy(host.data(), h->d_fp, (size_t)take * 16, cudaMemcpyDeviceToHost));
+        for (i64 k = 0; k < take; k++) {
+            hi[done + k] = host[2 * k];
+            lo[done + k] = host[2 * k + 1];
+        }
+        done += take;
+    }
+    return LTL_OK;
+}
+
+int ltl_core_export_cms(ltl_core* h, int64_t first, int64_t count, uint64_t* cms_out) {
+    ENTER(h);
+    if (first < 0 || count < 0 || (u64)(first + count) > h->n_entries) return h->fail(LTL_ERR_ARG, "entry range outside the store");
+    if (count == 0) return LTL_OK;
+    if (!cms_out) return h->fail(LTL_ERR_ARG, "null argument");
+    const i64 max_batch = std::max<i64>(1, ((i64)256 << 20) / (h->n * 8));
+    u64* d_out = nullptr;
+    const i64 batch = std::min<i64>(count, max_batch);
+    CK(cudaMalloc(&d_out, (size_t)batch * h->n * 8));
+    for (i64 done = 0; done < count;) {
+        const i64 take = std::min<i64>(batch, count - done);
+        const i64 f = first + done;
+        const i64 groups = ((f + take + 31) >> 5) - (f >> 5);
+        const i64 threads = groups * h->n * 32;
+        {
+            ScopedTimer t(h, LTL_K_MISC, (u64)take, 16.0 * (double)h->n * (double)take);
+            k_export<<<(unsigned)((threads + 255) / 256), 256, 0, h->stream>>>((const u64*)h->cms.base, f, take, h->n, d_out);
+        }
+        cudaError_t e = cudaMemcpyAsync(cms_out + (size_t)done * h->n, d_out, (size_t)take * h->n * 8, cudaMemcpyDeviceToHost, h->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
+        if (e != cudaSuccess) {
+            cudaFree(d_out);
+            return h->cuda_fail(e, "export_cms");
+        }
+        h->d2h_bytes += (size_t)take * h->n * 8;
+        done += take;
+    }
+    cudaFree(d_out);
+    drain_events(h);
+    return LTL_OK;
+}
+
+int ltl_core_get_cm(ltl_core* h, int64_t idx, uint64_t* out) {
+    if (!h) return LTL_ERR_ARG;
+    if (idx < 0 || (u64)idx >= h->n_entries) return h->fail(LTL_ERR_ARG, "entry index out of range");
+    return ltl_core_export_cms(h, idx, 1, out);
+}
+
+int ltl_core_export_records(ltl_core* h, int64_t first, int64_t count, int8_t* op, int32_t* lhs, int32_t* rhs) {
+    ENTER(h);
+    if (first < 0 || count < 0 || (u64)(first + count) > h->n_entries) return h->fail(LTL_ERR_ARG, "entry range outside the store");
+    if (count == 0) return LTL_OK;
+    if (!op || !lhs || !rhs) return h->fail(LTL_ERR_ARG, "null argument");
+    CK(cudaStreamSynchronize(h->stream));
+    CK(cudaMemcpy(op, h->rec_op.base + first, (size_t)count, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(lhs, h->rec_lhs.base + first * 4, (size_t)count * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(rhs, h->rec_rhs.base + first * 4, (size_t)count * 4, cudaMemcpyDeviceToHost));
+    h->d2h_bytes += (size_t)count * 9;
+    return LTL_OK;
+}
+
+int ltl_core_get_record(ltl_core* h, int64_t idx, int* op, int* lhs, int* rhs) {
+    if (!h) return LTL_ERR_ARG;
+    if (idx < 0 || (u64)idx >= h->n_entries) return h->fail(LTL_ERR_ARG, "entry index out of range");
+    int8_t o;
+    int32_t l, r;
+    int rc = ltl_core_export_records(h, idx, 1, &o, &l, &r);
+    if (rc) return rc;
+    *op = o;
+    *lhs = l;
+    *rhs = r;
+    return LTL_OK;
+}
+
+int ltl_core_counters(ltl_core* h, uint64_t out[5]) {
+    if (!h || !out) return LTL_ERR_ARG;
+    out[0] = h->n_entries;
+    out[1] = h->admitted * h->entry_bytes;  // reference _speedups.pyx:260
+    out[2] = h->offered;
+    out[3] = h->admitted;
+    out[4] = h->duplicates;
+    return LTL_OK;
+}
+
+int ltl_core_set_option(ltl_core* h, const char* name, int64_t value) {
+    if (!h || !name) return LTL_ERR_ARG;
+    if (!strcmp(name, "chunk_candidates")) {
+        if (value < 1 || value > ((int64_t)1 << 30)) return h->fail(LTL_ERR_ARG, "chunk_candidates outside [1, 2^30]");
+        h->chunk_cap = value;
+    } else if (!strcmp(name, "profile")) {
+        h->profile = value != 0;
+    } else if (!strcmp(name, "max_split")) {
+        h->max_split = (int)std::max<int64_t>(1, value);
+    } else if (!strcmp(name, "force_split")) {
+        h->force_split = (int)std::max<int64_t>(0, value);
+    } else {
+        return h->fail(LTL_ERR_ARG, std::string("unknown option ") + name);
+    }
+    return LTL_OK;
+}
+
+int ltl_core_kernel_stats(ltl_core* h, int cls, uint64_t* launches, double* ms, double* alg_bytes, uint64_t* units) {
+    ENTER(h);
+    if (cls < 0 || cls >= LTL_K_COUNT) return h->fail(LTL_ERR_ARG, "kernel class out of range");
+    CK(cudaStreamSynchronize(h->stream));
+    drain_events(h);
+    if (launches) *launches = h->stats[cls].launches;
+    if (ms) *ms = h->stats[cls].ms;
+    if (alg_bytes) *alg_bytes = h->stats[cls].bytes;
+    if (units) *units = h->stats[cls].units;
+    return LTL_OK;
+}
+
+int ltl_core_reset_kernel_stats(ltl_core* h) {
+    ENTER(h);
+    CK(cudaStreamSynchronize(h->stream));
+    drain_events(h);
+    for (auto& s : h->stats) s = KStat();
+    return LTL_OK;
+}
+
+int ltl_core_stream(ltl_core* h, void** stream_out) {
+    if (!h || !stream_out) return LTL_ERR_ARG;
+    *stream_out = (void*)h->stream;
+    return LTL_OK;
+}
+
+int ltl_core_transfer_stats(ltl_core* h, uint64_t out[2]) {
+    if (!h || !out) return LTL_ERR_ARG;
+    out[0] = h->h2d_bytes;
+    out[1] = h->d2h_bytes;
+    return LTL_OK;
+}
+
+int ltl_core_info(ltl_core* h, uint64_t out[6]) {
+    if (!h || !out) return LTL_ERR_ARG;
+    out[0] = h->cap_entries;
+    out[1] = h->cms.mapped;
+    out[2] = h->table_cap;
+    out[3] = (u64)h->chunk_cap;
+    out[4] = h->cms.vmm ? 1 : 0;
+    out[5] = (u64)h->n;
+    return LTL_OK;
+}
+
+}  // extern "C"

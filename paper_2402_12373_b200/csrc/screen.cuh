@@ -1,0 +1,418 @@
+// screen.cuh -- the two hot kernels of the screening core, templated on W = words per row.
+//
+//   k_screen<W, MUELLER>   "phase A": one warp per tile of (<= 4 entries of one operand) x (32 entries of
+//       the other); every lane evaluates its candidates' characteristic matrices row by row IN REGISTERS
+//       (nothing is written back), counts P/N classification errors (fused solve check, reference
+//       _speedups.pyx:327-333), folds the rows into the 126-bit fingerprint (reference _speedups.pyx:185-231)
+//       and files the fingerprint in the uniqueness table with atomicMin(rank)
+//       (= the sequential first-wins admission of _speedups.pyx:245-262, made order-independent).
+//   k_materialize<W>       "phase B": one warp per 32 consecutive NEW entries; re-evaluates only the
+//       winners from their (op, lhs, rhs) records and appends them to the store with full-line writes.
+//
+// Reference loop being replaced: _speedups.pyx:337-380 (screen_unary / screen_binary).
+#pragma once
+#include "semantics.cuh"
+
+// ------------------------------------------------------------------------------------------------
+// rank helpers
+
+__host__ __device__ __forceinline__ u64 piece_rank(const Piece& pc, i64 i, i64 j) {
+    if (pc.kind == PIECE_UNARY) return (u64)pc.cbase + (u64)(i - pc.i0);
+    if (pc.kind == PIECE_RECT) return (u64)pc.cbase + (u64)(i - pc.i0) * (u64)(pc.j1 - pc.j0) + (u64)(j - pc.j0);
+    return (u64)pc.cbase + tri_before((u64)(i - pc.i0), (u64)(pc.j1 - 1 - pc.i0)) + (u64)(j - i - 1);
+}
+
+// inverse of piece_rank: chunk-local rank -> (i, j); j = -1 for unary pieces
+__host__ __device__ inline void piece_unrank(const Piece& pc, u64 c, i64* i, i64* j) {
+    u64 local = c - (u64)pc.cbase;
+    if (pc.kind == PIECE_UNARY) {
+        *i = pc.i0 + (i64)local;
+        *j = -1;
+    } else if (pc.kind == PIECE_RECT) {
+        u64 nj = (u64)(pc.j1 - pc.j0);
+        u64 q = local / nj;
+        *i = pc.i0 + (i64)q;
+        *j = pc.j0 + (i64)(local - q * nj);
+    } else {
+        u64 m = (u64)(pc.j1 - 1 - pc.i0);
+        // largest q with T(q) <= local, T(q) = q*m - q(q-1)/2
+        double b = 2.0 * (double)m + 1.0;
+        double disc = b * b - 8.0 * (double)local;
+        if (disc < 0) disc = 0;
+        i64 q = (i64)((b - sqrt(disc)) * 0.5);
+        if (q < 0) q = 0;
+        if ((u64)q > m) q = (i64)m;
+        while (q > 0 && tri_before((u64)q, m) > local) q--;
+        while (tri_before((u64)q + 1, m) <= local) q++;
+        *i = pc.i0 + q;
+        *j = *i + 1 + (i64)(local - tri_before((u64)q, m));
+    }
+}
+
+#ifdef __CUDACC__
+
+// ------------------------------------------------------------------------------------------------
+// fingerprint finalisation + table filing for one candidate
+
+template <bool MUELLER>
+__device__ __forceinline__ void finish_candidate(const ScreenParams& p, u64 c, u64 s0, u64 s1, u32 err) {
+    u64 hi, lo;
+    if (MUELLER) {  // reference _speedups.pyx:203-204
+        hi = mix64(s0) & K_HI_CLEAR;
+        lo = mix64(s1);
+    } else {
+        hi = s0;
+        lo = s1;
+    }
+    // reference _speedups.pyx:223-229: clear the lowest mask_k bits of the 128-bit value
+    if (p.mask_k >= 64) {
+        lo = 0;
+        if (p.mask_k > 64) hi &= ~((1ull << (p.mask_k - 64)) - 1ull);
+    } else if (p.mask_k > 0) {
+        lo &= ~((1ull << p.mask_k) - 1ull);
+    }
+    const bool solves = p.check_solve && (int)err <= p.err_max;
+    if (solves) atomicMin(&p.ctl->solver_c, c);
+    if (p.mode == MODE_FP_ONLY) {
+        if (p.fp_out) {
+            p.fp_out[2 * c] = hi;
+            p.fp_out[2 * c + 1] = lo;
+        }
+        if (c == 0) {
+            p.ctl->fp_hi = hi;
+            p.ctl->fp_lo = lo;
+        }
+        return;
+    }
+    if (p.mode == MODE_LOOKUP) {
+        u64 s = table_find(p.table, p.table_mask, hi, lo);
+        p.ctl->found = (s != ~0ull && ld_rank(p.table + s) != LTL_RANK_NONE) ? 1ull : 0ull;
+        return;
+    }
+    if (solves) {  // a solving candidate is returned, never admitted (reference _speedups.pyx:372-374)
+        p.slot[c] = LTL_NONE;
+        return;
+    }
+    u64 s = table_find_or_claim(p.table, p.table_mask, hi, lo);
+    u64 old = atomicMin(&p.table[s].rank, p.gbase + c);
+    p.slot[c] = (old < p.gbase) ? LTL_NONE : (u32)s;  // key already a member from an earlier chunk
+}
+
+// ------------------------------------------------------------------------------------------------
+// one warp tile
+
+template <int W, bool MUELLER, int OP, int TI, bool XL>
+__device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc, const i64 row0, const i64 lg,
+                                          const int split, const int lane) {
+    constexpr bool BIN = !(OP == OP_IDENT || OP == OP_NOT || OP == OP_NEXT || OP == OP_FINALLY || OP == OP_GLOBALLY);
+    constexpr bool NEEDM = (OP == OP_NOT || OP == OP_GLOBALLY);
+    const i64 n = p.n;
+    const i64 e = lg * 32 + lane;  // the lane operand's entry index
+    const u64* __restrict__ pl = p.cms + (size_t)lg * (size_t)n * 32 + lane;
+    const u64* __restrict__ pr[TI];
+#pragma unroll
+    for (int t = 0; t < TI; t++) pr[t] = p.cms + cm_index(BIN ? row0 + t : 0, n, 0);
+
+    const int r0 = split * p.rows_per_split;
+    const int r1 = min(p.R, r0 + p.rows_per_split);
+
+    u64 s0[TI], s1[TI], h0[TI], h1[TI];
+    u32 err[TI];
+#pragma unroll
+    for (int t = 0; t < TI; t++) {
+        s0[t] = s1[t] = 0;
+        h0[t] = K_SEED0;
+        h1[t] = K_SEED1;
+        err[t] = 0;
+    }
+    u64 tw = ((u64)r0 * W + 1ull) * K_STEP;  // (k + 1) * STEP for the next word k
+    int d = 0;                               // next deposit (bits fingerprints)
+    if (!MUELLER) {
+        const u32 kfirst = (u32)r0 * W;
+        int lo_ = 0, hi_ = p.n_dep;
+        while (lo_ < hi_) {
+            int mid = (lo_ + hi_) >> 1;
+            if (p.deps[mid].k < kfirst) lo_ = mid + 1;
+            else hi_ = mid;
+        }
+        d = lo_;
+    }
+
+    auto do_row = [&](const int r) {
+        u64 a[W], m[W];
+        const size_t kb = (size_t)r * W;
+#pragma unroll
+        for (int w = 0; w < W; w++) a[w] = ld_nc(pl + (kb + w) * 32);
+#pragma unroll
+        for (int w = 0; w < W; w++) m[w] = NEEDM ? ld_nc(p.masks + kb + w) : 0ull;
+        const u32 ispos = r < p.n_pos ? 1u : 0u;
+#pragma unroll
+        for (int t = 0; t < TI; t++) {
+            u64 b[W], out[W];
+#pragma unroll
+            for (int w = 0; w < W; w++) b[w] = BIN ? ld_nc(pr[t] + (kb + w) * 32) : 0ull;
+            if (!BIN) apply_row<OP, W>(out, a, a, m);
+            else if (XL) apply_row<OP, W>(out, a, b, m);
+            else apply_row<OP, W>(out, b, a, m);
+            err[t] += (u32)(out[0] >> 63) ^ ispos;  // reference _speedups.pyx:327-333
+            if (MUELLER) {
+#pragma unroll
+                for (int w = 0; w < W; w++) {  // reference _speedups.pyx:196-202
+                    u64 mm = mix64(out[w] ^ (tw + (u64)w * K_STEP));
+                    h0[t] = (h0[t] ^ mm) * K_FOLD0;
+                    h1[t] = (h1[t] ^ ((mm << 32) | (mm >> 32))) * K_FOLD1;
+                    if (64 % W != 0) {  // per-word block boundary check (rows straddle hash blocks)
+                        const u64 k1 = kb + w + 1;
+                        if ((k1 & 63) == 0 || k1 == (u64)n) {
+                            if (((k1 - 1) >> 6) == 0) {
+                                s0[t] += h0[t];
+                                s1[t] += h1[t];
+                            } else {
+                                s0[t] += mix64(h0[t]);
+                                s1[t] += mix64(h1[t]);
+                            }
+                            h0[t] = K_SEED0;
+                            h1[t] = K_SEED1;
+                        }
+                    }
+                }
+            } else {
+                int dd = d;
+                while (dd < p.n_dep && p.deps[dd].k < kb + W) {
+                    const Deposit dp = p.deps[dd];
+                    u64 word = out[0];
+#pragma unroll
+                    for (int w = 1; w < W; w++)
+                        if (dp.k - kb == (size_t)w) word = out[w];
+                    const u64 v = (word >> dp.rsh) & dp.mask;
+                    if (dp.pos >= 64) s0[t] += v << (dp.pos - 64);
+                    else {
+                        s1[t] += v << dp.pos;
+                        if (dp.pos > 0) s0[t] += v >> (64 - dp.pos);
+                    }
+                    dd++;
+                }
+                if (t == TI - 1) d = dd;
+            }
+        }
+        tw += (u64)W * K_STEP;
+    };
+
+    if (MUELLER && 64 % W == 0) {
+        constexpr int RPB = (64 % W == 0) ? 64 / W : 1;  // rows per 64-word hash block
+        for (int rb = r0; rb < r1; rb += RPB) {
+            const int rend = min(rb + RPB, r1);
+            if (W == 1) {
+#pragma unroll 4
+                for (int r = rb; r < rend; r++) do_row(r);
+            } else {
+                for (int r = rb; r < rend; r++) do_row(r);
+            }
+#pragma unroll
+            for (int t = 0; t < TI; t++) {  // blocked Mueller: block 0 enters as is (== reference for n <= 64)
+                if (rb == 0) {
+                    s0[t] += h0[t];
+                    s1[t] += h1[t];
+                } else {
+                    s0[t] += mix64(h0[t]);
+                    s1[t] += mix64(h1[t]);
+                }
+                h0[t] = K_SEED0;
+                h1[t] = K_SEED1;
+            }
+        }
+    } else {
+        for (int r = r0; r < r1; r++) do_row(r);
+    }
+
+    // ---- per-candidate epilogue
+    const bool lane_in = pc.kind == PIECE_UNARY ? (e >= pc.i0 && e < pc.i1)
+                         : pc.kind == PIECE_RECT ? (pc.swap ? (e >= pc.i0 && e < pc.i1) : (e >= pc.j0 && e < pc.j1))
+                                                 : (e < pc.j1);
+#pragma unroll
+    for (int t = 0; t < TI; t++) {
+        i64 ci, cj;
+        if (pc.kind == PIECE_UNARY) {
+            ci = e;
+            cj = -1;
+        } else if (pc.kind == PIECE_RECT && pc.swap) {
+            ci = e;
+            cj = row0 + t;
+        } else {
+            ci = row0 + t;
+            cj = e;
+        }
+        const bool valid = lane_in && (pc.kind != PIECE_TRI || cj > ci);
+        if (!valid) continue;
+        const u64 c = piece_rank(pc, ci, cj);
+        if (p.nsplit > 1) {
+            atomicAdd(p.acc_s0 + c, s0[t]);
+            atomicAdd(p.acc_s1 + c, s1[t]);
+            if (err[t]) atomicAdd(p.acc_err + c, err[t]);
+        } else {
+            finish_candidate<MUELLER>(p, c, s0[t], s1[t], err[t]);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
+// phase A kernel
+
+template <int W, bool MUELLER>
+__global__ void __launch_bounds__(LTL_CTA, 2) k_screen(const __grid_constant__ ScreenParams p) {
+    const int lane = threadIdx.x & 31;
+    const i64 T = (i64)blockIdx.x * LTL_WARPS_PER_CTA + (threadIdx.x >> 5);
+    if (T >= p.total_tiles) return;
+    const int split = blockIdx.y;
+    // piece of this tile: last piece with tile_base <= T
+    int lo = 0, hi = p.n_pieces - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if (p.pieces[mid].tile_base <= T) lo = mid;
+        else hi = mid - 1;
+    }
+    const Piece pc = p.pieces[lo];
+    const i64 t = T - pc.tile_base;
+    i64 rt, lgi;
+    if ((u64)t < 0xFFFFFFFFull && (u64)pc.tiles_lane < 0xFFFFFFFFull) {
+        rt = (u32)t / (u32)pc.tiles_lane;
+        lgi = (u32)t - (u32)rt * (u32)pc.tiles_lane;
+    } else {
+        rt = t / pc.tiles_lane;
+        lgi = t - rt * pc.tiles_lane;
+    }
+    const i64 lg = pc.lane_g0 + lgi;
+    i64 row0 = 0;
+    int nv = 1;
+    if (pc.kind != PIECE_UNARY) {
+        const i64 org = (pc.kind == PIECE_RECT && pc.swap) ? pc.j0 : pc.i0;
+        const i64 end = (pc.kind == PIECE_RECT && pc.swap) ? pc.j1 : pc.i1;
+        row0 = org + rt * pc.ti;
+        nv = (int)min((i64)pc.ti, end - row0);
+        if (pc.kind == PIECE_TRI && lg * 32 + 31 <= row0) return;  // tile entirely on/below the diagonal
+    }
+    // a solver with a lower rank than anything in this tile makes the tile irrelevant
+    if (p.check_solve && p.mode == MODE_INSERT) {
+        i64 ci, cj;
+        const i64 lfirst = lg * 32;
+        if (pc.kind == PIECE_UNARY) {
+            ci = max(lfirst, pc.i0);
+            cj = -1;
+        } else if (pc.kind == PIECE_RECT && pc.swap) {
+            ci = max(lfirst, pc.i0);
+            cj = row0;
+        } else if (pc.kind == PIECE_RECT) {
+            ci = row0;
+            cj = max(lfirst, pc.j0);
+        } else {
+            ci = row0;
+            cj = max(lfirst, row0 + 1);
+        }
+        const u64 cmin = piece_rank(pc, ci, cj);
+        const u64 sol = *((volatile u64*)&p.ctl->solver_c);
+        if (sol < cmin) {
+            // the tile's slots stay unwritten: the resolve pass never looks above the solver
+            return;
+        }
+    }
+    const bool xl = pc.swap != 0;
+
+#define LTL_TILE(OP_, TI_, XL_) tile_eval<W, MUELLER, OP_, TI_, XL_>(p, pc, row0, lg, split, lane)
+#define LTL_TILE_TI(OP_, XL_)                       \
+    do {                                            \
+        if (W == 1 && MUELLER) {                    \
+            switch (nv) {                           \
+                case 1: LTL_TILE(OP_, 1, XL_); break; \
+                case 2: LTL_TILE(OP_, 2, XL_); break; \
+                case 3: LTL_TILE(OP_, 3, XL_); break; \
+                default: LTL_TILE(OP_, 4, XL_); break; \
+            }                                       \
+        } else {                                    \
+            LTL_TILE(OP_, 1, XL_);                  \
+        }                                           \
+    } while (0)
+
+    switch (pc.op) {
+        case OP_IDENT: LTL_TILE(OP_IDENT, 1, false); break;
+        case OP_NOT: LTL_TILE(OP_NOT, 1, false); break;
+        case OP_NEXT: LTL_TILE(OP_NEXT, 1, false); break;
+        case OP_FINALLY: LTL_TILE(OP_FINALLY, 1, false); break;
+        case OP_GLOBALLY: LTL_TILE(OP_GLOBALLY, 1, false); break;
+        case OP_AND: LTL_TILE_TI(OP_AND, false); break;
+        case OP_OR: LTL_TILE_TI(OP_OR, false); break;
+        case OP_UNTIL:
+            if (xl) LTL_TILE_TI(OP_UNTIL, true);
+            else LTL_TILE_TI(OP_UNTIL, false);
+            break;
+        default: break;
+    }
+#undef LTL_TILE_TI
+#undef LTL_TILE
+}
+
+// ------------------------------------------------------------------------------------------------
+// phase B kernel
+
+template <int W, int OP>
+__device__ __forceinline__ void mat_rows(const MaterializeParams& p, const bool mine, const i64 dst, const int lhs,
+                                         const int rhs, const int r0, const int r1) {
+    constexpr bool BIN = !(OP == OP_IDENT || OP == OP_NOT || OP == OP_NEXT || OP == OP_FINALLY || OP == OP_GLOBALLY);
+    constexpr bool NEEDM = (OP == OP_NOT || OP == OP_GLOBALLY);
+    if (!mine) return;
+    const i64 n = p.n;
+    const u64* __restrict__ px = p.cms + cm_index(lhs, n, 0);
+    const u64* __restrict__ py = p.cms + cm_index(BIN ? rhs : lhs, n, 0);
+    u64* __restrict__ po = p.cms + cm_index(dst, n, 0);
+#pragma unroll 4
+    for (int r = r0; r < r1; r++) {
+        const size_t kb = (size_t)r * W;
+        u64 x[W], y[W], m[W], out[W];
+#pragma unroll
+        for (int w = 0; w < W; w++) {
+            x[w] = ld_nc(px + (kb + w) * 32);
+            y[w] = BIN ? ld_nc(py + (kb + w) * 32) : 0ull;
+            m[w] = NEEDM ? ld_nc(p.masks + kb + w) : 0ull;
+        }
+        apply_row<OP, W>(out, x, y, m);
+#pragma unroll
+        for (int w = 0; w < W; w++) po[(kb + w) * 32] = out[w];
+    }
+}
+
+template <int W>
+__global__ void __launch_bounds__(LTL_CTA) k_materialize(const __grid_constant__ MaterializeParams p) {
+    const int lane = threadIdx.x & 31;
+    const i64 g = (p.n_base >> 5) + (i64)blockIdx.x * LTL_WARPS_PER_CTA + (threadIdx.x >> 5);
+    const i64 dst = g * 32 + lane;
+    if (g * 32 >= p.n_base + p.count) return;
+    const bool valid = dst >= p.n_base && dst < p.n_base + p.count;
+    const int op = valid ? (int)p.rec_op[dst] : -1;
+    const int lhs = valid ? p.rec_lhs[dst] : 0;
+    const int rhs = valid ? p.rec_rhs[dst] : 0;
+    const int r0 = blockIdx.y * p.rows_per_split;
+    const int r1 = min(p.R, r0 + p.rows_per_split);
+    unsigned remaining = __ballot_sync(0xFFFFFFFFu, valid);
+    while (remaining) {
+        const int leader = __ffs(remaining) - 1;
+        const int cur = __shfl_sync(0xFFFFFFFFu, op, leader);
+        const bool mine = valid && op == cur;
+        remaining &= ~__ballot_sync(0xFFFFFFFFu, mine);
+        switch (cur) {
+            case OP_NOT: mat_rows<W, OP_NOT>(p, mine, dst, lhs, rhs, r0, r1); break;
+            case OP_AND: mat_rows<W, OP_AND>(p, mine, dst, lhs, rhs, r0, r1); break;
+            case OP_OR: mat_rows<W, OP_OR>(p, mine, dst, lhs, rhs, r0, r1); break;
+            case OP_NEXT: mat_rows<W, OP_NEXT>(p, mine, dst, lhs, rhs, r0, r1); break;
+            case OP_FINALLY: mat_rows<W, OP_FINALLY>(p, mine, dst, lhs, rhs, r0, r1); break;
+            case OP_GLOBALLY: mat_rows<W, OP_GLOBALLY>(p, mine, dst, lhs, rhs, r0, r1); break;
+            case OP_UNTIL: mat_rows<W, OP_UNTIL>(p, mine, dst, lhs, rhs, r0, r1); break;
+            default: mat_rows<W, OP_IDENT>(p, mine, dst, lhs, rhs, r0, r1); break;
+        }
+        __syncwarp();
+    }
+}
+
+#endif  // __CUDACC__
+
+// launchers, one translation unit per W (screen_inst.cu compiled with -DLTL_W=<W>)
+typedef void (*screen_launch_fn)(const ScreenParams&, bool mueller, dim3 grid, cudaStream_t stream);
+typedef void (*materialize_launch_fn)(const MaterializeParams&, dim3 grid, cudaStream_t stream);

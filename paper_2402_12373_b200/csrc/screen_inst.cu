@@ -1,0 +1,18 @@
+// screen_inst.cu -- instantiates the hot kernels for one row width; compiled once per W with -DLTL_W=<W>.
+#include "screen.cuh"
+
+#ifndef LTL_W
+#error "compile with -DLTL_W=<words per row>"
+#endif
+
+#define LTL_CAT2(a, b) a##b
+#define LTL_CAT(a, b) LTL_CAT2(a, b)
+
+extern "C" void LTL_CAT(ltl_launch_screen_w, LTL_W)(const ScreenParams& p, bool mueller, dim3 grid, cudaStream_t stream) {
+    if (mueller) k_screen<LTL_W, true><<<grid, LTL_CTA, 0, stream>>>(p);
+    else k_screen<LTL_W, false><<<grid, LTL_CTA, 0, stream>>>(p);
+}
+
+extern "C" void LTL_CAT(ltl_launch_materialize_w, LTL_W)(const MaterializeParams& p, dim3 grid, cudaStream_t stream) {
+    k_materialize<LTL_W><<<grid, LTL_CTA, 0, stream>>>(p);
+}

@@ -1,0 +1,103 @@
+// semantics.cuh -- branch-free LTL connectives on one W-word row of a characteristic matrix.
+//
+// Position j of a trace lives in word j/64 at bit 63 - j%64 (MSB first), so "the suffix starting one
+// step later" is a logical LEFT shift of the whole W-word row; zeros enter from beyond the last word.
+// Temporal operators are O(log n) shift-by-powers-of-two scans with ROUNDS = ceil(log2(64*W)) rounds
+// (reference bitsem.py:107-149 for one word, width-generic form bitsem.py:307-334; _speedups.pyx:291-325).
+// Everything is fully unrolled over compile-time W: shifts >= 64 become register renames, shifts < 64
+// funnel shifts with the neighbouring word (the multi-word carry).
+#pragma once
+#include "common.cuh"
+
+template <int W>
+struct Rounds {
+    static constexpr int value = (64 * W <= 64) ? 6 : (64 * W <= 128) ? 7 : (64 * W <= 256) ? 8 : (64 * W <= 512) ? 9 : 10;
+};
+static_assert(LTL_MAX_W <= 16, "Rounds<> covers rows of up to 1024 positions");
+
+// word w of (a << S), row-wide
+template <int W, int S>
+__device__ __forceinline__ u64 shl_word(const u64 (&a)[W], int w) {
+    constexpr int q = S >> 6, r = S & 63;
+    u64 lo = (w + q < W) ? a[w + q] : 0ull;
+    if (r == 0) return lo;
+    u64 hi = (w + q + 1 < W) ? a[w + q + 1] : 0ull;
+    return (lo << r) | (hi >> ((64 - r) & 63));
+}
+
+// c |= c << 2^I for I = 0..ROUNDS-1 (in place; ascending w only reads words >= w, i.e. old values)
+template <int W, int I, int ROUNDS>
+struct SmearOr {
+    static __device__ __forceinline__ void run(u64 (&c)[W]) {
+#pragma unroll
+        for (int w = 0; w < W; w++) c[w] |= shl_word<W, (1 << I)>(c, w);
+        SmearOr<W, I + 1, ROUNDS>::run(c);
+    }
+};
+template <int W, int ROUNDS>
+struct SmearOr<W, ROUNDS, ROUNDS> {
+    static __device__ __forceinline__ void run(u64 (&)[W]) {}
+};
+
+// acc |= run & (acc << s); run &= run << s   (last run update is dead: reference _speedups.pyx:321-324)
+template <int W, int I, int ROUNDS>
+struct UntilRounds {
+    static __device__ __forceinline__ void run(u64 (&acc)[W], u64 (&rn)[W]) {
+#pragma unroll
+        for (int w = 0; w < W; w++) acc[w] |= rn[w] & shl_word<W, (1 << I)>(acc, w);
+        if (I + 1 < ROUNDS) {
+#pragma unroll
+            for (int w = 0; w < W; w++) rn[w] &= shl_word<W, (1 << I)>(rn, w);
+        }
+        UntilRounds<W, I + 1, ROUNDS>::run(acc, rn);
+    }
+};
+template <int W, int ROUNDS>
+struct UntilRounds<W, ROUNDS, ROUNDS> {
+    static __device__ __forceinline__ void run(u64 (&)[W], u64 (&)[W]) {}
+};
+
+// out = OP(x [, y]) on one row; m = the row's length mask (used by NOT / GLOBALLY only).
+// x is the left (or only) operand, y the right operand.
+template <int OP, int W>
+__device__ __forceinline__ void apply_row(u64 (&out)[W], const u64 (&x)[W], const u64 (&y)[W], const u64 (&m)[W]) {
+    if (OP == OP_IDENT) {
+#pragma unroll
+        for (int w = 0; w < W; w++) out[w] = x[w];
+    } else if (OP == OP_NOT) {
+#pragma unroll
+        for (int w = 0; w < W; w++) out[w] = ~x[w] & m[w];
+    } else if (OP == OP_AND) {
+#pragma unroll
+        for (int w = 0; w < W; w++) out[w] = x[w] & y[w];
+    } else if (OP == OP_OR) {
+#pragma unroll
+        for (int w = 0; w < W; w++) out[w] = x[w] | y[w];
+    } else if (OP == OP_NEXT) {
+#pragma unroll
+        for (int w = 0; w < W; w++) out[w] = shl_word<W, 1>(x, w);
+    } else if (OP == OP_FINALLY) {
+#pragma unroll
+        for (int w = 0; w < W; w++) out[w] = x[w];
+        SmearOr<W, 0, Rounds<W>::value>::run(out);
+    } else if (OP == OP_GLOBALLY) {  // dual of F inside the mask (reference bitsem.py:133-138)
+#pragma unroll
+        for (int w = 0; w < W; w++) out[w] = ~x[w] & m[w];
+        SmearOr<W, 0, Rounds<W>::value>::run(out);
+#pragma unroll
+        for (int w = 0; w < W; w++) out[w] = ~out[w] & m[w];
+    } else {  // OP_UNTIL
+        u64 rn[W];
+#pragma unroll
+        for (int w = 0; w < W; w++) {
+            out[w] = y[w];
+            rn[w] = x[w];
+        }
+        UntilRounds<W, 0, Rounds<W>::value>::run(out, rn);
+    }
+}
+
+__host__ __device__ __forceinline__ bool op_is_unary(int op) {
+    return op == OP_IDENT || op == OP_NOT || op == OP_NEXT || op == OP_FINALLY || op == OP_GLOBALLY;
+}
+__host__ __device__ __forceinline__ bool op_needs_mask(int op) { return op == OP_NOT || op == OP_GLOBALLY; }

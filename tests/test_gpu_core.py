@@ -1,0 +1,304 @@
+"""GPU parity tests: the CUDA screening core (through the C ABI, via ctypes) against the CPU oracle and
+the reference-generated golden fixtures.  Bit-exact: matrices, records, counters, statuses, fingerprints."""
+import numpy as np
+import pytest
+
+from helpers import (cfg_from_golden, golden, oracle_factory, random_spec, records_array, sha, spec_from_golden,
+                     unhex)
+from oracle import cpu_oracle
+from paper_2402_12373_b200 import learner as L
+from paper_2402_12373_b200.core import CudaCore, V_FKP, V_GATHER, V_MUELLER
+from paper_2402_12373_b200.errors import CoreOOM
+from paper_2402_12373_b200.formula import print_formula
+from paper_2402_12373_b200.packing import length_masks
+
+pytestmark = pytest.mark.gpu
+
+UNARY = (1, 4, 5, 6)
+
+
+def assert_same_state(cuda, ora):
+    assert cuda.counters() == ora._counters()
+    n = ora.n_entries
+    if n:
+        assert (cuda.export_cms() == ora.export_cms()).all()
+        assert (records_array(cuda) == records_array(ora)).all()
+
+
+def make_pair(masks, n_pos, err_max=0, variant=V_MUELLER, pr=(), po=(), fkp=0, mask_k=0, budget=1 << 30, W=1, **opt):
+    cuda = CudaCore(masks, n_pos, err_max, variant, pr, po, fkp, mask_k, budget, words_per_row=W, **opt)
+    ora = cpu_oracle.OracleCore(masks, n_pos, err_max, variant, pr, po, fkp, mask_k, budget, words_per_row=W, threads=4)
+    return cuda, ora
+
+
+def random_masks(rng, R, W, full=False):
+    lengths = np.full(R, 64 * W) if full else rng.integers(1, 64 * W + 1, size=R)
+    return length_masks(lengths, W).reshape(-1)
+
+
+def random_cm(rng, masks):
+    a = rng.integers(0, 1 << 63, size=len(masks), dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, size=len(masks), dtype=np.uint64)
+    return a & masks
+
+
+def drive(cuda, ora, rng, n_seed=5, rounds=2):
+    """Same call sequence on both cores; every return value must agree."""
+    masks = ora_masks = None  # noqa
+    for k in range(n_seed):
+        cm = random_cm(rng, drive.masks)
+        assert cuda.add_entry(cm, 0, k, -1) == ora.add_entry(cm, 0, k, -1)
+    lo = 0
+    for _ in range(rounds):
+        hi = ora.n_entries
+        for op in UNARY:
+            assert cuda.screen_unary(op, lo, hi) == ora.screen_unary(op, lo, hi)
+        for op, tri in ((2, True), (3, True), (7, False)):
+            assert cuda.screen_binary(op, 0, hi, 0, hi, tri) == ora.screen_binary(op, 0, hi, 0, hi, tri)
+        mid = ora.n_entries
+        assert cuda.screen_binary(7, hi, mid, 0, hi, False) == ora.screen_binary(7, hi, mid, 0, hi, False)
+        assert cuda.screen_binary(2, 1, hi, 0, mid, True) == ora.screen_binary(2, 1, hi, 0, mid, True)
+        lo = hi
+        if ora.n_entries > 6000:
+            break
+
+
+@pytest.mark.parametrize("R,W", [(2, 1), (16, 1), (64, 1), (65, 1), (200, 1), (1024, 1), (7, 2), (33, 3), (20, 4),
+                                 (9, 5), (12, 7), (40, 8), (5, 11), (24, 16), (130, 16)])
+def test_differential_random(R, W):
+    rng = np.random.default_rng(1000 * R + W)
+    masks = random_masks(rng, R, W)
+    n_pos = int(rng.integers(1, R)) if R > 1 else 1
+    cuda, ora = make_pair(masks, n_pos, err_max=-1, W=W)  # err_max -1: nothing ever solves
+    drive.masks = masks
+    drive(cuda, ora, rng, n_seed=4, rounds=2 if R * W <= 2048 else 1)
+    assert_same_state(cuda, ora)
+    cm = random_cm(rng, masks)
+    assert cuda.fingerprint_of(cm) == ora.fingerprint_of(cm)
+    assert cuda.contains(cm) == ora.contains(cm)
+    e = ora.get_cm(ora.n_entries // 2)
+    assert cuda.contains(e) and ora.contains(e)
+    assert (cuda.get_cm(ora.n_entries // 2) == e).all()
+    assert cuda.get_record(3) == ora.get_record(3)
+    cuda.close()
+
+
+@pytest.mark.parametrize("R,W,split,chunk", [(200, 1, 3, 97), (1024, 1, 16, 1000), (130, 16, 2, 333), (64, 3, 1, 50),
+                                             (300, 2, 4, 1 << 20)])
+def test_differential_split_and_chunked(R, W, split, chunk):
+    """Row-split evaluation (partial fingerprints combined by atomics) and tiny chunks (rows cut mid-way)."""
+    rng = np.random.default_rng(77 * R + W)
+    masks = random_masks(rng, R, W)
+    cuda, ora = make_pair(masks, R // 2, err_max=-1, W=W, chunk_candidates=chunk)
+    cuda.set_option("force_split", split)
+    drive.masks = masks
+    drive(cuda, ora, rng, n_seed=4, rounds=1)
+    assert_same_state(cuda, ora)
+    cuda.close()
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_solver_and_counters(seed):
+    """First solver in enumeration order wins; counters stop at the solver (reference _speedups.pyx:372-374)."""
+    rng = np.random.default_rng(500 + seed)
+    R, W = (24, 1) if seed % 2 == 0 else (12, 2)
+    masks = random_masks(rng, R, W)
+    n_pos = R // 2
+    err_max = R // 2 - 2 - seed % 3  # loose enough that something solves early
+    cuda, ora = make_pair(masks, n_pos, err_max=err_max, W=W, chunk_candidates=[1 << 20, 64][seed % 2])
+    drive.masks = masks
+    for k in range(4):
+        cm = random_cm(rng, masks)
+        assert cuda.add_entry(cm, 0, k, -1) == ora.add_entry(cm, 0, k, -1)
+    statuses = []
+    lo = 0
+    for _ in range(3):
+        hi = ora.n_entries
+        for op in UNARY:
+            a, b = cuda.screen_unary(op, lo, hi), ora.screen_unary(op, lo, hi)
+            assert a == b
+            statuses.append(a[0])
+        for op, tri in ((2, True), (3, True), (7, False)):
+            a, b = cuda.screen_binary(op, 0, hi, 0, hi, tri), ora.screen_binary(op, 0, hi, 0, hi, tri)
+            assert a == b
+            statuses.append(a[0])
+        assert_same_state(cuda, ora)
+        lo = hi
+    assert 1 in statuses, "test should exercise the SOLVED path"
+    cuda.close()
+
+
+def test_budget_oom_matches_oracle():
+    rng = np.random.default_rng(9)
+    R = 32
+    masks = random_masks(rng, R, 1)
+    eb = 8 * R + 16
+    for cap in (1, 3, 10, 57):
+        cuda, ora = make_pair(masks, 16, err_max=-1, budget=cap * eb + 5, chunk_candidates=40)
+        for k in range(5):
+            cm = random_cm(rng, masks)
+            try:
+                want = ora.add_entry(cm, 0, k, -1)
+            except cpu_oracle.CoreOOM:
+                with pytest.raises(CoreOOM):
+                    cuda.add_entry(cm, 0, k, -1)
+                continue
+            assert cuda.add_entry(cm, 0, k, -1) == want
+        n0 = ora.n_entries
+        for op in UNARY:
+            assert cuda.screen_unary(op, 0, n0) == ora.screen_unary(op, 0, n0)
+        assert cuda.screen_binary(7, 0, n0, 0, n0, False) == ora.screen_binary(7, 0, n0, 0, n0, False)
+        assert_same_state(cuda, ora)
+        cuda.close()
+
+
+def test_fingerprint_golden():
+    for case in golden()["fpvec"]:
+        cuda = CudaCore(unhex(case["masks"]), 1, 0, case["variant"], case["proj_rows"], case["proj_offs"],
+                        case["fkp_bits"], case["mask_k"])
+        for cm, fp in zip(case["cms"], case["fps"]):
+            assert cuda.fingerprint_of(unhex(cm)) == int(fp, 16)
+        cuda.close()
+
+
+def test_operator_golden_vectors():
+    names = {1: "not", 2: "and", 3: "or", 4: "next", 5: "finally", 6: "globally", 7: "until"}
+    for case in golden()["opvec"]:
+        masks = unhex(case["masks"])
+        cuda = CudaCore(masks, case["n_pos"], -1, V_MUELLER)
+        x, y = unhex(case["x"]), unhex(case["y"])
+        assert cuda.add_entry(x, 0, 0, -1) == 0
+        iy = cuda.add_entry(y, 0, 1, -1)
+        if iy < 0:
+            cuda.close()
+            continue
+        for op in UNARY:
+            cuda.screen_unary(op, 0, 1)
+        for op in (2, 3, 7):
+            cuda.screen_binary(op, 0, 1, 1, 2, False)
+        op_arr, lhs, rhs = cuda.export_records()
+        cms = cuda.export_cms()
+        for e in range(2, len(op_arr)):
+            assert (cms[e] == unhex(case[names[int(op_arr[e])]])).all(), names[int(op_arr[e])]
+        cuda.close()
+
+
+def test_transcripts_golden():
+    from test_oracle_golden import _replay_transcript
+
+    for tr in golden()["transcripts"]:
+        cuda = CudaCore(unhex(tr["masks"]), tr["n_pos"], 0, V_MUELLER, budget_bytes=1 << 24)
+        _replay_transcript(cuda, tr)
+        assert cuda.counters() == tr["counters"]
+        assert sha(cuda.export_cms()) == tr["cms_sha"]
+        assert sha(records_array(cuda)) == tr["records_sha"]
+        cuda.close()
+
+
+@pytest.mark.parametrize("case", golden()["learn"], ids=lambda c: c["name"])
+def test_learn_golden_cases(case):
+    """The product path end to end (learner -> C ABI -> CUDA) against the reference's recorded outcomes."""
+    spec, alphabet = spec_from_golden(case)
+    cfg = cfg_from_golden(case["cfg"])
+    cores = []
+    from paper_2402_12373_b200.core import make_core
+
+    def factory(*a, **kw):
+        cores.append(make_core(*a, **kw))
+        real_close = cores[-1].close
+        cores[-1].close = lambda: None
+        cores[-1]._real_close = real_close
+        return cores[-1]
+
+    out = L.enum_learn(spec, alphabet, cfg, core_factory=factory)
+    assert type(out).__name__ == case["outcome"]
+    st = out.stats.as_dict()
+    for k, v in case["stats"].items():
+        assert st[k] == v, k
+    got_levels = [{k: v for k, v in lv.items() if k != "ms"} for lv in out.stats.levels]
+    assert got_levels == case["levels"]
+    if case["outcome"] == "Solved":
+        assert print_formula(out.formula, alphabet) == case["formula"]
+        assert out.cost == case["cost"]
+    if "core" in case and cores:
+        core, g = cores[-1], case["core"]
+        assert core.n_entries == g["n_entries"]
+        assert sha(core.export_cms()) == g["cms_sha"]
+        assert sha(records_array(core)) == g["records_sha"]
+    for c in cores:
+        c._real_close()
+
+
+@pytest.mark.parametrize("n_props,n_pos,n_neg,length,max_cost,chunk", [
+    (3, 512, 512, 64, 6, None),      # BASELINE config 2 shape (one full word per trace)
+    (3, 256, 256, 1024, 4, None),    # BASELINE config 3 shape (16 words per row)
+    (3, 40, 40, 200, 5, 5000),       # 4 words per row, chunked
+    (5, 100, 100, 64, 4, None),
+])
+def test_learn_matches_oracle_beyond_reference_limits(n_props, n_pos, n_neg, length, max_cost, chunk):
+    rng = np.random.default_rng(n_props * 1000 + n_pos)
+    spec, alphabet = random_spec(rng, n_props, n_pos, n_neg, length, length)
+    want = L.learn(spec, None, alphabet, max_cost=max_cost, core_factory=oracle_factory(8), overfit_on_ceiling=False,
+                   budget_bytes=8 << 30)
+    opts = {} if chunk is None else {"chunk_candidates": chunk}
+    from paper_2402_12373_b200.core import make_core
+
+    cores = []
+
+    def factory(*a, **kw):
+        cores.append(make_core(*a, **kw, **opts))
+        rc = cores[-1].close
+        cores[-1].close = lambda: None
+        cores[-1]._real_close = rc
+        return cores[-1]
+
+    got = L.learn(spec, None, alphabet, max_cost=max_cost, core_factory=factory, overfit_on_ceiling=False,
+                  budget_bytes=8 << 30)
+    assert got.status == want.status
+    assert got.text == want.text and got.cost == want.cost
+    a, b = got.stats.as_dict(), want.stats.as_dict()
+    for lv in a["levels"] + b["levels"]:
+        lv.pop("ms", None)
+    assert a == b
+    for c in cores:
+        c._real_close()
+
+
+def test_many_rows_row_split():
+    """BASELINE config 4 shape, scaled: many short traces => row-split evaluation with combined fingerprints."""
+    rng = np.random.default_rng(4)
+    R = 1 << 14
+    masks = random_masks(rng, R, 1)
+    cuda, ora = make_pair(masks, R // 2, err_max=-1, budget=4 << 30)
+    drive.masks = masks
+    for k in range(4):
+        cm = random_cm(rng, masks)
+        assert cuda.add_entry(cm, 0, k, -1) == ora.add_entry(cm, 0, k, -1)
+    n0 = ora.n_entries
+    for op in UNARY:
+        assert cuda.screen_unary(op, 0, n0) == ora.screen_unary(op, 0, n0)
+    n1 = ora.n_entries
+    assert cuda.screen_binary(2, 0, n1, 0, n1, True) == ora.screen_binary(2, 0, n1, 0, n1, True)
+    assert cuda.screen_binary(7, 0, n0, 0, n1, False) == ora.screen_binary(7, 0, n0, 0, n1, False)
+    assert cuda.counters() == ora._counters()
+    hi, lo = cuda.entry_fingerprints()
+    for e in (0, n0, ora.n_entries - 1):
+        assert (int(hi[e]) << 64 | int(lo[e])) == ora.fingerprint_of(ora.get_cm(e))
+        assert (cuda.get_cm(e) == ora.get_cm(e)).all()
+    assert sha(cuda.export_cms()) == sha(ora.export_cms())
+    cuda.close()
+
+
+def test_argument_errors():
+    masks = np.full(4, 2**64 - 1, dtype=np.uint64)
+    with pytest.raises(ValueError):
+        CudaCore(masks, 1, 0, V_GATHER, list(range(127)), [0] * 127)
+    with pytest.raises(ValueError):
+        CudaCore(masks, 1, 0, V_MUELLER, words_per_row=17)
+    core = CudaCore(masks, 2, 0, V_MUELLER)
+    with pytest.raises(ValueError):
+        core.add_entry(np.zeros(3, dtype=np.uint64), 0, 0, -1)
+    with pytest.raises(IndexError):
+        core.get_cm(0)
+    with pytest.raises(ValueError):
+        core.screen_unary(1, 0, 5)
+    core.close()
