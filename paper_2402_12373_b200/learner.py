@@ -99,6 +99,8 @@ class EnumStats:
     atom_fast_path: bool = False
     levels: list = field(default_factory=list)
     search_seconds: float = 0.0
+    h2d_bytes: int = 0  # host->device / device->host bytes moved by the device core for this search
+    d2h_bytes: int = 0
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k in ("offered", "admitted", "duplicates", "peak_bytes", "precise",
@@ -217,72 +219,102 @@ def _run_level(core, segs: list[Segment], cfg: LearnerConfig):
     return None
 
 
-def enum_learn(spec: Specification, alphabet: Alphabet, cfg: LearnerConfig | None = None, *,
-               core_factory: Callable | None = None) -> EnumOutcome:
-    """Learn a separating formula, or report OOM / fall back to the overfitting formula."""
-    cfg = cfg or LearnerConfig()
-    _validate(spec, alphabet, cfg)
-    ctx = TraceContext.from_spec(spec, alphabet)
-    n_pos, err_max, h = spec.n_pos, cfg.err_max(spec), cfg.cost
-    stats = EnumStats()
-    stats.ceiling = overfit_cost(spec, alphabet, h)
-    ceiling = stats.ceiling if cfg.ceiling is None else min(cfg.ceiling, stats.ceiling)
+class Enumeration:
+    """One bottom-up search, split into `__init__` (validate, pack, atom fast path, create the device core,
+    admit the atoms -- everything up to "inputs resident in HBM") and `run` (the cost-level loop)."""
 
-    atom_c = h.of(OP_ATOM)
-    for p in range(alphabet.size):
-        if _host_error_count(ctx.atoms[p], n_pos) <= err_max:
-            stats.atom_fast_path = True
-            return Solved(Atom(p), atom_c, stats)
-    if cfg.require_nnf:
+    def __init__(self, spec: Specification, alphabet: Alphabet, cfg: LearnerConfig | None = None, *,
+                 core_factory: Callable | None = None):
+        cfg = cfg or LearnerConfig()
+        _validate(spec, alphabet, cfg)
+        self.spec, self.alphabet, self.cfg = spec, alphabet, cfg
+        self.ctx = ctx = TraceContext.from_spec(spec, alphabet)
+        n_pos, err_max, h = spec.n_pos, cfg.err_max(spec), cfg.cost
+        self.stats = stats = EnumStats()
+        stats.ceiling = overfit_cost(spec, alphabet, h)
+        self.ceiling = stats.ceiling if cfg.ceiling is None else min(cfg.ceiling, stats.ceiling)
+        self.outcome: EnumOutcome | None = None
+        self.core = None
+        self.cache = None
+
+        atom_c = h.of(OP_ATOM)
         for p in range(alphabet.size):
-            if _host_error_count(~ctx.atoms[p] & ctx.masks, n_pos) <= err_max:
+            if _host_error_count(ctx.atoms[p], n_pos) <= err_max:
                 stats.atom_fast_path = True
-                return Solved(Not(Atom(p)), atom_c + h.of(OP_NOT), stats)
+                self.outcome = Solved(Atom(p), atom_c, stats)
+                return
+        if cfg.require_nnf:
+            for p in range(alphabet.size):
+                if _host_error_count(~ctx.atoms[p] & ctx.masks, n_pos) <= err_max:
+                    stats.atom_fast_path = True
+                    self.outcome = Solved(Not(Atom(p)), atom_c + h.of(OP_NOT), stats)
+                    return
 
-    rs = resolve_scheme(cfg.hash, ctx.lengths, SuffixTable.from_spec(spec, limit=126))
-    stats.precise = rs.precise
-    if core_factory is None:
-        from .core import make_core as core_factory  # CUDA core; raises BackendUnavailable
-    core = core_factory(ctx.masks, n_pos, err_max, rs.variant, rs.proj_rows, rs.proj_offs, rs.fkp_bits, rs.mask_k,
-                        cfg.budget_bytes, words_per_row=ctx.words, device=cfg.device)
-    cache = LanguageCache(core)
-    t_search = time.perf_counter()
+        rs = resolve_scheme(cfg.hash, ctx.lengths, SuffixTable.from_spec(spec, limit=126))
+        stats.precise = rs.precise
+        if core_factory is None:
+            from .core import make_core as core_factory  # CUDA core; raises BackendUnavailable
+        self.core = core_factory(ctx.masks, n_pos, err_max, rs.variant, rs.proj_rows, rs.proj_offs, rs.fkp_bits,
+                                 rs.mask_k, cfg.budget_bytes, words_per_row=ctx.words, device=cfg.device)
+        self.cache = cache = LanguageCache(self.core)
+        self._t_search = time.perf_counter()
+        try:
+            admitted_atoms = [p for p in range(alphabet.size)
+                              if cache.try_admit(ctx.atoms[p], (OP_ATOM, p, -1), atom_c)]
+            if cfg.require_nnf:
+                neg_c = atom_c + h.of(OP_NOT)
+                for entry, p in enumerate(admitted_atoms):
+                    cache.try_admit(~ctx.atoms[p] & ctx.masks, (OP_NOT, entry, -1), neg_c)
+        except CoreOOM:
+            self.outcome = self._finish(OutOfMemory(stats))
 
-    def finish(outcome):
+    def _finish(self, outcome):
+        core, stats = self.core, self.stats
         _, bytes_used, stats.offered, stats.admitted, stats.duplicates = core.counters()
         stats.peak_bytes = bytes_used
-        stats.levels = cache.stats_rows()
-        stats.search_seconds = time.perf_counter() - t_search
-        close = getattr(core, "close", None)
-        if close:
-            close()
+        stats.levels = self.cache.stats_rows()
+        stats.search_seconds = time.perf_counter() - self._t_search
+        if hasattr(core, "transfer_stats"):
+            stats.h2d_bytes, stats.d2h_bytes = core.transfer_stats()
+        if not self.keep_core:
+            close = getattr(core, "close", None)
+            if close:
+                close()
         return outcome
 
-    try:
-        admitted_atoms = [p for p in range(alphabet.size) if cache.try_admit(ctx.atoms[p], (OP_ATOM, p, -1), atom_c)]
-        if cfg.require_nnf:
-            neg_c = atom_c + h.of(OP_NOT)
-            for entry, p in enumerate(admitted_atoms):
-                cache.try_admit(~ctx.atoms[p] & ctx.masks, (OP_NOT, entry, -1), neg_c)
-    except CoreOOM:
-        return finish(OutOfMemory(stats))
+    keep_core = False
 
-    ops = enabled_ops(cfg)
-    for c in range(atom_c + 1, ceiling):
-        _check_deadline(cfg)
-        t0 = time.perf_counter()
-        cache.begin_level(c)
-        hit = _run_level(core, level_segments(cache, cfg, ops, c), cfg)
-        if hit is not None:
-            status, op, li, ri = hit
-            if status == S_OOM:
-                return finish(OutOfMemory(stats))
-            formula = cache.build_candidate(op, li, ri)
+    def run(self) -> EnumOutcome:
+        if self.outcome is not None:
+            return self.outcome
+        cfg, cache, core, stats = self.cfg, self.cache, self.core, self.stats
+        ops = enabled_ops(cfg)
+        atom_c = cfg.cost.of(OP_ATOM)
+        for c in range(atom_c + 1, self.ceiling):
+            _check_deadline(cfg)
+            t0 = time.perf_counter()
+            cache.begin_level(c)
+            hit = _run_level(core, level_segments(cache, cfg, ops, c), cfg)
+            if hit is not None:
+                status, op, li, ri = hit
+                if status == S_OOM:
+                    self.outcome = self._finish(OutOfMemory(stats))
+                    return self.outcome
+                formula = cache.build_candidate(op, li, ri)
+                cache.end_level(c)
+                self.outcome = self._finish(Solved(formula, c, stats))
+                return self.outcome
             cache.end_level(c)
-            return finish(Solved(formula, c, stats))
-        cache.end_level(c)
-        cache._rows[-1]["ms"] = round((time.perf_counter() - t0) * 1e3, 3)
-    return finish(CeilingReached(spec, alphabet, ceiling, stats))
+            cache._rows[-1]["ms"] = round((time.perf_counter() - t0) * 1e3, 3)
+        self.outcome = self._finish(CeilingReached(self.spec, self.alphabet, self.ceiling, stats))
+        return self.outcome
+
+
+def enum_learn(spec: Specification, alphabet: Alphabet, cfg: LearnerConfig | None = None, *,
+               core_factory: Callable | None = None) -> EnumOutcome:
+    """Learn a separating formula, or report OOM / fall back to the overfitting formula (reference
+    `enumerator.py:159-251`)."""
+    return Enumeration(spec, alphabet, cfg, core_factory=core_factory).run()
 
 
 # ---------------------------------------------------------------------------------- learn()

@@ -151,7 +151,7 @@ def random_spec(n_props: int, n_pos: int, n_neg: int, min_len: int, max_len: int
 #: The five BASELINE.json configurations as concrete, seeded workloads.  `formula` is the planted formula,
 #: `max_cost` the inclusive search bound used by bench.py / the tests.
 CONFIGS = {
-    "c1_tiny": dict(n_props=2, n_pos=8, n_neg=8, min_len=4, max_len=16, formula="(p0 U p1) & F(G p0)", seed=3, max_cost=10),
+    "c1_tiny": dict(n_props=2, n_pos=8, n_neg=8, min_len=4, max_len=16, formula="(p0 U p1) & F(G p0)", seed=1, max_cost=10),
     "c2_planted": dict(n_props=3, n_pos=512, n_neg=512, min_len=64, max_len=64,
                        formula="(p0 U (p1 & X p2)) & X(p1 | p2)", seed=2402, max_cost=12),
     "c3_long": dict(n_props=3, n_pos=256, n_neg=256, min_len=1024, max_len=1024, formula="p0 U (p1 & X(p2 U p0))", seed=12373,
