@@ -222,7 +222,7 @@ def main():
     torch.cuda.synchronize()
     sampler.start()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    kstats = []
+    kstats, host_times, close_ms = [], [], 0.0
     launches = 0
     torch.cuda.synchronize()
     ev0.record()
@@ -230,7 +230,10 @@ def main():
     for en in searches:
         en.run()
         kstats.append(en.core.kernel_stats())
+        host_times.append(en.core.host_times())
+        tc = time.perf_counter()
         en.core.close()
+        close_ms += 1e3 * (time.perf_counter() - tc)
         flush.fill_(1)  # L2 flush between timed iterations
     ev1.record()
     torch.cuda.synchronize()
@@ -304,6 +307,10 @@ def main():
         "time_to_formula_ms": e2e_ms / args.steps, "formula": text, "cost": res.cost,
         "candidates_per_step": offered_per_step, "unique_cs_per_step": res.stats.admitted,
         "wall_ms_per_step": 1e3 * wall / args.steps,
+        "host_ms_per_step": {"grow": sum(h["grow_ms"] for h in host_times) / args.steps,
+                             "device_wait": sum(h["sync_ms"] for h in host_times) / args.steps,
+                             "close": close_ms / args.steps},
+        "levels": [[lv["cost"], lv["offered"], lv["admitted"], lv.get("ms")] for lv in res.stats.levels],
     }
     print(json.dumps(line))
 

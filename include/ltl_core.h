@@ -140,6 +140,8 @@ LTL_API int ltl_core_kernel_stats(ltl_core* h, int kernel_class, uint64_t* launc
 LTL_API int ltl_core_reset_kernel_stats(ltl_core* h);
 /* The CUDA stream (cudaStream_t) every kernel and copy of this handle is issued on, for CUDA-event timing. */
 LTL_API int ltl_core_stream(ltl_core* h, void** stream_out);
+/* out[0..2] = host wall milliseconds spent growing the store, waiting for the device, planning chunks. */
+LTL_API int ltl_core_host_times(ltl_core* h, double out[3]);
 /* out[0..1] = bytes copied host->device / device->host by this handle so far. */
 LTL_API int ltl_core_transfer_stats(ltl_core* h, uint64_t out[2]);
 /* out[0..5] = effective entry capacity, device bytes mapped for matrices, table slots, chunk candidates,

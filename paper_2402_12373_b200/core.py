@@ -81,6 +81,8 @@ def load_library():
     L.ltl_core_info.argtypes = [vp, u64p]
     L.ltl_core_stream.argtypes = [vp, C.POINTER(vp)]
     L.ltl_core_transfer_stats.argtypes = [vp, u64p]
+    L.ltl_core_host_times.argtypes = [vp, C.POINTER(C.c_double)]
+    L.ltl_core_host_times.restype = C.c_int
     for name in ("ltl_core_create", "ltl_core_add_entry", "ltl_core_screen_unary", "ltl_core_screen_binary",
                  "ltl_core_run_level", "ltl_core_contains", "ltl_core_fingerprint_of", "ltl_core_get_cm",
                  "ltl_core_get_record", "ltl_core_export_cms", "ltl_core_export_records",
@@ -285,6 +287,12 @@ class CudaCore:
         out = C.c_void_p()
         self._check(self._L.ltl_core_stream(self._h, C.byref(out)))
         return int(out.value or 0)
+
+    def host_times(self) -> dict:
+        """Host wall milliseconds: growing the store, waiting for the device, planning."""
+        out = (C.c_double * 3)()
+        self._check(self._L.ltl_core_host_times(self._h, out))
+        return {"grow_ms": out[0], "sync_ms": out[1], "plan_ms": out[2]}
 
     def transfer_stats(self) -> tuple[int, int]:
         """(host->device bytes, device->host bytes) copied so far."""

@@ -12,6 +12,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -400,6 +401,7 @@ struct ltl_core {
     u64* h_stage = nullptr;  // pinned, n words
     u64 n_entries = 0, offered = 0, admitted = 0, duplicates = 0;
     u64 h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic of this handle
+    double grow_ms = 0, sync_ms = 0, plan_ms = 0;  // host wall time: store growth, waiting for the device, planning
     int sm_count = 148;
     int max_split = 4096, force_split = 0;
     bool profile = false;
@@ -546,7 +548,15 @@ static int ensure_pieces(ltl_core* h, int n) {
     return LTL_OK;
 }
 
+struct HostTimer {
+    double* acc;
+    std::chrono::steady_clock::time_point t0;
+    explicit HostTimer(double* a) : acc(a), t0(std::chrono::steady_clock::now()) {}
+    ~HostTimer() { *acc += std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); }
+};
+
 static int ensure_entries(ltl_core* h, u64 entries) {  // matrices + records for `entries` entries
+    HostTimer ht(&h->grow_ms);
     const u64 groups = (entries + 31) / 32;
     if (h->cms.ensure((size_t)groups * 32 * (size_t)h->n * 8, h->stream) || h->rec_op.ensure((size_t)groups * 32, h->stream) ||
         h->rec_lhs.ensure((size_t)groups * 32 * 4, h->stream) || h->rec_rhs.ensure((size_t)groups * 32 * 4, h->stream)) {
@@ -763,7 +773,10 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
         }
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(h->h_ctl, h->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
-        CK(cudaStreamSynchronize(h->stream));
+        {
+            HostTimer ht(&h->sync_ms);
+            CK(cudaStreamSynchronize(h->stream));
+        }
         h->d2h_bytes += sizeof(Ctl);
     }
     const u64 solver_c = h->h_ctl->solver_c;
@@ -1335,6 +1348,14 @@ int ltl_core_reset_kernel_stats(ltl_core* h) {
 int ltl_core_stream(ltl_core* h, void** stream_out) {
     if (!h || !stream_out) return LTL_ERR_ARG;
     *stream_out = (void*)h->stream;
+    return LTL_OK;
+}
+
+int ltl_core_host_times(ltl_core* h, double out[3]) {
+    if (!h || !out) return LTL_ERR_ARG;
+    out[0] = h->grow_ms;
+    out[1] = h->sync_ms;
+    out[2] = h->plan_ms;
     return LTL_OK;
 }
 
