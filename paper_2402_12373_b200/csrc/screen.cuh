@@ -99,16 +99,56 @@ __device__ __forceinline__ void finish_candidate(const ScreenParams& p, u64 c, u
 }
 
 // ------------------------------------------------------------------------------------------------
+// per-warp asynchronous staging of the lane operand: in the group layout the 32 lanes' words k, k+1, ... of
+// one storage group are ONE contiguous stream of 256-byte lines, so a warp prefetches it with 1-D bulk
+// copies (TMA engine, cp.async.bulk) into its private shared-memory ring, completion on an mbarrier.
+
+template <int W>
+struct Ring {
+    static constexpr int RPC = (W <= 8) ? 8 / W : 1;      // rows per stage
+    static constexpr int STAGES = (W <= 8) ? 3 : 2;
+    static constexpr int STAGE_U64 = RPC * W * 32;         // 64-bit words per stage (<= 2 KiB for W <= 8)
+    static constexpr int WARP_U64 = STAGES * STAGE_U64;
+    static constexpr int CTA_BYTES = LTL_WARPS_PER_CTA * WARP_U64 * 8 + LTL_WARPS_PER_CTA * STAGES * 8;
+    static constexpr bool CHUNK_FOLD = (64 % (RPC * W)) == 0;  // hash blocks end on stage boundaries
+};
+
+__device__ __forceinline__ u32 smem_u32(const void* p) { return (u32)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(u64* bar, u32 count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(u64* bar, u32 bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, u32 bytes, u64* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "LAB_WAIT:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@p bra LAB_DONE;\n\t"
+        "bra LAB_WAIT;\n\t"
+        "LAB_DONE:\n\t}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+
+// ------------------------------------------------------------------------------------------------
 // one warp tile
 
 template <int W, bool MUELLER, int OP, int TI, bool XL>
 __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc, const i64 row0, const i64 lg,
-                                          const int split, const int lane) {
+                                          const int split, const int lane, u64* __restrict__ sbuf, u64* bars) {
     constexpr bool BIN = !(OP == OP_IDENT || OP == OP_NOT || OP == OP_NEXT || OP == OP_FINALLY || OP == OP_GLOBALLY);
     constexpr bool NEEDM = (OP == OP_NOT || OP == OP_GLOBALLY);
     const i64 n = p.n;
     const i64 e = lg * 32 + lane;  // the lane operand's entry index
-    const u64* __restrict__ pl = p.cms + (size_t)lg * (size_t)n * 32 + lane;
     const u64* __restrict__ pr[TI];
 #pragma unroll
     for (int t = 0; t < TI; t++) pr[t] = p.cms + cm_index(BIN ? row0 + t : 0, n, 0);
@@ -138,11 +178,27 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
         d = lo_;
     }
 
-    auto do_row = [&](const int r) {
+    auto fold = [&](const bool first) {  // blocked Mueller: block 0 enters as is (== reference for n <= 64)
+#pragma unroll
+        for (int t = 0; t < TI; t++) {
+            if (first) {
+                s0[t] += h0[t];
+                s1[t] += h1[t];
+            } else {
+                s0[t] += mix64(h0[t]);
+                s1[t] += mix64(h1[t]);
+            }
+            h0[t] = K_SEED0;
+            h1[t] = K_SEED1;
+        }
+    };
+
+    // src: this lane's column of the staged row (word w at src[w * 32])
+    auto do_row = [&](const int r, const u64* __restrict__ src) {
         u64 a[W], m[W];
         const size_t kb = (size_t)r * W;
 #pragma unroll
-        for (int w = 0; w < W; w++) a[w] = ld_nc(pl + (kb + w) * 32);
+        for (int w = 0; w < W; w++) a[w] = src[w * 32];
 #pragma unroll
         for (int w = 0; w < W; w++) m[w] = NEEDM ? ld_nc(p.masks + kb + w) : 0ull;
         const u32 ispos = r < p.n_pos ? 1u : 0u;
@@ -161,7 +217,7 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
                     u64 mm = mix64(out[w] ^ (tw + (u64)w * K_STEP));
                     h0[t] = (h0[t] ^ mm) * K_FOLD0;
                     h1[t] = (h1[t] ^ ((mm << 32) | (mm >> 32))) * K_FOLD1;
-                    if (64 % W != 0) {  // per-word block boundary check (rows straddle hash blocks)
+                    if (!Ring<W>::CHUNK_FOLD) {  // per-word block boundary check (rows straddle hash blocks)
                         const u64 k1 = kb + w + 1;
                         if ((k1 & 63) == 0 || k1 == (u64)n) {
                             if (((k1 - 1) >> 6) == 0) {
@@ -198,31 +254,53 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
         tw += (u64)W * K_STEP;
     };
 
-    if (MUELLER && 64 % W == 0) {
-        constexpr int RPB = (64 % W == 0) ? 64 / W : 1;  // rows per 64-word hash block
-        for (int rb = r0; rb < r1; rb += RPB) {
-            const int rend = min(rb + RPB, r1);
-            if (W == 1) {
-#pragma unroll 4
-                for (int r = rb; r < rend; r++) do_row(r);
-            } else {
-                for (int r = rb; r < rend; r++) do_row(r);
-            }
+    // ---- stream the lane operand through the shared-memory ring
+    typedef Ring<W> RG;
+    const int rows_total = r1 - r0;
+    const int nchunks = (rows_total + RG::RPC - 1) / RG::RPC;
+    const u64* __restrict__ gsrc = p.cms + ((size_t)lg * (size_t)n + (size_t)r0 * W) * 32;
+    auto issue = [&](const int c, const int s) {
+        const int rows_c = min(RG::RPC, rows_total - c * RG::RPC);
+        const u32 bytes = (u32)rows_c * W * 256u;
+        mbar_expect_tx(bars + s, bytes);
+        bulk_g2s(sbuf + s * RG::STAGE_U64, gsrc + (size_t)c * RG::STAGE_U64, bytes, bars + s);
+    };
+    if (lane == 0) {
 #pragma unroll
-            for (int t = 0; t < TI; t++) {  // blocked Mueller: block 0 enters as is (== reference for n <= 64)
-                if (rb == 0) {
-                    s0[t] += h0[t];
-                    s1[t] += h1[t];
-                } else {
-                    s0[t] += mix64(h0[t]);
-                    s1[t] += mix64(h1[t]);
-                }
-                h0[t] = K_SEED0;
-                h1[t] = K_SEED1;
-            }
+        for (int s = 0; s < RG::STAGES; s++) mbar_init(bars + s, 1);
+        fence_mbar_init();
+        fence_async_smem();
+#pragma unroll
+        for (int s = 0; s < RG::STAGES; s++)
+            if (s < nchunks) issue(s, s);
+    }
+    __syncwarp();
+    int stage = 0;
+    u32 parity = 0;
+    for (int c = 0; c < nchunks; c++) {
+        mbar_wait(bars + stage, parity);
+        const u64* __restrict__ src = sbuf + stage * RG::STAGE_U64 + lane;
+        const int rbase = r0 + c * RG::RPC;
+        const int rows_c = min(RG::RPC, r1 - rbase);
+        if (rows_c == RG::RPC) {
+#pragma unroll
+            for (int rr = 0; rr < RG::RPC; rr++) do_row(rbase + rr, src + rr * W * 32);
+        } else {
+            for (int rr = 0; rr < rows_c; rr++) do_row(rbase + rr, src + rr * W * 32);
         }
-    } else {
-        for (int r = r0; r < r1; r++) do_row(r);
+        if (MUELLER && RG::CHUNK_FOLD) {
+            const int rend = rbase + rows_c;
+            if ((((u32)rend * W) & 63u) == 0 || rend == p.R) fold((((u32)rend * W - 1) >> 6) == 0);
+        }
+        __syncwarp();
+        if (lane == 0 && c + RG::STAGES < nchunks) {
+            fence_async_smem();
+            issue(c + RG::STAGES, stage);
+        }
+        if (++stage == RG::STAGES) {
+            stage = 0;
+            parity ^= 1u;
+        }
     }
 
     // ---- per-candidate epilogue
@@ -260,8 +338,12 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
 
 template <int W, bool MUELLER>
 __global__ void __launch_bounds__(LTL_CTA, 2) k_screen(const __grid_constant__ ScreenParams p) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
-    const i64 T = (i64)blockIdx.x * LTL_WARPS_PER_CTA + (threadIdx.x >> 5);
+    const int warp = threadIdx.x >> 5;
+    u64* sbuf = reinterpret_cast<u64*>(smem_raw) + warp * Ring<W>::WARP_U64;
+    u64* bars = reinterpret_cast<u64*>(smem_raw) + LTL_WARPS_PER_CTA * Ring<W>::WARP_U64 + warp * Ring<W>::STAGES;
+    const i64 T = (i64)blockIdx.x * LTL_WARPS_PER_CTA + warp;
     if (T >= p.total_tiles) return;
     const int split = blockIdx.y;
     // piece of this tile: last piece with tile_base <= T
@@ -317,7 +399,7 @@ __global__ void __launch_bounds__(LTL_CTA, 2) k_screen(const __grid_constant__ S
     }
     const bool xl = pc.swap != 0;
 
-#define LTL_TILE(OP_, TI_, XL_) tile_eval<W, MUELLER, OP_, TI_, XL_>(p, pc, row0, lg, split, lane)
+#define LTL_TILE(OP_, TI_, XL_) tile_eval<W, MUELLER, OP_, TI_, XL_>(p, pc, row0, lg, split, lane, sbuf, bars)
 #define LTL_TILE_TI(OP_, XL_)                       \
     do {                                            \
         if (W == 1 && MUELLER) {                    \
