@@ -131,7 +131,10 @@ LTL_API int ltl_core_counters(ltl_core* h, uint64_t out[5]);
 
 /* Tuning / measurement (no reference counterpart).
  * options: "chunk_candidates" (candidates per device pass), "profile" (1: time every kernel with CUDA
- * events on the launching stream), "max_split" (cap on row splits), "force_split" (tests). */
+ * events on the launching stream), "max_split" (cap on row splits), "force_split" (tests),
+ * "store_results" (0: from now on admitted entries keep fingerprint + record but their matrices are not
+ * written -- for the last cost level of a search, whose entries are never operands; counters, records and
+ * statuses are unaffected, get_cm / export_cms of such entries fail with LTL_ERR_ARG). */
 LTL_API int ltl_core_set_option(ltl_core* h, const char* name, int64_t value);
 /* Accumulated per kernel class since creation / the last reset: launches, device milliseconds (profile
  * mode only), algorithmic bytes and candidates / entries processed. */
@@ -140,6 +143,9 @@ LTL_API int ltl_core_kernel_stats(ltl_core* h, int kernel_class, uint64_t* launc
 LTL_API int ltl_core_reset_kernel_stats(ltl_core* h);
 /* The CUDA stream (cudaStream_t) every kernel and copy of this handle is issued on, for CUDA-event timing. */
 LTL_API int ltl_core_stream(ltl_core* h, void** stream_out);
+/* Released stores are pooled per process (virtual range + physical pages) for the next core; this returns
+ * every pooled page to the driver and reports the bytes freed.  LTL_NO_POOL=1 disables pooling. */
+LTL_API uint64_t ltl_pool_trim(void);
 /* out[0..2] = host wall milliseconds spent growing the store, waiting for the device, planning chunks. */
 LTL_API int ltl_core_host_times(ltl_core* h, double out[3]);
 /* out[0..1] = bytes copied host->device / device->host by this handle so far. */

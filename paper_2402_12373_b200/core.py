@@ -83,6 +83,7 @@ def load_library():
     L.ltl_core_transfer_stats.argtypes = [vp, u64p]
     L.ltl_core_host_times.argtypes = [vp, C.POINTER(C.c_double)]
     L.ltl_core_host_times.restype = C.c_int
+    L.ltl_pool_trim.restype = C.c_uint64
     for name in ("ltl_core_create", "ltl_core_add_entry", "ltl_core_screen_unary", "ltl_core_screen_binary",
                  "ltl_core_run_level", "ltl_core_contains", "ltl_core_fingerprint_of", "ltl_core_get_cm",
                  "ltl_core_get_record", "ltl_core_export_cms", "ltl_core_export_records",
@@ -91,6 +92,11 @@ def load_library():
         getattr(L, name).restype = C.c_int
     _lib = L
     return L
+
+
+def pool_trim() -> int:
+    """Return pooled device memory of released cores to the driver; bytes freed."""
+    return int(load_library().ltl_pool_trim())
 
 
 def device_count() -> int:

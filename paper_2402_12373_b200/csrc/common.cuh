@@ -70,6 +70,11 @@ struct Piece {
     i64 tile_base;  // first warp tile of this piece in the launch
     i64 tiles_lane; // lane groups spanned
     i64 lane_g0;    // first lane group (entry index >> 5)
+    // fused unary tiles: the unary connectives of one level all read the same operand bucket, so the first
+    // unary piece of a range evaluates up to 4 of them per pass (its siblings then own no tiles).
+    int nfuse;      // 0/1: plain piece; >= 2: number of fused connectives
+    int fops;       // their opcodes, one nibble each, in enumeration order
+    i64 fcbase[4];  // chunk-local rank base of each fused connective's piece
 };
 
 // One deposit of the "bits" fingerprints (gather / fkp): take ((word[k] >> rsh) & mask) and add it

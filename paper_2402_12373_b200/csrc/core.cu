@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -234,6 +235,15 @@ static DriverApi& drv() {
 
 // A device buffer that grows in place: a reserved virtual range, physical memory mapped on demand
 // (180 GB of HBM is filled without ever copying the store).  Falls back to malloc + copy without VMM.
+struct GrowBuf;
+static std::mutex g_pool_mutex;
+static std::vector<GrowBuf>& g_pool();
+static bool pool_enabled() {
+    static int on = -1;
+    if (on < 0) on = getenv("LTL_NO_POOL") ? 0 : 1;
+    return on == 1;
+}
+
 struct GrowBuf {
     char* base = nullptr;
     size_t reserved = 0, mapped = 0, gran = 0;
@@ -241,9 +251,33 @@ struct GrowBuf {
     int device = 0;
     std::vector<std::pair<CUmemGenericAllocationHandle, size_t>> parts;
 
+    // Released buffers keep their virtual range and physical pages in a process-wide pool, so the next core
+    // (a learner makes one per search; divide-and-conquer makes many) starts with memory already mapped:
+    // mapping and unmapping tens of GB costs far more than the search itself.
+    bool take_from_pool(int dev, size_t max_bytes) {
+        std::lock_guard<std::mutex> lock(g_pool_mutex);
+        auto& pool = g_pool();
+        int best = -1;
+        for (int k = 0; k < (int)pool.size(); k++)
+            if (pool[k].device == dev && pool[k].reserved >= max_bytes &&
+                (best < 0 || pool[k].mapped > pool[best].mapped || (pool[k].mapped == pool[best].mapped && pool[k].reserved < pool[best].reserved)))
+                best = k;
+        if (best < 0) return false;
+        *this = pool[best];
+        pool.erase(pool.begin() + best);
+        return true;
+    }
+
     int init(int dev, size_t max_bytes) {
         device = dev;
         DriverApi& d = drv();
+        if (d.ok && pool_enabled()) {
+            // size classes (powers of two >= 1 GiB of VIRTUAL space) make pooled ranges reusable
+            size_t cls = (size_t)1 << 30;
+            while (cls < max_bytes) cls <<= 1;
+            max_bytes = cls;
+            if (take_from_pool(dev, max_bytes)) return 0;
+        }
         if (d.ok) {
             CUmemAllocationProp prop;
             memset(&prop, 0, sizeof(prop));
@@ -330,6 +364,20 @@ struct GrowBuf {
     }
 
     void release() {
+        if (vmm && base && pool_enabled()) {
+            std::lock_guard<std::mutex> lock(g_pool_mutex);
+            if (g_pool().size() < 64) {
+                g_pool().push_back(*this);
+                base = nullptr;
+                mapped = reserved = 0;
+                parts.clear();
+                return;
+            }
+        }
+        destroy();
+    }
+
+    void destroy() {
         if (vmm) {
             DriverApi& d = drv();
             size_t off = 0;
@@ -347,6 +395,22 @@ struct GrowBuf {
         mapped = reserved = 0;
     }
 };
+
+static std::vector<GrowBuf>& g_pool() {
+    static std::vector<GrowBuf> pool;
+    return pool;
+}
+
+static size_t pool_trim() {  // give every pooled page back to the driver
+    std::lock_guard<std::mutex> lock(g_pool_mutex);
+    size_t freed = 0;
+    for (auto& b : g_pool()) {
+        freed += b.mapped;
+        b.destroy();
+    }
+    g_pool().clear();
+    return freed;
+}
 
 // ------------------------------------------------------------------------------------------------
 // the core object
@@ -404,6 +468,9 @@ struct ltl_core {
     double grow_ms = 0, sync_ms = 0, plan_ms = 0;  // host wall time: store growth, waiting for the device, planning
     int sm_count = 148;
     int max_split = 4096, force_split = 0;
+    bool fuse_unary = true;
+    bool store_results = true;    // false: admitted entries get records and fingerprints but no matrix
+    u64 unstored_from = ~0ull;    // first entry index without a stored matrix
     bool profile = false;
     KStat stats[LTL_K_COUNT];
     std::vector<PendingEvent> pending;
@@ -558,12 +625,14 @@ struct HostTimer {
 static int ensure_entries(ltl_core* h, u64 entries) {  // matrices + records for `entries` entries
     HostTimer ht(&h->grow_ms);
     const u64 groups = (entries + 31) / 32;
-    if (h->cms.ensure((size_t)groups * 32 * (size_t)h->n * 8, h->stream) || h->rec_op.ensure((size_t)groups * 32, h->stream) ||
-        h->rec_lhs.ensure((size_t)groups * 32 * 4, h->stream) || h->rec_rhs.ensure((size_t)groups * 32 * 4, h->stream)) {
+    for (int attempt = 0; attempt < 2; attempt++) {
+        if (!(h->cms.ensure((size_t)groups * 32 * (size_t)h->n * 8, h->stream) || h->rec_op.ensure((size_t)groups * 32, h->stream) ||
+              h->rec_lhs.ensure((size_t)groups * 32 * 4, h->stream) || h->rec_rhs.ensure((size_t)groups * 32 * 4, h->stream)))
+            return LTL_OK;
         cudaGetLastError();
-        return h->fail(LTL_ERR_DEVICE_OOM, "device memory exhausted growing the entry store");
+        if (attempt == 0 && pool_trim() == 0) break;
     }
-    return LTL_OK;
+    return h->fail(LTL_ERR_DEVICE_OOM, "device memory exhausted growing the entry store");
 }
 
 static int ensure_records(ltl_core* h, u64 entries) {
@@ -619,6 +688,22 @@ static void push_piece(ltl_core* h, std::vector<Piece>& pieces, i64& total, i64&
     p.cbase = total;
     p.tile_base = tiles;
     total += p.count;
+    // fuse with an earlier unary piece over the same operand range (same chunk): it evaluates this connective too
+    if (kind == PIECE_UNARY && h->W == 1 && h->variant == VAR_MUELLER && h->fuse_unary && p.op != OP_IDENT) {
+        for (auto& q : pieces) {
+            if (q.kind != PIECE_UNARY || q.i0 != i0 || q.i1 != i1 || q.nfuse == 0 || q.nfuse >= 4) continue;
+            if (((q.fops >> (4 * (q.nfuse - 1))) & 15) >= p.op) continue;  // keep nibbles in ascending opcode order
+            q.fops |= p.op << (4 * q.nfuse);
+            q.fcbase[q.nfuse] = p.cbase;
+            q.nfuse++;
+            p.nfuse = 0;  // sibling: owns no tiles
+            pieces.push_back(p);
+            return;
+        }
+        p.nfuse = 1;
+        p.fops = p.op;
+        p.fcbase[0] = p.cbase;
+    }
     tiles += row_tiles * p.tiles_lane;
     pieces.push_back(p);
 }
@@ -632,6 +717,8 @@ static int expand_segments(ltl_core* h, const ltl_segment* segs, int n_segs, std
         const bool unary = g.op == OP_NOT || g.op == OP_NEXT || g.op == OP_FINALLY || g.op == OP_GLOBALLY;
         if (!unary && !is_binary(g.op)) return h->fail(LTL_ERR_ARG, "segment: unknown opcode");
         if (g.a0 < 0 || g.a1 > ne || g.a0 > g.a1) return h->fail(LTL_ERR_ARG, "segment: left range outside the store");
+        if ((u64)g.a1 > h->unstored_from || (!unary && g.b1 > 0 && (u64)g.b1 > h->unstored_from))
+            return h->fail(LTL_ERR_ARG, "segment: operand matrices were not stored (store_results was off)");
         if (unary) {
             if (g.a1 > g.a0) units.push_back({PIECE_UNARY, g.op, s, g.a0, g.a1, -1, -1});
             continue;
@@ -786,7 +873,8 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     const bool oom = winners > room;
     const u64 count = oom ? room : winners;
     if (oom && oom_c == ~0ull) return h->fail(LTL_ERR_CUDA, "internal: overflow rank missing");
-    if (count > 0 && materialize) {
+    if (count > 0 && materialize && !h->store_results && h->unstored_from == ~0ull) h->unstored_from = h->n_entries;
+    if (count > 0 && materialize && h->store_results) {
         if ((rc = ensure_entries(h, h->n_entries + count))) return rc;
         MaterializeParams m;
         memset(&m, 0, sizeof(m));
@@ -1239,6 +1327,7 @@ int ltl_core_export_cms(ltl_core* h, int64_t first, int64_t count, uint64_t* cms
     if (first < 0 || count < 0 || (u64)(first + count) > h->n_entries) return h->fail(LTL_ERR_ARG, "entry range outside the store");
     if (count == 0) return LTL_OK;
     if (!cms_out) return h->fail(LTL_ERR_ARG, "null argument");
+    if ((u64)(first + count) > h->unstored_from) return h->fail(LTL_ERR_ARG, "matrices of these entries were not stored");
     const i64 max_batch = std::max<i64>(1, ((i64)256 << 20) / (h->n * 8));
     u64* d_out = nullptr;
     const i64 batch = std::min<i64>(count, max_batch);
@@ -1313,6 +1402,11 @@ int ltl_core_set_option(ltl_core* h, const char* name, int64_t value) {
     if (!strcmp(name, "chunk_candidates")) {
         if (value < 1 || value > ((int64_t)1 << 30)) return h->fail(LTL_ERR_ARG, "chunk_candidates outside [1, 2^30]");
         h->chunk_cap = value;
+    } else if (!strcmp(name, "store_results")) {
+        if (value && h->unstored_from != ~0ull) return h->fail(LTL_ERR_ARG, "matrices were already skipped: storing cannot resume");
+        h->store_results = value != 0;
+    } else if (!strcmp(name, "fuse_unary")) {
+        h->fuse_unary = value != 0;
     } else if (!strcmp(name, "profile")) {
         h->profile = value != 0;
     } else if (!strcmp(name, "max_split")) {
@@ -1350,6 +1444,8 @@ int ltl_core_stream(ltl_core* h, void** stream_out) {
     *stream_out = (void*)h->stream;
     return LTL_OK;
 }
+
+uint64_t ltl_pool_trim(void) { return (uint64_t)pool_trim(); }
 
 int ltl_core_host_times(ltl_core* h, double out[3]) {
     if (!h || !out) return LTL_ERR_ARG;

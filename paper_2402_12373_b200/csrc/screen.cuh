@@ -142,11 +142,38 @@ __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier
 // ------------------------------------------------------------------------------------------------
 // one warp tile
 
+// connective of slot t of a tile: OPS is either one opcode (every slot applies it to a different row operand)
+// or >= 2 opcodes packed one nibble each (fused unary tile: every slot applies its own connective)
+template <int OPS>
+__host__ __device__ constexpr int slot_op(int t) {
+    return OPS < 16 ? OPS : ((OPS >> (4 * t)) & 15);
+}
+template <int OPS, int W>
+__device__ __forceinline__ void apply_slot(const int t, u64 (&out)[W], const u64 (&x)[W], const u64 (&y)[W], const u64 (&m)[W]) {
+    switch (t) {  // t is a constant after unrolling
+        case 0: apply_row<slot_op<OPS>(0), W>(out, x, y, m); break;
+        case 1: apply_row<slot_op<OPS>(1), W>(out, x, y, m); break;
+        case 2: apply_row<slot_op<OPS>(2), W>(out, x, y, m); break;
+        default: apply_row<slot_op<OPS>(3), W>(out, x, y, m); break;
+    }
+}
+__host__ __device__ constexpr bool op_unary_c(int op) {
+    return op == OP_IDENT || op == OP_NOT || op == OP_NEXT || op == OP_FINALLY || op == OP_GLOBALLY;
+}
+template <int OPS>
+__host__ __device__ constexpr bool ops_need_mask() {
+    return OPS < 16 ? (OPS == OP_NOT || OPS == OP_GLOBALLY)
+                    : ((OPS & 15) == OP_NOT || (OPS & 15) == OP_GLOBALLY || ((OPS >> 4) & 15) == OP_NOT ||
+                       ((OPS >> 4) & 15) == OP_GLOBALLY || ((OPS >> 8) & 15) == OP_NOT || ((OPS >> 8) & 15) == OP_GLOBALLY ||
+                       ((OPS >> 12) & 15) == OP_NOT || ((OPS >> 12) & 15) == OP_GLOBALLY);
+}
+
 template <int W, bool MUELLER, int OP, int TI, bool XL>
 __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc, const i64 row0, const i64 lg,
                                           const int split, const int lane, u64* __restrict__ sbuf, u64* bars) {
-    constexpr bool BIN = !(OP == OP_IDENT || OP == OP_NOT || OP == OP_NEXT || OP == OP_FINALLY || OP == OP_GLOBALLY);
-    constexpr bool NEEDM = (OP == OP_NOT || OP == OP_GLOBALLY);
+    constexpr bool FUSED = OP >= 16;
+    constexpr bool BIN = !op_unary_c(slot_op<OP>(0));
+    constexpr bool NEEDM = ops_need_mask<OP>();
     const i64 n = p.n;
     const i64 e = lg * 32 + lane;  // the lane operand's entry index
     const u64* __restrict__ pr[TI];
@@ -207,9 +234,9 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
             u64 b[W], out[W];
 #pragma unroll
             for (int w = 0; w < W; w++) b[w] = BIN ? ld_nc(pr[t] + (kb + w) * 32) : 0ull;
-            if (!BIN) apply_row<OP, W>(out, a, a, m);
-            else if (XL) apply_row<OP, W>(out, a, b, m);
-            else apply_row<OP, W>(out, b, a, m);
+            if (!BIN) apply_slot<OP, W>(t, out, a, a, m);
+            else if (XL) apply_slot<OP, W>(t, out, a, b, m);
+            else apply_slot<OP, W>(t, out, b, a, m);
             err[t] += (u32)(out[0] >> 63) ^ ispos;  // reference _speedups.pyx:327-333
             if (MUELLER) {
 #pragma unroll
@@ -322,7 +349,7 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
         }
         const bool valid = lane_in && (pc.kind != PIECE_TRI || cj > ci);
         if (!valid) continue;
-        const u64 c = piece_rank(pc, ci, cj);
+        const u64 c = FUSED ? (u64)pc.fcbase[t] + (u64)(e - pc.i0) : piece_rank(pc, ci, cj);
         if (p.nsplit > 1) {
             atomicAdd(p.acc_s0 + c, s0[t]);
             atomicAdd(p.acc_s1 + c, s1[t]);
@@ -414,6 +441,23 @@ __global__ void __launch_bounds__(LTL_CTA, 2) k_screen(const __grid_constant__ S
         }                                           \
     } while (0)
 
+    if (W == 1 && MUELLER && pc.kind == PIECE_UNARY && pc.nfuse > 1) {
+        switch (pc.fops) {
+            case 0x41: LTL_TILE(0x41, 2, false); break;
+            case 0x51: LTL_TILE(0x51, 2, false); break;
+            case 0x61: LTL_TILE(0x61, 2, false); break;
+            case 0x54: LTL_TILE(0x54, 2, false); break;
+            case 0x64: LTL_TILE(0x64, 2, false); break;
+            case 0x65: LTL_TILE(0x65, 2, false); break;
+            case 0x541: LTL_TILE(0x541, 3, false); break;
+            case 0x641: LTL_TILE(0x641, 3, false); break;
+            case 0x651: LTL_TILE(0x651, 3, false); break;
+            case 0x654: LTL_TILE(0x654, 3, false); break;
+            case 0x6541: LTL_TILE(0x6541, 4, false); break;
+            default: break;
+        }
+        return;
+    }
     switch (pc.op) {
         case OP_IDENT: LTL_TILE(OP_IDENT, 1, false); break;
         case OP_NOT: LTL_TILE(OP_NOT, 1, false); break;

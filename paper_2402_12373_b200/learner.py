@@ -77,6 +77,9 @@ class LearnerConfig:
     device: int = 0
     max_traces: Optional[int] = None
     max_trace_len: int = MAX_WORDS_PER_ROW * 64
+    #: keep the characteristic matrices of the last cost level too.  They are never operands (the search
+    #: ends there), so by default only their fingerprints and records are kept; results are identical.
+    store_last_level: bool = False
 
     def __post_init__(self):
         if not 0.0 <= self.noise <= 1.0:
@@ -294,6 +297,8 @@ class Enumeration:
             _check_deadline(cfg)
             t0 = time.perf_counter()
             cache.begin_level(c)
+            if c == self.ceiling - 1 and not cfg.store_last_level and hasattr(core, "set_option"):
+                core.set_option("store_results", 0)
             hit = _run_level(core, level_segments(cache, cfg, ops, c), cfg)
             if hit is not None:
                 status, op, li, ri = hit

@@ -66,6 +66,7 @@ def cfg_from_golden(kw: dict) -> LearnerConfig:
         kw["hash"] = HashScheme(**kw["hash"])
     if "cost" in kw:
         kw["cost"] = CostHomomorphism(tuple(kw["cost"]))
+    kw.setdefault("store_last_level", True)  # the fixtures hash every stored matrix
     return LearnerConfig(**kw)
 
 

@@ -302,3 +302,55 @@ def test_argument_errors():
     with pytest.raises(ValueError):
         core.screen_unary(1, 0, 5)
     core.close()
+
+
+def test_last_level_matrices_can_be_skipped():
+    """store_results=0 (what the learner does on the final cost level): identical statuses, counters and
+    records, but the skipped matrices cannot be read or used as operands."""
+    rng = np.random.default_rng(31)
+    masks = random_masks(rng, 40, 1)
+    cuda, ora = make_pair(masks, 20, err_max=-1)
+    drive.masks = masks
+    for k in range(4):
+        cm = random_cm(rng, masks)
+        assert cuda.add_entry(cm, 0, k, -1) == ora.add_entry(cm, 0, k, -1)
+    n0 = ora.n_entries
+    for op in UNARY:
+        assert cuda.screen_unary(op, 0, n0) == ora.screen_unary(op, 0, n0)
+    n1 = ora.n_entries
+    cuda.set_option("store_results", 0)
+    assert cuda.screen_binary(7, 0, n1, 0, n1, False) == ora.screen_binary(7, 0, n1, 0, n1, False)
+    assert cuda.counters() == ora._counters()
+    assert (records_array(cuda) == records_array(ora)).all()
+    assert (cuda.export_cms(0, n1) == ora.export_cms(0, n1)).all()
+    with pytest.raises((ValueError, IndexError)):
+        cuda.get_cm(n1)
+    with pytest.raises(ValueError):
+        cuda.screen_unary(1, n1, n1 + 1)
+    cuda.close()
+
+
+def test_fused_unary_levels_match_unfused():
+    """run_level fuses the unary connectives of a level into one pass per operand group; same results as
+    screening them one at a time."""
+    from paper_2402_12373_b200.learner import Segment
+
+    rng = np.random.default_rng(32)
+    masks = random_masks(rng, 100, 1)
+    a, b = (CudaCore(masks, 50, -1, V_MUELLER) for _ in range(2))
+    b.set_option("fuse_unary", 0)
+    for k in range(5):
+        cm = random_cm(rng, masks)
+        assert a.add_entry(cm, 0, k, -1) == b.add_entry(cm, 0, k, -1)
+    lo = 0
+    for _ in range(2):
+        hi = a.n_entries
+        segs = [Segment(1, lo, hi), Segment(2, 0, hi, 0, hi, True), Segment(4, lo, hi), Segment(5, lo, hi),
+                Segment(6, lo, hi), Segment(7, 0, hi, 0, hi, False)]
+        assert a.run_level(segs) == b.run_level(segs)
+        assert a.counters() == b.counters()
+        lo = hi
+    assert (a.export_cms() == b.export_cms()).all()
+    assert (records_array(a) == records_array(b)).all()
+    a.close()
+    b.close()
