@@ -1,11 +1,25 @@
 // semantics.cuh -- branch-free LTL connectives on one W-word row of a characteristic matrix.
 //
 // Position j of a trace lives in word j/64 at bit 63 - j%64 (MSB first), so "the suffix starting one
-// step later" is a logical LEFT shift of the whole W-word row; zeros enter from beyond the last word.
-// Temporal operators are O(log n) shift-by-powers-of-two scans with ROUNDS = ceil(log2(64*W)) rounds
-// (reference bitsem.py:107-149 for one word, width-generic form bitsem.py:307-334; _speedups.pyx:291-325).
+// step later" is a logical LEFT shift of the whole W-word row; zeros enter from beyond the last word, and
+// word 0 is the MOST significant word of the row read as one 64*W-bit integer.
+//
+// The reference computes F / G / U as O(log n) shift-by-powers-of-two scans with ceil(log2(64*W)) rounds
+// (bitsem.py:107-149 for one word, width-generic form bitsem.py:307-334; _speedups.pyx:291-325).  Both are
+// closures that move information from later positions to earlier ones, i.e. from LOW bits to HIGH bits --
+// the direction an integer adder propagates carries.  The default device formulation therefore lets the
+// adder do the scan (results are bit-identical, the parity tests compare against the scan oracle):
+//     F x   = x | -x                         all bits at and above the lowest set bit
+//     G x   = ~F(~x & m) & m                 (dual inside the length mask, reference bitsem.py:133-138)
+//     x U y = y | s | (((x + s) ^ x) & x),   s = x & (y << 1)
+//             (a seed s sits where x holds and y holds one step later; adding it to x ripples a carry up
+//              through the run of x-ones above it, and the bits the addition flipped are the flooded run)
+// which is ~12 instead of ~56 integer instructions per 64-bit word for U (and 4 vs 24 for F); ncu showed
+// k_screen ALU-pipe bound at 58 instructions per candidate word with the scans (profiles/README.md).
+// Multi-word rows chain the carry from word W-1 up to word 0.  Building with -DLTL_SEMANTICS_SCAN selects
+// the reference's scan formulation instead (kept for A/B measurements).
 // Everything is fully unrolled over compile-time W: shifts >= 64 become register renames, shifts < 64
-// funnel shifts with the neighbouring word (the multi-word carry).
+// funnel shifts with the neighbouring word.
 #pragma once
 #include "common.cuh"
 
@@ -57,6 +71,31 @@ struct UntilRounds<W, ROUNDS, ROUNDS> {
     static __device__ __forceinline__ void run(u64 (&)[W], u64 (&)[W]) {}
 };
 
+// out = a + b over the whole row (word W-1 least significant); carries chained upward
+template <int W>
+__device__ __forceinline__ void row_add(u64 (&out)[W], const u64 (&a)[W], const u64 (&b)[W]) {
+    u64 c = 0;
+#pragma unroll
+    for (int w = W - 1; w >= 0; w--) {
+        const u64 t = a[w] + b[w];
+        const u64 t2 = t + c;
+        c = (u64)(t < a[w]) | (u64)(t2 < t);
+        out[w] = t2;
+    }
+}
+
+// out = x | -x over the whole row: every bit at and above the lowest set bit
+template <int W>
+__device__ __forceinline__ void row_smear_up(u64 (&out)[W], const u64 (&x)[W]) {
+    u64 c = 1;  // -x = ~x + 1
+#pragma unroll
+    for (int w = W - 1; w >= 0; w--) {
+        const u64 t = ~x[w] + c;
+        c = c & (u64)(t == 0);
+        out[w] = x[w] | t;
+    }
+}
+
 // out = OP(x [, y]) on one row; m = the row's length mask (used by NOT / GLOBALLY only).
 // x is the left (or only) operand, y the right operand.
 template <int OP, int W>
@@ -76,6 +115,7 @@ __device__ __forceinline__ void apply_row(u64 (&out)[W], const u64 (&x)[W], cons
     } else if (OP == OP_NEXT) {
 #pragma unroll
         for (int w = 0; w < W; w++) out[w] = shl_word<W, 1>(x, w);
+#ifdef LTL_SEMANTICS_SCAN
     } else if (OP == OP_FINALLY) {
 #pragma unroll
         for (int w = 0; w < W; w++) out[w] = x[w];
@@ -95,6 +135,25 @@ __device__ __forceinline__ void apply_row(u64 (&out)[W], const u64 (&x)[W], cons
         }
         UntilRounds<W, 0, Rounds<W>::value>::run(out, rn);
     }
+#else
+    } else if (OP == OP_FINALLY) {
+        row_smear_up<W>(out, x);
+    } else if (OP == OP_GLOBALLY) {  // dual of F inside the mask (reference bitsem.py:133-138)
+        u64 t[W];
+#pragma unroll
+        for (int w = 0; w < W; w++) t[w] = ~x[w] & m[w];
+        row_smear_up<W>(out, t);
+#pragma unroll
+        for (int w = 0; w < W; w++) out[w] = ~out[w] & m[w];
+    } else {  // OP_UNTIL
+        u64 sd[W], t[W];
+#pragma unroll
+        for (int w = 0; w < W; w++) sd[w] = x[w] & shl_word<W, 1>(y, w);
+        row_add<W>(t, x, sd);
+#pragma unroll
+        for (int w = 0; w < W; w++) out[w] = y[w] | sd[w] | ((t[w] ^ x[w]) & x[w]);
+    }
+#endif
 }
 
 __host__ __device__ __forceinline__ bool op_is_unary(int op) {
