@@ -235,9 +235,6 @@ static DriverApi& drv() {
 
 // A device buffer that grows in place: a reserved virtual range, physical memory mapped on demand
 // (180 GB of HBM is filled without ever copying the store).  Falls back to malloc + copy without VMM.
-struct GrowBuf;
-static std::mutex g_pool_mutex;
-static std::vector<GrowBuf>& g_pool();
 static bool pool_enabled() {
     static int on = -1;
     if (on < 0) on = getenv("LTL_NO_POOL") ? 0 : 1;
@@ -251,33 +248,9 @@ struct GrowBuf {
     int device = 0;
     std::vector<std::pair<CUmemGenericAllocationHandle, size_t>> parts;
 
-    // Released buffers keep their virtual range and physical pages in a process-wide pool, so the next core
-    // (a learner makes one per search; divide-and-conquer makes many) starts with memory already mapped:
-    // mapping and unmapping tens of GB costs far more than the search itself.
-    bool take_from_pool(int dev, size_t max_bytes) {
-        std::lock_guard<std::mutex> lock(g_pool_mutex);
-        auto& pool = g_pool();
-        int best = -1;
-        for (int k = 0; k < (int)pool.size(); k++)
-            if (pool[k].device == dev && pool[k].reserved >= max_bytes &&
-                (best < 0 || pool[k].mapped > pool[best].mapped || (pool[k].mapped == pool[best].mapped && pool[k].reserved < pool[best].reserved)))
-                best = k;
-        if (best < 0) return false;
-        *this = pool[best];
-        pool.erase(pool.begin() + best);
-        return true;
-    }
-
     int init(int dev, size_t max_bytes) {
         device = dev;
         DriverApi& d = drv();
-        if (d.ok && pool_enabled()) {
-            // size classes (powers of two >= 1 GiB of VIRTUAL space) make pooled ranges reusable
-            size_t cls = (size_t)1 << 30;
-            while (cls < max_bytes) cls <<= 1;
-            max_bytes = cls;
-            if (take_from_pool(dev, max_bytes)) return 0;
-        }
         if (d.ok) {
             CUmemAllocationProp prop;
             memset(&prop, 0, sizeof(prop));
@@ -364,20 +337,6 @@ struct GrowBuf {
     }
 
     void release() {
-        if (vmm && base && pool_enabled()) {
-            std::lock_guard<std::mutex> lock(g_pool_mutex);
-            if (g_pool().size() < 64) {
-                g_pool().push_back(*this);
-                base = nullptr;
-                mapped = reserved = 0;
-                parts.clear();
-                return;
-            }
-        }
-        destroy();
-    }
-
-    void destroy() {
         if (vmm) {
             DriverApi& d = drv();
             size_t off = 0;
@@ -395,22 +354,6 @@ struct GrowBuf {
         mapped = reserved = 0;
     }
 };
-
-static std::vector<GrowBuf>& g_pool() {
-    static std::vector<GrowBuf> pool;
-    return pool;
-}
-
-static size_t pool_trim() {  // give every pooled page back to the driver
-    std::lock_guard<std::mutex> lock(g_pool_mutex);
-    size_t freed = 0;
-    for (auto& b : g_pool()) {
-        freed += b.mapped;
-        b.destroy();
-    }
-    g_pool().clear();
-    return freed;
-}
 
 // ------------------------------------------------------------------------------------------------
 // the core object
@@ -433,19 +376,20 @@ struct Unit {
 
 static thread_local std::string g_create_error;
 
-struct ltl_core {
-    int device = 0, R = 0, W = 0, n_pos = 0, err_max = 0, variant = 0, fkp_bits = 0, mask_k = 0;
-    i64 n = 0;
-    u64 budget = 0, entry_bytes = 0;
-    u64 cap_entries = 0;  // admissions allowed: min(logical budget, what the device can hold)
+// Every device / pinned resource of a core.  Released arenas are pooled per process and handed to the next
+// core on the same device (a learner creates one core per search, divide-and-conquer many): mapping,
+// unmapping and (de)allocating tens of GB costs far more than a search and varies wildly between runs, so in
+// steady state a search performs no memory-management call at all.
+struct Arena {
+    int device = -1;
     cudaStream_t stream = nullptr;
     u64* d_masks = nullptr;
+    i64 masks_cap = 0;
     Deposit* d_deps = nullptr;
-    int n_dep = 0;
+    int deps_cap = 0;
     GrowBuf cms, rec_op, rec_lhs, rec_rhs;
     Slot* table = nullptr;
-    u64 table_cap = 0, keys_upper = 0;
-    i64 chunk_cap = 1 << 24;
+    u64 table_cap = 0;
     i64 scratch_cap = 0;
     u32* d_slot = nullptr;
     u32* d_flagw = nullptr;
@@ -462,7 +406,91 @@ struct ltl_core {
     Ctl* d_ctl = nullptr;
     Ctl* h_ctl = nullptr;
     u64* d_stage = nullptr;
-    u64* h_stage = nullptr;  // pinned, n words
+    u64* h_stage = nullptr;  // pinned
+    i64 stage_cap = 0;
+    std::vector<cudaEvent_t> event_pool;
+
+    void destroy_all() {
+        if (device < 0) return;
+        cudaSetDevice(device);
+        for (auto e : event_pool) cudaEventDestroy(e);
+        event_pool.clear();
+        cms.release();
+        rec_op.release();
+        rec_lhs.release();
+        rec_rhs.release();
+        cudaFree(table);
+        cudaFree(d_masks);
+        cudaFree(d_deps);
+        cudaFree(d_slot);
+        cudaFree(d_flagw);
+        cudaFree(d_blocksum);
+        cudaFree(d_blockoff);
+        cudaFree(d_acc_s0);
+        cudaFree(d_acc_s1);
+        cudaFree(d_acc_err);
+        cudaFree(d_fp);
+        cudaFree(d_pieces);
+        cudaFree(d_ctl);
+        cudaFree(d_stage);
+        cudaFreeHost(h_pieces);
+        cudaFreeHost(h_ctl);
+        cudaFreeHost(h_stage);
+        if (stream) cudaStreamDestroy(stream);
+        cudaGetLastError();
+        *this = Arena();
+    }
+};
+
+static std::mutex g_pool_mutex;
+static std::vector<Arena>& g_pool() {
+    static std::vector<Arena> pool;
+    return pool;
+}
+
+static bool pool_take(int device, Arena& out) {
+    std::lock_guard<std::mutex> lock(g_pool_mutex);
+    auto& pool = g_pool();
+    int best = -1;
+    for (int k = 0; k < (int)pool.size(); k++)
+        if (pool[k].device == device && (best < 0 || pool[k].cms.mapped > pool[best].cms.mapped)) best = k;
+    if (best < 0) return false;
+    out = pool[best];
+    pool.erase(pool.begin() + best);
+    return true;
+}
+
+static void pool_give(Arena& a) {
+    if (pool_enabled() && a.device >= 0) {
+        std::lock_guard<std::mutex> lock(g_pool_mutex);
+        if (g_pool().size() < 16) {
+            g_pool().push_back(a);
+            a = Arena();
+            return;
+        }
+    }
+    a.destroy_all();
+}
+
+static size_t pool_trim() {  // give every pooled page back to the driver
+    std::lock_guard<std::mutex> lock(g_pool_mutex);
+    size_t freed = 0;
+    for (auto& a : g_pool()) {
+        freed += a.cms.mapped + a.table_cap * sizeof(Slot);
+        a.destroy_all();
+    }
+    g_pool().clear();
+    return freed;
+}
+
+struct ltl_core : Arena {
+    int R = 0, W = 0, n_pos = 0, err_max = 0, variant = 0, fkp_bits = 0, mask_k = 0;
+    i64 n = 0;
+    u64 budget = 0, entry_bytes = 0;
+    u64 cap_entries = 0;  // admissions allowed: min(logical budget, what the device can hold)
+    int n_dep = 0;
+    u64 keys_upper = 0;
+    i64 chunk_cap = 1 << 24;
     u64 n_entries = 0, offered = 0, admitted = 0, duplicates = 0;
     u64 h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic of this handle
     double grow_ms = 0, sync_ms = 0, plan_ms = 0;  // host wall time: store growth, waiting for the device, planning
@@ -474,7 +502,6 @@ struct ltl_core {
     bool profile = false;
     KStat stats[LTL_K_COUNT];
     std::vector<PendingEvent> pending;
-    std::vector<cudaEvent_t> event_pool;
     std::string err;
 
     int fail(int code, const std::string& msg) {
@@ -1098,33 +1125,13 @@ const char* ltl_core_last_error(const ltl_core* h) { return h ? h->err.c_str() :
 
 void ltl_core_destroy(ltl_core* h) {
     if (!h) return;
-    cudaSetDevice(h->device);
-    if (h->stream) cudaStreamSynchronize(h->stream);
-    drain_events(h);
-    for (auto e : h->event_pool) cudaEventDestroy(e);
-    h->cms.release();
-    h->rec_op.release();
-    h->rec_lhs.release();
-    h->rec_rhs.release();
-    cudaFree(h->table);
-    cudaFree(h->d_masks);
-    cudaFree(h->d_deps);
-    cudaFree(h->d_slot);
-    cudaFree(h->d_flagw);
-    cudaFree(h->d_blocksum);
-    cudaFree(h->d_blockoff);
-    cudaFree(h->d_acc_s0);
-    cudaFree(h->d_acc_s1);
-    cudaFree(h->d_acc_err);
-    cudaFree(h->d_fp);
-    cudaFree(h->d_pieces);
-    cudaFree(h->d_ctl);
-    cudaFree(h->d_stage);
-    cudaFreeHost(h->h_pieces);
-    cudaFreeHost(h->h_ctl);
-    cudaFreeHost(h->h_stage);
-    if (h->stream) cudaStreamDestroy(h->stream);
-    cudaGetLastError();
+    if (h->device >= 0) {
+        cudaSetDevice(h->device);
+        if (h->stream) cudaStreamSynchronize(h->stream);
+        drain_events(h);
+        cudaGetLastError();
+        pool_give(*static_cast<Arena*>(h));
+    }
     delete h;
 }
 
@@ -1167,12 +1174,14 @@ int ltl_core_create(const uint64_t* masks, int R, int W, int n_pos, int err_max,
     int rc = LTL_OK;
     auto boot = [&]() -> int {
         CK(cudaSetDevice(device));
-        cudaDeviceProp prop;
-        CK(cudaGetDeviceProperties(&prop, device));
-        h->sm_count = prop.multiProcessorCount;
-        CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        CK(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device));
+        Arena pooled;
+        if (pool_enabled() && pool_take(device, pooled)) static_cast<Arena&>(*h) = pooled;
+        h->device = device;
+        if (!h->stream) CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
         size_t free_b = 0, total_b = 0;
         CK(cudaMemGetInfo(&free_b, &total_b));
+        free_b += h->cms.mapped;  // a pooled arena's pages are ours to reuse
         // admissions allowed by the logical budget: OOM when admitted*eb + eb > budget (reference _speedups.pyx:252-253)
         u64 logical = h->budget / h->entry_bytes;
         const double per_entry = 8.0 * (double)h->n + 9.0 + 2.5 * sizeof(Slot);
@@ -1180,27 +1189,57 @@ int ltl_core_create(const uint64_t* masks, int R, int W, int n_pos, int err_max,
         u64 physical = usable > per_entry ? (u64)(usable / per_entry) : 0;
         h->cap_entries = std::min<u64>(std::min(logical, physical), (1ull << 31) - 64);
         const u64 cap_groups = (h->cap_entries + 63) / 32;
-        h->cms.init(device, (size_t)cap_groups * 32 * (size_t)h->n * 8);
-        h->rec_op.init(device, (size_t)cap_groups * 32);
-        h->rec_lhs.init(device, (size_t)cap_groups * 32 * 4);
-        h->rec_rhs.init(device, (size_t)cap_groups * 32 * 4);
-        CK(cudaMalloc(&h->d_masks, (size_t)h->n * 8));
-        CK(cudaMemcpyAsync(h->d_masks, masks, (size_t)h->n * 8, cudaMemcpyHostToDevice, h->stream));
+        // virtual reservations are generous and uniform so that pooled arenas fit the next core
+        auto reserve = [&](GrowBuf& g, size_t need, size_t floor_bytes) {
+            need = std::max(need, floor_bytes);
+            if (g.base && g.reserved >= need) return;
+            g.release();
+            g.init(device, need);
+        };
+        reserve(h->cms, (size_t)cap_groups * 32 * (size_t)h->n * 8, (size_t)256 << 30);
+        reserve(h->rec_op, (size_t)cap_groups * 32, (size_t)2 << 30);
+        reserve(h->rec_lhs, (size_t)cap_groups * 32 * 4, (size_t)8 << 30);
+        reserve(h->rec_rhs, (size_t)cap_groups * 32 * 4, (size_t)8 << 30);
+        if (h->masks_cap < h->n) {
+            cudaFree(h->d_masks);
+            h->d_masks = nullptr;
+            h->masks_cap = 0;
+            CK(cudaMalloc(&h->d_masks, (size_t)h->n * 8));
+            h->masks_cap = h->n;
+        }
+        if (h->stage_cap < h->n) {
+            cudaFree(h->d_stage);
+            cudaFreeHost(h->h_stage);
+            h->d_stage = h->h_stage = nullptr;
+            h->stage_cap = 0;
+            CK(cudaMalloc(&h->d_stage, (size_t)h->n * 8));
+            CK(cudaMallocHost(&h->h_stage, (size_t)h->n * 8));
+            h->stage_cap = h->n;
+        }
+        memcpy(h->h_stage, masks, (size_t)h->n * 8);  // pinned staging: the copy below is truly asynchronous
+        CK(cudaMemcpyAsync(h->d_masks, h->h_stage, (size_t)h->n * 8, cudaMemcpyHostToDevice, h->stream));
         h->h2d_bytes += (size_t)h->n * 8;
-        CK(cudaStreamSynchronize(h->stream));
         std::vector<Deposit> deps;
         int r2 = build_deposits(h, proj_rows, proj_offs, n_proj, deps);
         if (r2) return r2;
         h->n_dep = (int)deps.size();
-        CK(cudaMalloc(&h->d_deps, sizeof(Deposit) * std::max<size_t>(1, deps.size())));
+        if (h->deps_cap < std::max(1, h->n_dep)) {
+            cudaFree(h->d_deps);
+            h->d_deps = nullptr;
+            h->deps_cap = 0;
+            CK(cudaMalloc(&h->d_deps, sizeof(Deposit) * std::max<size_t>(1, deps.size())));
+            h->deps_cap = std::max(1, h->n_dep);
+        }
         if (!deps.empty()) {
             CK(cudaMemcpyAsync(h->d_deps, deps.data(), sizeof(Deposit) * deps.size(), cudaMemcpyHostToDevice, h->stream));
             CK(cudaStreamSynchronize(h->stream));
         }
-        CK(cudaMalloc(&h->d_ctl, sizeof(Ctl)));
-        CK(cudaMallocHost(&h->h_ctl, sizeof(Ctl)));
-        CK(cudaMalloc(&h->d_stage, (size_t)h->n * 8));
-        CK(cudaMallocHost(&h->h_stage, (size_t)h->n * 8));
+        if (!h->d_ctl) CK(cudaMalloc(&h->d_ctl, sizeof(Ctl)));
+        if (!h->h_ctl) CK(cudaMallocHost(&h->h_ctl, sizeof(Ctl)));
+        if (h->table) {  // pooled table: keep its size (no rehash in steady state), forget its keys
+            CK(cudaMemsetAsync(h->table, 0xFF, h->table_cap * sizeof(Slot), h->stream));
+            return LTL_OK;
+        }
         return ensure_table(h, 1);
     };
     rc = boot();
