@@ -490,7 +490,7 @@ struct ltl_core : Arena {
     u64 cap_entries = 0;  // admissions allowed: min(logical budget, what the device can hold)
     int n_dep = 0;
     u64 keys_upper = 0;
-    i64 chunk_cap = 1 << 24;
+    i64 chunk_cap = 1 << 22;  // candidates per device pass: small enough that little work follows a solver
     u64 n_entries = 0, offered = 0, admitted = 0, duplicates = 0;
     u64 h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic of this handle
     double grow_ms = 0, sync_ms = 0, plan_ms = 0;  // host wall time: store growth, waiting for the device, planning
