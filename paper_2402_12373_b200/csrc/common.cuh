@@ -62,7 +62,7 @@ struct Piece {
     int swap;       // RECT only: lanes run over the left operand i, row tiles over j
     int ti;         // max rows per warp tile (1..4)
     int seg;        // index of the caller's segment this piece belongs to
-    int pad;
+    int owns_tiles; // 0: a fused sibling, evaluated by the primary unary piece of its range
     i64 i0, i1;
     i64 j0, j1;
     i64 cbase;      // chunk-local rank of this piece's first candidate
@@ -106,6 +106,7 @@ struct ScreenParams {
     int R, W, n_pos, err_max;
     i64 n;  // words per entry
     i64 total_tiles;
+    i64 tile_offset;   // first warp tile of this launch (a level's phase A is issued in several launches)
     int nsplit;        // row splits (gridDim.y); > 1 => partial sums go to acc_*, k_finalize completes
     int rows_per_split;  // multiple of LTL_SPLIT_ROWS
     int variant, mask_k, n_dep;

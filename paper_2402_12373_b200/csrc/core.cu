@@ -490,7 +490,10 @@ struct ltl_core : Arena {
     u64 cap_entries = 0;  // admissions allowed: min(logical budget, what the device can hold)
     int n_dep = 0;
     u64 keys_upper = 0;
-    i64 chunk_cap = 1 << 22;  // candidates per device pass: small enough that little work follows a solver
+    i64 chunk_cap = 1 << 28;  // candidates per ordered-admission pass (normally a whole cost level)
+    i64 sub_tiles = 1 << 15;  // warp tiles per phase-A launch: little work is issued after a solver shows up
+    cudaEvent_t sub_ev[2] = {nullptr, nullptr};
+    u64* h_solver = nullptr;  // pinned: solver rank as of the end of each of the last two launches
     u64 n_entries = 0, offered = 0, admitted = 0, duplicates = 0;
     u64 h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic of this handle
     double grow_ms = 0, sync_ms = 0, plan_ms = 0;  // host wall time: store growth, waiting for the device, planning
@@ -690,6 +693,7 @@ static void push_piece(ltl_core* h, std::vector<Piece>& pieces, i64& total, i64&
     p.j1 = j1;
     p.swap = 0;
     p.ti = 1;
+    p.owns_tiles = 1;
     i64 lane_lo, lane_hi, rows;
     if (kind == PIECE_UNARY) {
         p.count = i1 - i0;
@@ -724,6 +728,7 @@ static void push_piece(ltl_core* h, std::vector<Piece>& pieces, i64& total, i64&
             q.fcbase[q.nfuse] = p.cbase;
             q.nfuse++;
             p.nfuse = 0;  // sibling: owns no tiles
+            p.owns_tiles = 0;
             pieces.push_back(p);
             return;
         }
@@ -766,6 +771,17 @@ static int expand_segments(ltl_core* h, const ltl_segment* segs, int n_segs, std
 
 // ------------------------------------------------------------------------------------------------
 // one chunk
+
+// lowest chunk-local rank a warp tile of a piece can hold (mirrors the early-exit test in k_screen)
+static i64 tile_min_rank(const Piece& pc, i64 t) {
+    const i64 rt = t / pc.tiles_lane;
+    const i64 lfirst = (pc.lane_g0 + (t - rt * pc.tiles_lane)) * 32;
+    if (pc.kind == PIECE_UNARY) return (i64)piece_rank(pc, std::max(lfirst, pc.i0), -1);
+    if (pc.kind == PIECE_RECT && pc.swap) return (i64)piece_rank(pc, std::max(lfirst, pc.i0), pc.j0 + rt * pc.ti);
+    const i64 row0 = pc.i0 + rt * pc.ti;
+    if (pc.kind == PIECE_RECT) return (i64)piece_rank(pc, row0, std::max(lfirst, pc.j0));
+    return (i64)piece_rank(pc, row0, std::max(lfirst, row0 + 1));
+}
 
 struct ChunkOut {
     int status = LTL_S_DONE;
@@ -845,10 +861,42 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
         CK(cudaMemsetAsync(h->d_acc_err, 0, (size_t)total * 4, h->stream));
     }
     const bool mueller = h->variant == VAR_MUELLER;
+    // Phase A goes out in launches of sub_tiles warp tiles, in enumeration order, with no host wait in
+    // between (two in flight); after each one the solver rank is copied to pinned memory, and once a solver is
+    // known no launch is issued whose first tile lies above it.
     {
-        ScopedTimer t(h, LTL_K_SCREEN, (u64)total, screen_bytes(h, pieces));
-        dim3 grid((unsigned)((tiles + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), (unsigned)p.nsplit);
-        SCREEN_FN[h->W](p, mueller, grid, h->stream);
+        const i64 per = (p.nsplit > 1 || mode != MODE_INSERT) ? tiles : std::max<i64>(h->sub_tiles, LTL_WARPS_PER_CTA);
+        const double bytes_all = screen_bytes(h, pieces);
+        u64 known_solver = ~0ull;
+        int k = 0;
+        for (i64 t0 = 0; t0 < tiles; t0 += per, k++) {
+            const i64 t1 = std::min(tiles, t0 + per);
+            if (per < tiles) {
+                if (k >= 2) {
+                    HostTimer ht(&h->sync_ms);
+                    CK(cudaEventSynchronize(h->sub_ev[k & 1]));
+                    known_solver = std::min(known_solver, h->h_solver[k & 1]);
+                }
+                if (known_solver != ~0ull && check_solve) {
+                    // first tile of this launch: its piece and the lowest rank it can hold
+                    size_t pi = 0;
+                    for (size_t q = 0; q < pieces.size(); q++)
+                        if (pieces[q].owns_tiles && pieces[q].tile_base <= t0) pi = q;
+                    if ((u64)tile_min_rank(pieces[pi], t0 - pieces[pi].tile_base) > known_solver) break;
+                }
+            }
+            p.tile_offset = t0;
+            const double frac = (double)(t1 - t0) / (double)tiles;
+            ScopedTimer t(h, LTL_K_SCREEN, (u64)((double)total * frac), bytes_all * frac);
+            dim3 grid((unsigned)((t1 - t0 + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), (unsigned)p.nsplit);
+            ScreenParams q = p;
+            q.total_tiles = t1;
+            SCREEN_FN[h->W](q, mueller, grid, h->stream);
+            if (per < tiles) {
+                CK(cudaMemcpyAsync(h->h_solver + (k & 1), &h->d_ctl->solver_c, sizeof(u64), cudaMemcpyDeviceToHost, h->stream));
+                CK(cudaEventRecord(h->sub_ev[k & 1], h->stream));
+            }
+        }
     }
     CK(cudaGetLastError());
     if (p.nsplit > 1) {
@@ -1129,6 +1177,9 @@ void ltl_core_destroy(ltl_core* h) {
         cudaSetDevice(h->device);
         if (h->stream) cudaStreamSynchronize(h->stream);
         drain_events(h);
+        if (h->sub_ev[0]) cudaEventDestroy(h->sub_ev[0]);
+        if (h->sub_ev[1]) cudaEventDestroy(h->sub_ev[1]);
+        cudaFreeHost(h->h_solver);
         cudaGetLastError();
         pool_give(*static_cast<Arena*>(h));
     }
@@ -1233,6 +1284,11 @@ int ltl_core_create(const uint64_t* masks, int R, int W, int n_pos, int err_max,
         if (!deps.empty()) {
             CK(cudaMemcpyAsync(h->d_deps, deps.data(), sizeof(Deposit) * deps.size(), cudaMemcpyHostToDevice, h->stream));
             CK(cudaStreamSynchronize(h->stream));
+        }
+        if (!h->sub_ev[0]) {
+            CK(cudaEventCreateWithFlags(&h->sub_ev[0], cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&h->sub_ev[1], cudaEventDisableTiming));
+            CK(cudaMallocHost(&h->h_solver, 2 * sizeof(u64)));
         }
         if (!h->d_ctl) CK(cudaMalloc(&h->d_ctl, sizeof(Ctl)));
         if (!h->h_ctl) CK(cudaMallocHost(&h->h_ctl, sizeof(Ctl)));
@@ -1441,6 +1497,8 @@ int ltl_core_set_option(ltl_core* h, const char* name, int64_t value) {
     if (!strcmp(name, "chunk_candidates")) {
         if (value < 1 || value > ((int64_t)1 << 30)) return h->fail(LTL_ERR_ARG, "chunk_candidates outside [1, 2^30]");
         h->chunk_cap = value;
+    } else if (!strcmp(name, "sub_tiles")) {
+        h->sub_tiles = std::max<int64_t>(LTL_WARPS_PER_CTA, value);
     } else if (!strcmp(name, "store_results")) {
         if (value && h->unstored_from != ~0ull) return h->fail(LTL_ERR_ARG, "matrices were already skipped: storing cannot resume");
         h->store_results = value != 0;

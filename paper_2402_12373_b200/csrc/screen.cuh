@@ -370,7 +370,7 @@ __global__ void __launch_bounds__(LTL_CTA, 2) k_screen(const __grid_constant__ S
     const int warp = threadIdx.x >> 5;
     u64* sbuf = reinterpret_cast<u64*>(smem_raw) + warp * Ring<W>::WARP_U64;
     u64* bars = reinterpret_cast<u64*>(smem_raw) + LTL_WARPS_PER_CTA * Ring<W>::WARP_U64 + warp * Ring<W>::STAGES;
-    const i64 T = (i64)blockIdx.x * LTL_WARPS_PER_CTA + warp;
+    const i64 T = p.tile_offset + (i64)blockIdx.x * LTL_WARPS_PER_CTA + warp;
     if (T >= p.total_tiles) return;
     const int split = blockIdx.y;
     // piece of this tile: last piece with tile_base <= T

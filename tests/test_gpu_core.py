@@ -354,3 +354,24 @@ def test_fused_unary_levels_match_unfused():
     assert (records_array(a) == records_array(b)).all()
     a.close()
     b.close()
+
+
+@pytest.mark.parametrize("sub_tiles,chunk", [(8, None), (16, 700), (64, None)])
+def test_sub_launched_levels_match_oracle(sub_tiles, chunk):
+    """Phase A issued in many small launches (early stop after a solver) gives the sequential result."""
+    rng = np.random.default_rng(sub_tiles)
+    spec, alphabet = random_spec(rng, 2, 20, 20, 10, 30)
+    want = L.learn(spec, None, alphabet, max_cost=9, core_factory=oracle_factory(4))
+    from paper_2402_12373_b200.core import make_core
+
+    def factory(*a, **kw):
+        core = make_core(*a, **kw, **({} if chunk is None else {"chunk_candidates": chunk}))
+        core.set_option("sub_tiles", sub_tiles)
+        return core
+
+    got = L.learn(spec, None, alphabet, max_cost=9, core_factory=factory)
+    assert (got.status, got.text, got.cost) == (want.status, want.text, want.cost)
+    a, b = got.stats.as_dict(), want.stats.as_dict()
+    for lv in a["levels"] + b["levels"]:
+        lv.pop("ms", None)
+    assert a == b
