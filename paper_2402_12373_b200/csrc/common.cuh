@@ -69,6 +69,8 @@ struct Piece {
     i64 count;      // candidates in this piece
     i64 tile_base;  // first warp tile of this piece in the launch
     i64 tiles_lane; // lane groups spanned
+    i64 tiles_row;  // row tiles (ceil(rows / ti)); tile t = (row tile, lane group), ordered so that the lowest
+                    // rank of a tile never decreases with t: row-major, except swapped RECT (lane-group-major)
     i64 lane_g0;    // first lane group (entry index >> 5)
     // fused unary tiles: the unary connectives of one level all read the same operand bucket, so the first
     // unary piece of a range evaluates up to 4 of them per pass (its siblings then own no tiles).

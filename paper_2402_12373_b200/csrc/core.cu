@@ -716,6 +716,7 @@ static void push_piece(ltl_core* h, std::vector<Piece>& pieces, i64& total, i64&
     p.lane_g0 = lane_lo >> 5;
     p.tiles_lane = ((lane_hi - 1) >> 5) - p.lane_g0 + 1;
     const i64 row_tiles = (rows + p.ti - 1) / p.ti;
+    p.tiles_row = row_tiles;
     p.cbase = total;
     p.tile_base = tiles;
     total += p.count;
@@ -724,6 +725,9 @@ static void push_piece(ltl_core* h, std::vector<Piece>& pieces, i64& total, i64&
         for (auto& q : pieces) {
             if (q.kind != PIECE_UNARY || q.i0 != i0 || q.i1 != i1 || q.nfuse == 0 || q.nfuse >= 4) continue;
             if (((q.fops >> (4 * (q.nfuse - 1))) & 15) >= p.op) continue;  // keep nibbles in ascending opcode order
+            // only rank-adjacent pieces fuse (NEXT, FINALLY, GLOBALLY follow one another in the enumeration
+            // order; NOT is followed by the binary connectives): the launch order stays the rank order
+            if (q.fcbase[q.nfuse - 1] + q.count != p.cbase) continue;
             q.fops |= p.op << (4 * q.nfuse);
             q.fcbase[q.nfuse] = p.cbase;
             q.nfuse++;
@@ -774,8 +778,11 @@ static int expand_segments(ltl_core* h, const ltl_segment* segs, int n_segs, std
 
 // lowest chunk-local rank a warp tile of a piece can hold (mirrors the early-exit test in k_screen)
 static i64 tile_min_rank(const Piece& pc, i64 t) {
-    const i64 rt = t / pc.tiles_lane;
-    const i64 lfirst = (pc.lane_g0 + (t - rt * pc.tiles_lane)) * 32;
+    const bool lane_major = pc.kind == PIECE_RECT && pc.swap;
+    const i64 minor = lane_major ? pc.tiles_row : pc.tiles_lane;
+    const i64 hi_ = t / minor, lo_ = t - hi_ * minor;
+    const i64 rt = lane_major ? lo_ : hi_;
+    const i64 lfirst = (pc.lane_g0 + (lane_major ? hi_ : lo_)) * 32;
     if (pc.kind == PIECE_UNARY) return (i64)piece_rank(pc, std::max(lfirst, pc.i0), -1);
     if (pc.kind == PIECE_RECT && pc.swap) return (i64)piece_rank(pc, std::max(lfirst, pc.i0), pc.j0 + rt * pc.ti);
     const i64 row0 = pc.i0 + rt * pc.ti;

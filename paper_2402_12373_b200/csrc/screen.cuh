@@ -383,12 +383,21 @@ __global__ void __launch_bounds__(LTL_CTA, 2) k_screen(const __grid_constant__ S
     const Piece pc = p.pieces[lo];
     const i64 t = T - pc.tile_base;
     i64 rt, lgi;
-    if ((u64)t < 0xFFFFFFFFull && (u64)pc.tiles_lane < 0xFFFFFFFFull) {
-        rt = (u32)t / (u32)pc.tiles_lane;
-        lgi = (u32)t - (u32)rt * (u32)pc.tiles_lane;
-    } else {
-        rt = t / pc.tiles_lane;
-        lgi = t - rt * pc.tiles_lane;
+    {
+        // tile order inside a piece keeps ranks monotone: (row tile, lane group) row-major, but for a swapped
+        // RECT (lanes over the left operand i, which is the major rank index) lane-group-major
+        const bool lane_major = pc.kind == PIECE_RECT && pc.swap;
+        const i64 minor = lane_major ? pc.tiles_row : pc.tiles_lane;
+        i64 hi_, lo_;
+        if ((u64)t < 0xFFFFFFFFull && (u64)minor < 0xFFFFFFFFull) {
+            hi_ = (u32)t / (u32)minor;
+            lo_ = (u32)t - (u32)hi_ * (u32)minor;
+        } else {
+            hi_ = t / minor;
+            lo_ = t - hi_ * minor;
+        }
+        rt = lane_major ? lo_ : hi_;
+        lgi = lane_major ? hi_ : lo_;
     }
     const i64 lg = pc.lane_g0 + lgi;
     i64 row0 = 0;
@@ -401,6 +410,7 @@ __global__ void __launch_bounds__(LTL_CTA, 2) k_screen(const __grid_constant__ S
         if (pc.kind == PIECE_TRI && lg * 32 + 31 <= row0) return;  // tile entirely on/below the diagonal
     }
     // a solver with a lower rank than anything in this tile makes the tile irrelevant
+    u64 sol = ~0ull, fuse_off = 0;
     if (p.check_solve && p.mode == MODE_INSERT) {
         i64 ci, cj;
         const i64 lfirst = lg * 32;
@@ -418,11 +428,12 @@ __global__ void __launch_bounds__(LTL_CTA, 2) k_screen(const __grid_constant__ S
             cj = max(lfirst, row0 + 1);
         }
         const u64 cmin = piece_rank(pc, ci, cj);
-        const u64 sol = *((volatile u64*)&p.ctl->solver_c);
+        sol = *((volatile u64*)&p.ctl->solver_c);
         if (sol < cmin) {
             // the tile's slots stay unwritten: the resolve pass never looks above the solver
             return;
         }
+        fuse_off = (u64)(ci - pc.i0);
     }
     const bool xl = pc.swap != 0;
 
@@ -442,7 +453,16 @@ __global__ void __launch_bounds__(LTL_CTA, 2) k_screen(const __grid_constant__ S
     } while (0)
 
     if (W == 1 && MUELLER && pc.kind == PIECE_UNARY && pc.nfuse > 1) {
-        switch (pc.fops) {
+        // connectives whose every candidate of this tile ranks above a known solver are dropped (they form a
+        // suffix: fused connectives are consecutive in enumeration order)
+        int nf = pc.nfuse;
+        while (nf > 1 && (u64)pc.fcbase[nf - 1] + fuse_off > sol) nf--;
+        const int fops = pc.fops & ((1 << (4 * nf)) - 1);
+        switch (fops) {
+            case OP_NOT: LTL_TILE(OP_NOT, 1, false); break;
+            case OP_NEXT: LTL_TILE(OP_NEXT, 1, false); break;
+            case OP_FINALLY: LTL_TILE(OP_FINALLY, 1, false); break;
+            case OP_GLOBALLY: LTL_TILE(OP_GLOBALLY, 1, false); break;
             case 0x41: LTL_TILE(0x41, 2, false); break;
             case 0x51: LTL_TILE(0x51, 2, false); break;
             case 0x61: LTL_TILE(0x61, 2, false); break;
