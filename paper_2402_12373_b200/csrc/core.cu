@@ -505,6 +505,7 @@ struct ltl_core : Arena {
     bool profile = false;
     KStat stats[LTL_K_COUNT];
     std::vector<PendingEvent> pending;
+    std::vector<std::pair<u64, u64>> pending_mat;  // (first entry, count) admitted, matrices not yet written
     std::string err;
 
     int fail(int code, const std::string& msg) {
@@ -956,27 +957,10 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     const u64 count = oom ? room : winners;
     if (oom && oom_c == ~0ull) return h->fail(LTL_ERR_CUDA, "internal: overflow rank missing");
     if (count > 0 && materialize && !h->store_results && h->unstored_from == ~0ull) h->unstored_from = h->n_entries;
-    if (count > 0 && materialize && h->store_results) {
-        if ((rc = ensure_entries(h, h->n_entries + count))) return rc;
-        MaterializeParams m;
-        memset(&m, 0, sizeof(m));
-        m.cms = (u64*)h->cms.base;
-        m.masks = h->d_masks;
-        m.R = h->R;
-        m.W = h->W;
-        m.n = h->n;
-        m.n_base = (i64)h->n_entries;
-        m.count = (i64)count;
-        m.rec_op = (const unsigned char*)h->rec_op.base;
-        m.rec_lhs = (const int*)h->rec_lhs.base;
-        m.rec_rhs = (const int*)h->rec_rhs.base;
-        const i64 groups = (i64)((h->n_entries + count + 31) / 32 - h->n_entries / 32);
-        choose_split(h, groups, &m.nsplit, &m.rows_per_split);
-        ScopedTimer t(h, LTL_K_MATERIALIZE, count, (double)count * (8.0 * (double)h->n + 16.0 + 9.0));
-        dim3 grid((unsigned)((groups + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), (unsigned)m.nsplit);
-        MATERIALIZE_FN[h->W](m, grid, h->stream);
-        CK(cudaGetLastError());
-    }
+    // Matrices are written lazily: the winners' records exist now, their matrices are only needed when they
+    // first serve as operands (next cost level) or are read back -- a search that ends at this level (solved,
+    // ceiling) never pays for them.
+    if (count > 0 && materialize && h->store_results) h->pending_mat.push_back({h->n_entries, count});
     // ---- counters (reference _speedups.pyx:347-354, 372-379)
     u64 offered_c;
     if (oom) {
@@ -1009,6 +993,35 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     return LTL_OK;
 }
 
+// Phase B for every admitted-but-unwritten range.
+static int flush_materialize(ltl_core* h) {
+    int rc;
+    for (auto& pr : h->pending_mat) {
+        const u64 n_base = pr.first, count = pr.second;
+        if ((rc = ensure_entries(h, n_base + count))) return rc;
+        MaterializeParams m;
+        memset(&m, 0, sizeof(m));
+        m.cms = (u64*)h->cms.base;
+        m.masks = h->d_masks;
+        m.R = h->R;
+        m.W = h->W;
+        m.n = h->n;
+        m.n_base = (i64)n_base;
+        m.count = (i64)count;
+        m.rec_op = (const unsigned char*)h->rec_op.base;
+        m.rec_lhs = (const int*)h->rec_lhs.base;
+        m.rec_rhs = (const int*)h->rec_rhs.base;
+        const i64 groups = (i64)((n_base + count + 31) / 32 - n_base / 32);
+        choose_split(h, groups, &m.nsplit, &m.rows_per_split);
+        ScopedTimer t(h, LTL_K_MATERIALIZE, count, (double)count * (8.0 * (double)h->n + 16.0 + 9.0));
+        dim3 grid((unsigned)((groups + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), (unsigned)m.nsplit);
+        MATERIALIZE_FN[h->W](m, grid, h->stream);
+        CK(cudaGetLastError());
+    }
+    h->pending_mat.clear();
+    return LTL_OK;
+}
+
 // ------------------------------------------------------------------------------------------------
 // level driver: units -> chunks of <= chunk_cap candidates, consecutive in enumeration order
 
@@ -1017,6 +1030,10 @@ static int run_units(ltl_core* h, const std::vector<Unit>& units, bool check_sol
     *status = LTL_S_DONE;
     *seg_index = -1;
     *li = *ri = -1;
+    if (!units.empty()) {
+        int rcf = flush_materialize(h);
+        if (rcf) return rcf;
+    }
     std::vector<Piece> pieces;
     size_t ui = 0;
     i64 row = units.empty() ? 0 : units[0].i0;  // next row (left index) of the current unit
@@ -1395,6 +1412,11 @@ int ltl_core_entry_fingerprints(ltl_core* h, int64_t first, int64_t count, uint6
     if (first < 0 || count < 0 || (u64)(first + count) > h->n_entries) return h->fail(LTL_ERR_ARG, "entry range outside the store");
     if (count == 0) return LTL_OK;
     if (!hi || !lo) return h->fail(LTL_ERR_ARG, "null argument");
+    if ((u64)(first + count) > h->unstored_from) return h->fail(LTL_ERR_ARG, "matrices of these entries were not stored");
+    {
+        int rcf = flush_materialize(h);
+        if (rcf) return rcf;
+    }
     std::vector<u64> host;
     for (i64 done = 0; done < count;) {
         const i64 take = std::min<i64>(count - done, 1 << 20);
@@ -1430,6 +1452,10 @@ int ltl_core_export_cms(ltl_core* h, int64_t first, int64_t count, uint64_t* cms
     if (count == 0) return LTL_OK;
     if (!cms_out) return h->fail(LTL_ERR_ARG, "null argument");
     if ((u64)(first + count) > h->unstored_from) return h->fail(LTL_ERR_ARG, "matrices of these entries were not stored");
+    {
+        int rcf = flush_materialize(h);
+        if (rcf) return rcf;
+    }
     const i64 max_batch = std::max<i64>(1, ((i64)256 << 20) / (h->n * 8));
     u64* d_out = nullptr;
     const i64 batch = std::min<i64>(count, max_batch);
