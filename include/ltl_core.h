@@ -143,6 +143,29 @@ LTL_API int ltl_core_kernel_stats(ltl_core* h, int kernel_class, uint64_t* launc
 LTL_API int ltl_core_reset_kernel_stats(ltl_core* h);
 /* The CUDA stream (cudaStream_t) every kernel and copy of this handle is issued on, for CUDA-event timing. */
 LTL_API int ltl_core_stream(ltl_core* h, void** stream_out);
+/* ---- Multi-GPU stages (one process per GPU; orchestration in paper_2402_12373_b200/sharded.py). ----------
+ * A cost level's candidates have level ranks 0 .. level_size-1 in enumeration order; every rank of the job
+ * holds the same replicated store and evaluates a contiguous slice.  d_* arguments are DEVICE pointers on the
+ * handle's device (torch tensors); every stage returns after its work completed on the device.
+ *   level_size   candidates in the level
+ *   stage_eval   fingerprints (hi, lo per candidate, 2 x uint64) of level ranks [lo, hi) and the lowest
+ *                solving level rank in the slice (-1: none); stops after the chunk that holds a solver
+ *   stage_file   owner side: file (hi, lo, global rank) tuples in this handle's table shard with
+ *                atomicMin(rank); d_win[t] = 1 iff tuple t owns its key and the key was not a member before
+ *   stage_decode level ranks -> (op, lhs, rhs) records
+ *   stage_append append `count` admitted entries (records, in rank order) and advance the counters;
+ *                matrices are materialised locally from the records when first needed
+ *   stage_purge  forget keys filed at or above a global rank (solver / budget cut) */
+LTL_API int ltl_core_level_size(ltl_core* h, const ltl_segment* segs, int n_segs, int64_t* total);
+LTL_API int ltl_core_stage_eval(ltl_core* h, const ltl_segment* segs, int n_segs, int64_t lo, int64_t hi, uint64_t* d_fp,
+                        int64_t* solver_rank);
+LTL_API int ltl_core_stage_file(ltl_core* h, const uint64_t* d_tuples, int64_t count, unsigned char* d_win, int64_t* n_win);
+LTL_API int ltl_core_stage_decode(ltl_core* h, const ltl_segment* segs, int n_segs, const int64_t* d_ranks, int64_t count,
+                          unsigned char* d_op, int32_t* d_lhs, int32_t* d_rhs);
+LTL_API int ltl_core_stage_append(ltl_core* h, const unsigned char* d_op, const int32_t* d_lhs, const int32_t* d_rhs,
+                          int64_t count, uint64_t offered_delta, uint64_t duplicates_delta);
+LTL_API int ltl_core_stage_purge(ltl_core* h, uint64_t global_rank_cut);
+
 /* Released stores are pooled per process (virtual range + physical pages) for the next core; this returns
  * every pooled page to the driver and reports the bytes freed.  LTL_NO_POOL=1 disables pooling. */
 LTL_API uint64_t ltl_pool_trim(void);

@@ -84,6 +84,15 @@ def load_library():
     L.ltl_core_host_times.argtypes = [vp, C.POINTER(C.c_double)]
     L.ltl_core_host_times.restype = C.c_int
     L.ltl_pool_trim.restype = C.c_uint64
+    L.ltl_core_level_size.argtypes = [vp, C.POINTER(Segment), C.c_int, i64p]
+    L.ltl_core_stage_eval.argtypes = [vp, C.POINTER(Segment), C.c_int, C.c_int64, C.c_int64, vp, i64p]
+    L.ltl_core_stage_file.argtypes = [vp, vp, C.c_int64, vp, i64p]
+    L.ltl_core_stage_decode.argtypes = [vp, C.POINTER(Segment), C.c_int, vp, C.c_int64, vp, vp, vp]
+    L.ltl_core_stage_append.argtypes = [vp, vp, vp, vp, C.c_int64, C.c_uint64, C.c_uint64]
+    L.ltl_core_stage_purge.argtypes = [vp, C.c_uint64]
+    for name in ("ltl_core_level_size", "ltl_core_stage_eval", "ltl_core_stage_file", "ltl_core_stage_decode",
+                 "ltl_core_stage_append", "ltl_core_stage_purge"):
+        getattr(L, name).restype = C.c_int
     for name in ("ltl_core_create", "ltl_core_add_entry", "ltl_core_screen_unary", "ltl_core_screen_binary",
                  "ltl_core_run_level", "ltl_core_contains", "ltl_core_fingerprint_of", "ltl_core_get_cm",
                  "ltl_core_get_record", "ltl_core_export_cms", "ltl_core_export_records",
@@ -128,6 +137,7 @@ class CudaCore:
         if len(pr) > 126:
             raise ValueError("projection wider than the fingerprint")  # reference `_speedups.pyx:92-93`
         self.R, self.W, self.n = len(m) // W, W, len(m)
+        self.device_index = int(device)
         self._L = L
         self._h = C.c_void_p()
         i32p = C.POINTER(C.c_int32)
@@ -269,6 +279,83 @@ class CudaCore:
         self._check(self._L.ltl_core_run_level(self._h, arr, len(segments), C.byref(st), C.byref(seg), C.byref(li),
                                                C.byref(ri)))
         return st.value, seg.value, li.value, ri.value
+
+    # -- multi-GPU stages (device tensors in / out; see sharded.py) -----------------------
+    @staticmethod
+    def _segments(segments):
+        segments = list(segments)
+        arr = (Segment * max(1, len(segments)))()
+        for k, s in enumerate(segments):
+            arr[k] = Segment(int(s.op), int(bool(s.tri)), int(s.a0), int(s.a1), int(s.b0), int(s.b1))
+        return arr, len(segments)
+
+    def level_size(self, segments) -> int:
+        arr, n = self._segments(segments)
+        total = C.c_int64()
+        self._check(self._L.ltl_core_level_size(self._h, arr, n, C.byref(total)))
+        return int(total.value)
+
+    def stage_eval(self, segments, lo: int, hi: int):
+        """Fingerprints of level ranks [lo, hi): int64[hi - lo, 2] device tensor (hi, lo bit patterns), and the
+        lowest solving level rank of the slice or -1."""
+        import torch
+
+        dev = torch.device("cuda", self.device_index)
+        fp = torch.empty((max(hi - lo, 0), 2), dtype=torch.int64, device=dev)
+        arr, n = self._segments(segments)
+        solver = C.c_int64(-1)
+        torch.cuda.current_stream(dev).synchronize()
+        self._check(self._L.ltl_core_stage_eval(self._h, arr, n, int(lo), int(hi), C.c_void_p(fp.data_ptr()),
+                                                C.byref(solver)))
+        return fp, int(solver.value)
+
+    def stage_file(self, tuples):
+        """Owner side: file int64[N, 3] (hi, lo, global rank) device tuples; uint8[N] winner flags."""
+        import torch
+
+        tuples = tuples.contiguous()
+        win = torch.zeros(tuples.shape[0], dtype=torch.uint8, device=tuples.device)
+        n_win = C.c_int64()
+        torch.cuda.current_stream(tuples.device).synchronize()
+        self._check(self._L.ltl_core_stage_file(self._h, C.c_void_p(tuples.data_ptr()), tuples.shape[0],
+                                                C.c_void_p(win.data_ptr()), C.byref(n_win)))
+        return win
+
+    def stage_decode(self, segments, ranks):
+        """Level ranks (int64 device tensor) -> (op uint8, lhs int32, rhs int32) device tensors."""
+        import torch
+
+        ranks = ranks.contiguous()
+        n = ranks.shape[0]
+        op = torch.empty(n, dtype=torch.uint8, device=ranks.device)
+        lhs = torch.empty(n, dtype=torch.int32, device=ranks.device)
+        rhs = torch.empty(n, dtype=torch.int32, device=ranks.device)
+        arr, ns = self._segments(segments)
+        torch.cuda.current_stream(ranks.device).synchronize()
+        self._check(self._L.ltl_core_stage_decode(self._h, arr, ns, C.c_void_p(ranks.data_ptr()), n,
+                                                  C.c_void_p(op.data_ptr()), C.c_void_p(lhs.data_ptr()),
+                                                  C.c_void_p(rhs.data_ptr())))
+        return op, lhs, rhs
+
+    def stage_append(self, op, lhs, rhs, offered_delta: int, duplicates_delta: int):
+        import torch
+
+        op, lhs, rhs = op.contiguous(), lhs.contiguous(), rhs.contiguous()
+        torch.cuda.current_stream(op.device).synchronize()
+        self._check(self._L.ltl_core_stage_append(self._h, C.c_void_p(op.data_ptr()), C.c_void_p(lhs.data_ptr()),
+                                                  C.c_void_p(rhs.data_ptr()), op.shape[0], int(offered_delta),
+                                                  int(duplicates_delta)))
+
+    def stage_purge(self, global_rank_cut: int):
+        self._check(self._L.ltl_core_stage_purge(self._h, int(global_rank_cut)))
+
+    def capacity_entries(self) -> int:
+        return self.info()["capacity_entries"]
+
+    def stage_device(self):
+        import torch
+
+        return torch.device("cuda", self.device_index)
 
     # -- tuning / measurement ------------------------------------------------------------
     def set_option(self, name: str, value: int):

@@ -193,6 +193,51 @@ __global__ void k_purge(Slot* table, u64 cap, u64 gcut) {
     if (r != LTL_RANK_NONE && r >= gcut) table[s].rank = LTL_RANK_NONE;
 }
 
+// ---- multi-GPU stages (sharded.py): the owner of a fingerprint files (hi, lo, global rank) tuples received
+// from every rank, then says which tuple owns its key
+__global__ void k_file_insert(const u64* __restrict__ tuples, u64 count, Slot* table, u64 mask, u64 gbase,
+                              u32* __restrict__ slot_out) {
+    u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= count) return;
+    const u64 hi = tuples[3 * t], lo = tuples[3 * t + 1], rank = tuples[3 * t + 2];
+    const u64 s = table_find_or_claim(table, mask, hi, lo);
+    const u64 old = atomicMin(&table[s].rank, rank);
+    slot_out[t] = old < gbase ? LTL_NONE : (u32)s;
+}
+
+__global__ void k_file_verdict(const u64* __restrict__ tuples, const u32* __restrict__ slot, u64 count,
+                               const Slot* __restrict__ table, unsigned char* __restrict__ win, Ctl* ctl) {
+    u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    bool w = false;
+    if (t < count) {
+        const u32 s = slot[t];
+        w = s != LTL_NONE && ld_rank(table + s) == tuples[3 * t + 2];
+        win[t] = w ? 1 : 0;
+    }
+    const unsigned b = __ballot_sync(0xFFFFFFFFu, w);
+    if ((threadIdx.x & 31) == 0 && b) atomicAdd(&ctl->total, (u64)__popc(b));
+}
+
+// level ranks -> records
+__global__ void k_decode(const i64* __restrict__ ranks, u64 count, const Piece* __restrict__ pieces, int n_pieces,
+                         unsigned char* __restrict__ op, int* __restrict__ lhs, int* __restrict__ rhs) {
+    u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= count) return;
+    const u64 c = (u64)ranks[t];
+    int lo = 0, hi = n_pieces - 1;
+    while (lo < hi) {
+        int mid = (lo + hi + 1) >> 1;
+        if ((u64)pieces[mid].cbase <= c) lo = mid;
+        else hi = mid - 1;
+    }
+    const Piece pc = pieces[lo];
+    i64 i, j;
+    piece_unrank(pc, c, &i, &j);
+    op[t] = (unsigned char)pc.op;
+    lhs[t] = (int)i;
+    rhs[t] = (int)j;
+}
+
 // ------------------------------------------------------------------------------------------------
 // driver API (virtual memory management) through the runtime's entry-point lookup: no link-time libcuda
 
@@ -505,6 +550,7 @@ struct ltl_core : Arena {
     bool profile = false;
     KStat stats[LTL_K_COUNT];
     std::vector<PendingEvent> pending;
+    u64* fp_ext = nullptr;  // MODE_FP_ONLY output override (device pointer owned by the caller)
     std::vector<std::pair<u64, u64>> pending_mat;  // (first entry, count) admitted, matrices not yet written
     std::string err;
 
@@ -857,7 +903,7 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     p.table_mask = h->table_cap ? h->table_cap - 1 : 0;
     p.gbase = h->offered;
     p.slot = h->d_slot;
-    p.fp_out = mode == MODE_FP_ONLY ? h->d_fp : nullptr;
+    p.fp_out = mode == MODE_FP_ONLY ? (h->fp_ext ? h->fp_ext : h->d_fp) : nullptr;
     p.ctl = h->d_ctl;
     if (p.nsplit > 1) {
         if ((rc = ensure_acc(h, total))) return rc;
@@ -1115,6 +1161,66 @@ static int run_units(ltl_core* h, const std::vector<Unit>& units, bool check_sol
         }
     }
     return LTL_OK;
+}
+
+static i64 unit_count(const Unit& u) {
+    if (u.kind == PIECE_UNARY) return u.i1 - u.i0;
+    if (u.kind == PIECE_RECT) return (u.i1 - u.i0) * (u.j1 - u.j0);
+    return (i64)tri_before((u64)(u.i1 - u.i0), (u64)(u.j1 - 1 - u.i0));
+}
+
+// Pieces covering exactly the level ranks [lo, hi) of the unit list, in rank order (piece cbase = rank - lo).
+static void plan_range(ltl_core* h, const std::vector<Unit>& units, i64 lo, i64 hi, std::vector<Piece>& pieces,
+                       i64& total, i64& tiles) {
+    i64 ustart = 0;
+    for (const Unit& u : units) {
+        const i64 cnt = unit_count(u);
+        const i64 a = std::max(lo, ustart) - ustart, b = std::min(hi, ustart + cnt) - ustart;
+        ustart += cnt;
+        if (a >= b) continue;
+        if (u.kind == PIECE_UNARY) {
+            push_piece(h, pieces, total, tiles, u, u.i0 + a, u.i0 + b, -1, -1, PIECE_UNARY);
+        } else if (u.kind == PIECE_RECT) {
+            const i64 nj = u.j1 - u.j0;
+            i64 ra = a / nj, ca = a % nj;
+            const i64 rb = b / nj, cb = b % nj;
+            if (ra == rb) {
+                push_piece(h, pieces, total, tiles, u, u.i0 + ra, u.i0 + ra + 1, u.j0 + ca, u.j0 + cb, PIECE_RECT);
+                continue;
+            }
+            if (ca > 0) {
+                push_piece(h, pieces, total, tiles, u, u.i0 + ra, u.i0 + ra + 1, u.j0 + ca, u.j1, PIECE_RECT);
+                ra++;
+            }
+            if (rb > ra) push_piece(h, pieces, total, tiles, u, u.i0 + ra, u.i0 + rb, u.j0, u.j1, PIECE_RECT);
+            if (cb > 0) push_piece(h, pieces, total, tiles, u, u.i0 + rb, u.i0 + rb + 1, u.j0, u.j0 + cb, PIECE_RECT);
+        } else {
+            Piece t;
+            memset(&t, 0, sizeof(t));
+            t.kind = PIECE_TRI;
+            t.i0 = u.i0;
+            t.i1 = u.i1;
+            t.j1 = u.j1;
+            i64 ia, ja, ib, jb;
+            piece_unrank(t, (u64)a, &ia, &ja);
+            if (b < cnt) piece_unrank(t, (u64)b, &ib, &jb);
+            else {
+                ib = u.i1;
+                jb = u.i1 + 1;
+            }
+            // [ (ia, ja), (ib, jb) ) in row-major order; row i holds columns (i, j1)
+            if (ia == ib) {
+                push_piece(h, pieces, total, tiles, u, ia, ia + 1, ja, jb, PIECE_RECT);
+                continue;
+            }
+            if (ja > ia + 1) {
+                push_piece(h, pieces, total, tiles, u, ia, ia + 1, ja, u.j1, PIECE_RECT);
+                ia++;
+            }
+            if (ib > ia) push_piece(h, pieces, total, tiles, u, ia, ib, -1, u.j1, PIECE_TRI);
+            if (ib < u.i1 && jb > ib + 1) push_piece(h, pieces, total, tiles, u, ib, ib + 1, ib + 1, jb, PIECE_RECT);
+        }
+    }
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -1572,6 +1678,142 @@ int ltl_core_reset_kernel_stats(ltl_core* h) {
 int ltl_core_stream(ltl_core* h, void** stream_out) {
     if (!h || !stream_out) return LTL_ERR_ARG;
     *stream_out = (void*)h->stream;
+    return LTL_OK;
+}
+
+// ---- multi-GPU stages ---------------------------------------------------------------------------
+
+int ltl_core_level_size(ltl_core* h, const ltl_segment* segs, int n_segs, int64_t* total) {
+    ENTER(h);
+    if (!total || n_segs < 0 || (n_segs && !segs)) return h->fail(LTL_ERR_ARG, "null argument");
+    std::vector<Unit> units;
+    int rc = expand_segments(h, segs, n_segs, units);
+    if (rc) return rc;
+    i64 t = 0;
+    for (auto& u : units) t += unit_count(u);
+    *total = t;
+    return LTL_OK;
+}
+
+int ltl_core_stage_eval(ltl_core* h, const ltl_segment* segs, int n_segs, int64_t lo, int64_t hi, uint64_t* d_fp,
+                        int64_t* solver_rank) {
+    ENTER(h);
+    if (!solver_rank || n_segs < 0 || (n_segs && !segs)) return h->fail(LTL_ERR_ARG, "null argument");
+    *solver_rank = -1;
+    std::vector<Unit> units;
+    int rc = expand_segments(h, segs, n_segs, units);
+    if (rc) return rc;
+    i64 level_total = 0;
+    for (auto& u : units) level_total += unit_count(u);
+    if (lo < 0 || hi < lo || hi > level_total) return h->fail(LTL_ERR_ARG, "rank range outside the level");
+    if (hi == lo) return LTL_OK;
+    if (!d_fp) return h->fail(LTL_ERR_ARG, "null fingerprint buffer");
+    if ((rc = flush_materialize(h))) return rc;
+    std::vector<Piece> pieces;
+    const i64 cap = std::min<i64>(h->chunk_cap, (i64)1 << 26);
+    for (i64 c0 = lo; c0 < hi; c0 += cap) {
+        const i64 c1 = std::min<i64>(hi, c0 + cap);
+        pieces.clear();
+        i64 total = 0, tiles = 0;
+        plan_range(h, units, c0, c1, pieces, total, tiles);
+        if (total != c1 - c0) return h->fail(LTL_ERR_CUDA, "internal: range plan does not cover the slice");
+        h->fp_ext = (u64*)d_fp + 2 * (c0 - lo);
+        ChunkOut co;
+        rc = run_chunk(h, pieces, total, tiles, MODE_FP_ONLY, true, false, &co);
+        h->fp_ext = nullptr;
+        if (rc) return rc;
+        if (h->h_ctl->solver_c != ~0ull) {
+            *solver_rank = c0 + (i64)h->h_ctl->solver_c;
+            break;  // fingerprints above a solver are never used
+        }
+    }
+    return LTL_OK;
+}
+
+int ltl_core_stage_file(ltl_core* h, const uint64_t* d_tuples, int64_t count, unsigned char* d_win, int64_t* n_win) {
+    ENTER(h);
+    if (count < 0 || !n_win) return h->fail(LTL_ERR_ARG, "bad argument");
+    *n_win = 0;
+    if (count == 0) return LTL_OK;
+    if (!d_tuples || !d_win) return h->fail(LTL_ERR_ARG, "null argument");
+    int rc;
+    if ((rc = ensure_table(h, h->keys_upper + (u64)count))) return rc;
+    if ((rc = ensure_scratch(h, count))) return rc;
+    CK(cudaMemsetAsync(&h->d_ctl->total, 0, sizeof(u64), h->stream));
+    const unsigned nb = (unsigned)((count + 255) / 256);
+    {
+        ScopedTimer t(h, LTL_K_RESOLVE, (u64)count, (double)count * 56.0);
+        k_file_insert<<<nb, 256, 0, h->stream>>>((const u64*)d_tuples, (u64)count, h->table, h->table_cap - 1, h->offered, h->d_slot);
+        k_file_verdict<<<nb, 256, 0, h->stream>>>((const u64*)d_tuples, h->d_slot, (u64)count, h->table, d_win, h->d_ctl);
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h->h_ctl, h->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->d2h_bytes += sizeof(Ctl);
+    drain_events(h);
+    *n_win = (int64_t)h->h_ctl->total;
+    h->keys_upper += h->h_ctl->total;
+    return LTL_OK;
+}
+
+int ltl_core_stage_decode(ltl_core* h, const ltl_segment* segs, int n_segs, const int64_t* d_ranks, int64_t count,
+                          unsigned char* d_op, int32_t* d_lhs, int32_t* d_rhs) {
+    ENTER(h);
+    if (count < 0) return h->fail(LTL_ERR_ARG, "bad argument");
+    if (count == 0) return LTL_OK;
+    if (!d_ranks || !d_op || !d_lhs || !d_rhs) return h->fail(LTL_ERR_ARG, "null argument");
+    std::vector<Unit> units;
+    int rc = expand_segments(h, segs, n_segs, units);
+    if (rc) return rc;
+    i64 level_total = 0;
+    for (auto& u : units) level_total += unit_count(u);
+    std::vector<Piece> pieces;
+    i64 total = 0, tiles = 0;
+    plan_range(h, units, 0, level_total, pieces, total, tiles);
+    if ((rc = ensure_pieces(h, (int)pieces.size()))) return rc;
+    CK(cudaStreamSynchronize(h->stream));
+    memcpy(h->h_pieces, pieces.data(), sizeof(Piece) * pieces.size());
+    CK(cudaMemcpyAsync(h->d_pieces, h->h_pieces, sizeof(Piece) * pieces.size(), cudaMemcpyHostToDevice, h->stream));
+    {
+        ScopedTimer t(h, LTL_K_EMIT, (u64)count, (double)count * 17.0);
+        k_decode<<<(unsigned)((count + 255) / 256), 256, 0, h->stream>>>((const i64*)d_ranks, (u64)count, h->d_pieces,
+                                                                          (int)pieces.size(), d_op, d_lhs, d_rhs);
+    }
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->stream));
+    drain_events(h);
+    return LTL_OK;
+}
+
+int ltl_core_stage_append(ltl_core* h, const unsigned char* d_op, const int32_t* d_lhs, const int32_t* d_rhs, int64_t count,
+                          uint64_t offered_delta, uint64_t duplicates_delta) {
+    ENTER(h);
+    if (count < 0) return h->fail(LTL_ERR_ARG, "bad argument");
+    if (count > 0) {
+        if (!d_op || !d_lhs || !d_rhs) return h->fail(LTL_ERR_ARG, "null argument");
+        if (h->n_entries + (u64)count > h->cap_entries) return h->fail(LTL_ERR_BUDGET, "append beyond the entry capacity");
+        int rc = ensure_records(h, h->n_entries + (u64)count);
+        if (rc) return rc;
+        CK(cudaMemcpyAsync(h->rec_op.base + h->n_entries, d_op, (size_t)count, cudaMemcpyDeviceToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->rec_lhs.base + h->n_entries * 4, d_lhs, (size_t)count * 4, cudaMemcpyDeviceToDevice, h->stream));
+        CK(cudaMemcpyAsync(h->rec_rhs.base + h->n_entries * 4, d_rhs, (size_t)count * 4, cudaMemcpyDeviceToDevice, h->stream));
+        CK(cudaStreamSynchronize(h->stream));
+        if (h->store_results) h->pending_mat.push_back({h->n_entries, (u64)count});
+        else if (h->unstored_from == ~0ull) h->unstored_from = h->n_entries;
+        h->n_entries += (u64)count;
+        h->admitted += (u64)count;
+    }
+    h->offered += offered_delta;
+    h->duplicates += duplicates_delta;
+    return LTL_OK;
+}
+
+int ltl_core_stage_purge(ltl_core* h, uint64_t global_rank_cut) {
+    ENTER(h);
+    ScopedTimer t(h, LTL_K_PURGE, h->table_cap, (double)h->table_cap * sizeof(Slot));
+    k_purge<<<(unsigned)((h->table_cap + 255) / 256), 256, 0, h->stream>>>(h->table, h->table_cap, global_rank_cut);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->stream));
     return LTL_OK;
 }
 

@@ -1,0 +1,162 @@
+"""TEST INFRASTRUCTURE: a CPU stand-in for the multi-GPU stage API of `CudaCore` (level_size, stage_eval,
+stage_file, stage_decode, stage_append, stage_purge), built on the CPU oracle, so that the sharded
+orchestration (`paper_2402_12373_b200/sharded.py`) can be exercised with gloo processes on a machine without
+a GPU.  Tensors are CPU torch tensors."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from oracle import cpu_oracle
+from paper_2402_12373_b200 import errors as E
+
+UNARY = (1, 4, 5, 6)
+MASK64 = (1 << 64) - 1
+
+
+def _i64(x: int) -> int:
+    x &= MASK64
+    return x - (1 << 64) if x >= (1 << 63) else x
+
+
+def _u64(x: int) -> int:
+    return x & MASK64
+
+
+def seg_count(s) -> int:
+    na = s.a1 - s.a0
+    if s.op in UNARY:
+        return max(na, 0)
+    if na <= 0 or s.b1 <= s.b0:
+        return 0
+    if not s.tri:
+        return na * (s.b1 - s.b0)
+    return sum(max(0, s.b1 - max(s.b0, i + 1)) for i in range(s.a0, s.a1))
+
+
+def seg_candidates(s):
+    if s.op in UNARY:
+        for i in range(s.a0, s.a1):
+            yield s.op, i, -1
+        return
+    for i in range(s.a0, s.a1):
+        for j in range(max(s.b0, i + 1) if s.tri else s.b0, s.b1):
+            yield s.op, i, j
+
+
+class OracleStageCore:
+    def __init__(self, masks, n_pos, err_max, variant, proj_rows=(), proj_offs=(), fkp_bits=0, mask_k=0,
+                 budget_bytes=2 << 30, *, words_per_row=1, device=None):
+        self.o = cpu_oracle.OracleCore(masks, n_pos, err_max, variant, proj_rows, proj_offs, fkp_bits, mask_k,
+                                       1 << 60, words_per_row=words_per_row)
+        self.err_max = err_max
+        self.entry_bytes = 8 * self.o.n + 16
+        self.cap = int(budget_bytes) // self.entry_bytes
+        self.offered = self.admitted = self.duplicates = 0
+        self.table: dict[tuple[int, int], int] = {}  # this rank's shard: key -> owning global rank
+        self.store = True
+
+    # -- replicated calls
+    def add_entry(self, cm, op, lhs, rhs):
+        rank = self.offered
+        self.offered += 1
+        fp = self.o.fingerprint_of(cm)
+        key = (fp >> 64, fp & MASK64)
+        if key in self.table:
+            self.duplicates += 1
+            return -1
+        if self.admitted + 1 > self.cap:
+            raise E.CoreOOM
+        self.table[key] = rank
+        idx = self.o.add_entry(cm, op, lhs, rhs)
+        assert idx == self.admitted
+        self.admitted += 1
+        return idx
+
+    def get_record(self, idx):
+        return self.o.get_record(idx)
+
+    def counters(self):
+        n = self.o.n_entries
+        return [n, self.admitted * self.entry_bytes, self.offered, self.admitted, self.duplicates]
+
+    def capacity_entries(self):
+        return self.cap
+
+    def set_option(self, name, value):
+        pass
+
+    # -- stages
+    def level_size(self, segments):
+        return sum(seg_count(s) for s in segments)
+
+    def _candidates(self, segments, lo, hi):
+        r = 0
+        for s in segments:
+            c = seg_count(s)
+            if r + c <= lo:
+                r += c
+                continue
+            for cand in seg_candidates(s):
+                if r >= hi:
+                    return
+                if r >= lo:
+                    yield r, cand
+                r += 1
+
+    def _eval(self, op, i, j):
+        x = self.o.get_cm(i)
+        return self.o.apply_unary(op, x) if j < 0 else self.o.apply_binary(op, x, self.o.get_cm(j))
+
+    def stage_eval(self, segments, lo, hi):
+        fp = torch.zeros((max(hi - lo, 0), 2), dtype=torch.int64)
+        solver = -1
+        for r, (op, i, j) in self._candidates(segments, lo, hi):
+            cm = self._eval(op, i, j)
+            f = self.o.fingerprint_of(cm)
+            fp[r - lo, 0], fp[r - lo, 1] = _i64(f >> 64), _i64(f)
+            if self.o.errors(cm) <= self.err_max:
+                solver = r
+                break
+        return fp, solver
+
+    def stage_file(self, tuples):
+        gbase = self.offered
+        rows = [(_u64(int(a)), _u64(int(b)), int(c)) for a, b, c in tuples.tolist()]
+        contenders = {}
+        for hi, lo, rank in rows:
+            old = self.table.get((hi, lo))
+            if old is not None and old < gbase:
+                continue
+            contenders[(hi, lo)] = min(contenders.get((hi, lo), rank), rank)
+        win = torch.zeros(len(rows), dtype=torch.uint8)
+        for k, (hi, lo, rank) in enumerate(rows):
+            if contenders.get((hi, lo)) == rank:
+                win[k] = 1
+                self.table[(hi, lo)] = rank
+        return win
+
+    def stage_decode(self, segments, ranks):
+        want = [int(v) for v in ranks.tolist()]
+        out = {}
+        if want:
+            lo, hi = min(want), max(want) + 1
+            need = set(want)
+            for r, cand in self._candidates(segments, lo, hi):
+                if r in need:
+                    out[r] = cand
+        op = torch.tensor([out[r][0] for r in want], dtype=torch.uint8)
+        lhs = torch.tensor([out[r][1] for r in want], dtype=torch.int32)
+        rhs = torch.tensor([out[r][2] for r in want], dtype=torch.int32)
+        return op, lhs, rhs
+
+    def stage_append(self, op, lhs, rhs, offered_delta, duplicates_delta):
+        for o, l, r in zip(op.tolist(), lhs.tolist(), rhs.tolist()):
+            idx = self.o.add_entry(self._eval(int(o), int(l), int(r)), int(o), int(l), int(r))
+            assert idx >= 0, "an admitted entry must be new in the replicated store"
+            self.admitted += 1
+        self.offered += int(offered_delta)
+        self.duplicates += int(duplicates_delta)
+
+    def stage_purge(self, cut):
+        self.table = {k: v for k, v in self.table.items() if v < cut}
