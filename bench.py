@@ -272,9 +272,16 @@ def main():
     neg_c, neg_l = spec.chars[spec.n_pos:].copy(), spec.lengths[spec.n_pos:].copy()
     from paper_2402_12373_b200.traces import Specification
 
+    e2e_parts = {"spec_ms": 0.0, "learn_ms": 0.0}
+
     def e2e_once():
+        ta = time.perf_counter()
         s = Specification.from_arrays(pos_c, pos_l, neg_c, neg_l)
-        return learn(s, None, alphabet, max_cost=max_cost, budget_bytes=budget, device=local_rank)
+        tb = time.perf_counter()
+        out = learn(s, None, alphabet, max_cost=max_cost, budget_bytes=budget, device=local_rank)
+        e2e_parts["spec_ms"] += 1e3 * (tb - ta)
+        e2e_parts["learn_ms"] += 1e3 * (time.perf_counter() - tb)
+        return out
 
     r = e2e_once()
     assert r.text == text
@@ -290,7 +297,9 @@ def main():
     torch.cuda.synchronize()
     e2e_ms = e0.elapsed_time(e1)
     e2e = {"value": offered_per_step * args.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
-           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps}
+           "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps,
+           "host_ms_per_step": {k: v / (args.steps + 1) for k, v in e2e_parts.items()},
+           "search_ms_last": 1e3 * r.stats.search_seconds}
 
     # ---- CPU baseline on a bounded sample
     cpu = None

@@ -20,6 +20,7 @@ OBJ = os.path.join(CSRC, "build")
 MAX_W = 16
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden"]
+FLAGS += os.environ.get("LTL_NVCC_DEFS", "").split()  # A/B switches, e.g. -DLTL_SEMANTICS_SCAN -DLTL_SHIFT_MADHI
 
 
 def nvcc() -> str:

@@ -1,0 +1,99 @@
+"""`learn` command line (the reference specifies it, `/root/reference/SPEC.md:569-608`, but ships none).
+
+    python -m paper_2402_12373_b200.cli learn TRACE_FILE [--max-cost N] [--hash mueller|fkp] [--mask-bits K]
+        [--nnf] [--no-until] [--noise EPS] [--budget BYTES] [--costs a,n,c,d,x,f,g,u] [--timeout SECS]
+        [--device D] [--json PATH] [--verify]
+
+Reads a trace file (format `traces.py`, reference `traces.py:180-253`), runs the enumerative learner on the
+B200 core and writes the JSON report of `SPEC.md:158`: {formula, cost, wall_ms, mode, hash, stats}.  Only the
+`learn` subcommand is in scope (component 13); D&C (`--window`, `--strategy`) is not built.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import sys
+import time
+
+from .errors import BackendUnavailable, TimeoutExceeded
+from .formula import parse_formula, print_formula
+from .learner import learn
+from .scheme import HashScheme
+from .traces import TraceFormatError, load_spec
+
+
+def cmd_learn(args) -> int:
+    try:
+        spec, alphabet = load_spec(args.trace_file)
+    except (OSError, TraceFormatError) as exc:
+        print(f"error: {exc}", file=sys.stderr)
+        return 2
+    costs = None if args.costs is None else [int(v) for v in args.costs.split(",")]
+    t0 = time.perf_counter()
+    report = {"input": args.trace_file, "n_pos": spec.n_pos, "n_neg": spec.n_neg, "max_len": spec.max_len,
+              "config": {"max_cost": args.max_cost, "hash": args.hash, "mask_bits": args.mask_bits, "nnf": args.nnf,
+                         "no_until": args.no_until, "noise": args.noise, "budget": args.budget, "costs": costs}}
+    try:
+        res = learn(spec, None, alphabet, max_cost=args.max_cost, costs=costs, require_nnf=args.nnf,
+                    forbid_until=args.no_until, noise=args.noise,
+                    hash=HashScheme(args.hash, args.mask_bits), budget_bytes=args.budget, deadline_s=args.timeout,
+                    device=args.device)
+    except BackendUnavailable as exc:
+        print(f"error: {exc}", file=sys.stderr)
+        return 3
+    except TimeoutExceeded:
+        report.update(status="timeout", wall_ms=round(1e3 * (time.perf_counter() - t0), 3))
+        _emit(report, args)
+        return 4
+    report.update(status=res.status, formula=res.text, cost=res.cost,
+                  wall_ms=round(1e3 * (time.perf_counter() - t0), 3),
+                  mode="precise" if res.stats.precise else "hashed", hash=args.hash, overfit_cost=res.stats.ceiling,
+                  ratio=None if res.cost is None else res.cost / max(res.stats.ceiling, 1), stats=res.stats.as_dict())
+    rc = 0 if res.status in ("solved", "ceiling") else 1
+    if args.verify and res.formula is not None:
+        from .workloads import error_count
+
+        reparsed = parse_formula(print_formula(res.formula, alphabet), alphabet)
+        errs = error_count(reparsed, spec, alphabet)
+        report["verified_errors"] = errs
+        allowed = int(args.noise * spec.size + 1e-9)
+        if errs > allowed:
+            print(f"error: learned formula misclassifies {errs} traces (allowed {allowed})", file=sys.stderr)
+            rc = 5
+    _emit(report, args)
+    return rc
+
+
+def _emit(report, args):
+    text = json.dumps(report, sort_keys=True)
+    if args.json:
+        with open(args.json, "w", encoding="utf-8") as fh:
+            fh.write(text + "\n")
+    else:
+        print(text)
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(prog="paper_2402_12373_b200", description=__doc__.split("\n\n")[0])
+    sub = ap.add_subparsers(dest="cmd", required=True)
+    lp = sub.add_parser("learn", help="learn a minimal separating LTL formula from a trace file")
+    lp.add_argument("trace_file")
+    lp.add_argument("--max-cost", type=int, default=None, help="inclusive cost bound (default: up to the overfit cost)")
+    lp.add_argument("--hash", choices=["mueller", "fkp"], default="mueller")
+    lp.add_argument("--mask-bits", type=int, default=0)
+    lp.add_argument("--nnf", action="store_true")
+    lp.add_argument("--no-until", action="store_true")
+    lp.add_argument("--noise", type=float, default=0.0)
+    lp.add_argument("--budget", type=int, default=None, help="logical memory budget in bytes")
+    lp.add_argument("--costs", default=None, help="8 weights: atom,not,and,or,next,finally,globally,until")
+    lp.add_argument("--timeout", type=float, default=None)
+    lp.add_argument("--device", type=int, default=0)
+    lp.add_argument("--json", default=None, help="write the report here instead of stdout")
+    lp.add_argument("--verify", action="store_true", help="re-evaluate the learned formula on the input")
+    lp.set_defaults(fn=cmd_learn)
+    args = ap.parse_args(argv)
+    return args.fn(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -453,6 +453,8 @@ struct Arena {
     u64* d_stage = nullptr;
     u64* h_stage = nullptr;  // pinned
     i64 stage_cap = 0;
+    cudaEvent_t sub_ev[2] = {nullptr, nullptr};
+    u64* h_solver = nullptr;  // pinned: solver rank as of the end of each of the last two phase-A launches
     std::vector<cudaEvent_t> event_pool;
 
     void destroy_all() {
@@ -460,6 +462,9 @@ struct Arena {
         cudaSetDevice(device);
         for (auto e : event_pool) cudaEventDestroy(e);
         event_pool.clear();
+        if (sub_ev[0]) cudaEventDestroy(sub_ev[0]);
+        if (sub_ev[1]) cudaEventDestroy(sub_ev[1]);
+        cudaFreeHost(h_solver);
         cms.release();
         rec_op.release();
         rec_lhs.release();
@@ -537,8 +542,6 @@ struct ltl_core : Arena {
     u64 keys_upper = 0;
     i64 chunk_cap = 1 << 28;  // candidates per ordered-admission pass (normally a whole cost level)
     i64 sub_tiles = 1 << 15;  // warp tiles per phase-A launch: little work is issued after a solver shows up
-    cudaEvent_t sub_ev[2] = {nullptr, nullptr};
-    u64* h_solver = nullptr;  // pinned: solver rank as of the end of each of the last two launches
     u64 n_entries = 0, offered = 0, admitted = 0, duplicates = 0;
     u64 h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic of this handle
     double grow_ms = 0, sync_ms = 0, plan_ms = 0;  // host wall time: store growth, waiting for the device, planning
@@ -1307,9 +1310,6 @@ void ltl_core_destroy(ltl_core* h) {
         cudaSetDevice(h->device);
         if (h->stream) cudaStreamSynchronize(h->stream);
         drain_events(h);
-        if (h->sub_ev[0]) cudaEventDestroy(h->sub_ev[0]);
-        if (h->sub_ev[1]) cudaEventDestroy(h->sub_ev[1]);
-        cudaFreeHost(h->h_solver);
         cudaGetLastError();
         pool_give(*static_cast<Arena*>(h));
     }

@@ -51,6 +51,28 @@ __host__ __device__ inline void piece_unrank(const Piece& pc, u64 c, i64* i, i64
 
 #ifdef __CUDACC__
 
+// mix64 for the hot loop.  With -DLTL_SHIFT_MADHI the three `hi >> s` of the xor-shifts are computed as
+// multiply-high on the FMA pipe (hi * 2^(32-s) >> 32) instead of shifts on the ALU pipe (A/B switch: the loop
+// is ALU-pipe bound, see profiles/README.md).
+__device__ __forceinline__ u64 mix64_hot(u64 x) {
+#ifdef LTL_SHIFT_MADHI
+    u32 lo = (u32)x, hi = (u32)(x >> 32);
+    lo ^= __funnelshift_r(lo, hi, 30);
+    hi ^= __umulhi(hi, 1u << 2);
+    x = (((u64)hi << 32) | lo) * K_MIX1;
+    lo = (u32)x, hi = (u32)(x >> 32);
+    lo ^= __funnelshift_r(lo, hi, 27);
+    hi ^= __umulhi(hi, 1u << 5);
+    x = (((u64)hi << 32) | lo) * K_MIX2;
+    lo = (u32)x, hi = (u32)(x >> 32);
+    lo ^= __funnelshift_r(lo, hi, 31);
+    hi ^= __umulhi(hi, 1u << 1);
+    return ((u64)hi << 32) | lo;
+#else
+    return mix64(x);
+#endif
+}
+
 // ------------------------------------------------------------------------------------------------
 // fingerprint finalisation + table filing for one candidate
 
@@ -184,13 +206,16 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
     const int r1 = min(p.R, r0 + p.rows_per_split);
 
     u64 s0[TI], s1[TI], h0[TI], h1[TI];
-    u32 err[TI];
+    // Verdict bits (MSB of word 0 of every row) are COUNTED with one multiply-add-high per row on the FMA pipe
+    // (ones += hi32 * 2 >> 32); the count over the positive rows is snapshotted when the row index crosses n_pos:
+    // errors = (#positives - ones_pos) + (ones - ones_pos)          (reference _speedups.pyx:327-333)
+    u32 ones[TI], ones_pos[TI];
 #pragma unroll
     for (int t = 0; t < TI; t++) {
         s0[t] = s1[t] = 0;
         h0[t] = K_SEED0;
         h1[t] = K_SEED1;
-        err[t] = 0;
+        ones[t] = ones_pos[t] = 0;
     }
     u64 tw = ((u64)r0 * W + 1ull) * K_STEP;  // (k + 1) * STEP for the next word k
     int d = 0;                               // next deposit (bits fingerprints)
@@ -220,6 +245,11 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
         }
     };
 
+    auto snapshot = [&]() {
+#pragma unroll
+        for (int t = 0; t < TI; t++) ones_pos[t] = ones[t];
+    };
+
     // src: this lane's column of the staged row (word w at src[w * 32])
     auto do_row = [&](const int r, const u64* __restrict__ src) {
         u64 a[W], m[W];
@@ -228,7 +258,6 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
         for (int w = 0; w < W; w++) a[w] = src[w * 32];
 #pragma unroll
         for (int w = 0; w < W; w++) m[w] = NEEDM ? ld_nc(p.masks + kb + w) : 0ull;
-        const u32 ispos = r < p.n_pos ? 1u : 0u;
 #pragma unroll
         for (int t = 0; t < TI; t++) {
             u64 b[W], out[W];
@@ -237,11 +266,11 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
             if (!BIN) apply_slot<OP, W>(t, out, a, a, m);
             else if (XL) apply_slot<OP, W>(t, out, a, b, m);
             else apply_slot<OP, W>(t, out, b, a, m);
-            err[t] += (u32)(out[0] >> 63) ^ ispos;  // reference _speedups.pyx:327-333
+            asm("mad.hi.u32 %0, %1, 2, %0;" : "+r"(ones[t]) : "r"((u32)(out[0] >> 32)));
             if (MUELLER) {
 #pragma unroll
                 for (int w = 0; w < W; w++) {  // reference _speedups.pyx:196-202
-                    u64 mm = mix64(out[w] ^ (tw + (u64)w * K_STEP));
+                    u64 mm = mix64_hot(out[w] ^ (tw + (u64)w * K_STEP));
                     h0[t] = (h0[t] ^ mm) * K_FOLD0;
                     h1[t] = (h1[t] ^ ((mm << 32) | (mm >> 32))) * K_FOLD1;
                     if (!Ring<W>::CHUNK_FOLD) {  // per-word block boundary check (rows straddle hash blocks)
@@ -309,11 +338,16 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
         const u64* __restrict__ src = sbuf + stage * RG::STAGE_U64 + lane;
         const int rbase = r0 + c * RG::RPC;
         const int rows_c = min(RG::RPC, r1 - rbase);
-        if (rows_c == RG::RPC) {
+        const bool straddle = p.n_pos > rbase && p.n_pos < rbase + rows_c;
+        if (rbase == p.n_pos) snapshot();
+        if (rows_c == RG::RPC && !straddle) {
 #pragma unroll
             for (int rr = 0; rr < RG::RPC; rr++) do_row(rbase + rr, src + rr * W * 32);
         } else {
-            for (int rr = 0; rr < rows_c; rr++) do_row(rbase + rr, src + rr * W * 32);
+            for (int rr = 0; rr < rows_c; rr++) {
+                if (rr && rbase + rr == p.n_pos) snapshot();
+                do_row(rbase + rr, src + rr * W * 32);
+            }
         }
         if (MUELLER && RG::CHUNK_FOLD) {
             const int rend = rbase + rows_c;
@@ -331,6 +365,15 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
     }
 
     // ---- per-candidate epilogue
+    u32 err[TI];
+    {
+        const int npos_here = max(0, min(r1, p.n_pos) - r0);  // positive rows of this split
+#pragma unroll
+        for (int t = 0; t < TI; t++) {
+            if (p.n_pos >= r1) ones_pos[t] = ones[t];  // every row of the split is positive
+            err[t] = ((u32)npos_here - ones_pos[t]) + (ones[t] - ones_pos[t]);
+        }
+    }
     const bool lane_in = pc.kind == PIECE_UNARY ? (e >= pc.i0 && e < pc.i1)
                          : pc.kind == PIECE_RECT ? (pc.swap ? (e >= pc.i0 && e < pc.i1) : (e >= pc.j0 && e < pc.j1))
                                                  : (e < pc.j1);

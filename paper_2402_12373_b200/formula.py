@@ -243,7 +243,7 @@ def overfit_cost(spec, alphabet, h: CostHomomorphism = UNIFORM) -> int:
     m*atom + (n-m)*(atom+not) + (n-1)*and; every position adds one `&` and one `X`; every
     trace adds the end marker; the disjunction adds |P|-1 `|` nodes.
     """
-    n_traces = len(spec.pos)
+    n_traces = spec.n_pos  # (not len(spec.pos): that would materialise 2^20 tuples)
     if not n_traces:
         raise EmptyPositiveSet("cannot overfit an empty positive set")
     n = alphabet.size

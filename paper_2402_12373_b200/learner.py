@@ -349,7 +349,8 @@ def learn(P, N=None, alphabet: Alphabet | int | Sequence[str] | None = None, max
           costs: CostHomomorphism | Sequence[int] | None = None, *, require_nnf: bool = False,
           forbid_until: bool = False, noise: float = 0.0, hash: HashScheme | None = None,
           budget_bytes: int | None = None, deadline_s: float | None = None, device: int = 0,
-          overfit_on_ceiling: bool = True, core_factory: Callable | None = None) -> LearnResult:
+          overfit_on_ceiling: bool = True, store_last_level: bool = False,
+          core_factory: Callable | None = None) -> LearnResult:
     """Learn a minimal LTL formula accepting every trace in ``P`` and rejecting every trace in ``N``.
 
     ``P`` / ``N``: iterables of traces (each a sequence of int character bitmasks), or ``P`` a
@@ -372,6 +373,7 @@ def learn(P, N=None, alphabet: Alphabet | int | Sequence[str] | None = None, max
     cfg = LearnerConfig(cost=costs, require_nnf=require_nnf, forbid_until=forbid_until, noise=noise,
                         hash=hash or HashScheme(), ceiling=None if max_cost is None else int(max_cost) + 1,
                         deadline=None if deadline_s is None else time.monotonic() + deadline_s, device=device,
+                        store_last_level=store_last_level,
                         **({} if budget_bytes is None else {"budget_bytes": int(budget_bytes)}))
     out = enum_learn(spec, alphabet, cfg, core_factory=core_factory)
     if isinstance(out, Solved):

@@ -192,8 +192,9 @@ class Specification:
         closed-form overfit cost needs."""
         pc = self.chars[: self.n_pos]
         n_positions = int(self.lengths[: self.n_pos].sum())
-        bits = np.unpackbits(pc.view(np.uint8), axis=None)
-        return n_positions, int(bits.sum())
+        hist = np.bincount(pc.reshape(-1), minlength=1 << 16)  # characters are 16-bit masks
+        popcount = np.array([bin(v).count("1") for v in np.nonzero(hist)[0]], dtype=np.int64)
+        return n_positions, int((hist[np.nonzero(hist)[0]] * popcount).sum())
 
     def __repr__(self):
         return f"Specification(|P|={self.n_pos}, |N|={self.n_neg}, max_len={self.max_len})"

@@ -92,7 +92,7 @@ def planted_spec(n_props: int, n_pos: int, n_neg: int, min_len: int, max_len: in
     rng = np.random.default_rng(seed)
     pos_c, pos_l, neg_c, neg_l = [], [], [], []
     need_p, need_n = n_pos, n_neg
-    seen: set[bytes] = set()
+    earlier: list[np.ndarray] = []  # keys of the traces drawn in earlier batches
     batch = max(256, 2 * (n_pos + n_neg))
     for _ in range(max_draws):
         if need_p <= 0 and need_n <= 0:
@@ -100,24 +100,24 @@ def planted_spec(n_props: int, n_pos: int, n_neg: int, min_len: int, max_len: in
         lengths = rng.integers(min_len, max_len + 1, size=batch).astype(np.int64)
         chars = rng.integers(0, 1 << n_props, size=(batch, max_len)).astype(np.uint16)
         chars[np.arange(max_len)[None, :] >= lengths[:, None]] = 0
-        fresh = []
-        for k in range(batch):
-            key = chars[k, : lengths[k]].tobytes() + bytes([255, lengths[k] & 255, lengths[k] >> 8])
-            if key not in seen:
-                seen.add(key)
-                fresh.append(k)
-        fresh = np.array(fresh, dtype=np.int64)
-        chars, lengths = chars[fresh], lengths[fresh]
-        ctx = _ctx_from_arrays(chars, lengths, alphabet)
-        ok = accepts(f, ctx)
-        for k in range(len(fresh)):
-            if ok[k] and need_p > 0 and lengths[k] > 0:
-                pos_c.append(chars[k]); pos_l.append(lengths[k]); need_p -= 1  # noqa: E702
-            elif not ok[k] and need_n > 0:
-                neg_c.append(chars[k]); neg_l.append(lengths[k]); need_n -= 1  # noqa: E702
+        # distinct traces only: first occurrence inside the batch, none that an earlier batch drew
+        keyed = np.ascontiguousarray(np.concatenate([chars, lengths[:, None].astype(np.uint16)], axis=1))
+        keys = keyed.view(np.dtype((np.void, keyed.shape[1] * 2))).reshape(-1)
+        _, first = np.unique(keys, return_index=True)
+        first.sort()
+        for old in earlier:
+            first = first[~np.isin(keys[first], old)]
+        earlier.append(keys[first].copy())
+        chars, lengths = chars[first], lengths[first]
+        ok = accepts(f, _ctx_from_arrays(chars, lengths, alphabet))
+        take_p = np.nonzero(ok & (lengths > 0))[0][: max(need_p, 0)]
+        take_n = np.nonzero(~ok)[0][: max(need_n, 0)]
+        pos_c.append(chars[take_p]); pos_l.append(lengths[take_p]); need_p -= len(take_p)  # noqa: E702
+        neg_c.append(chars[take_n]); neg_l.append(lengths[take_n]); need_n -= len(take_n)  # noqa: E702
     if need_p > 0 or need_n > 0:
         raise RuntimeError("planted formula is too one-sided on random traces: could not fill both sides")
-    spec = Specification.from_arrays(np.array(pos_c), np.array(pos_l), np.array(neg_c), np.array(neg_l))
+    spec = Specification.from_arrays(np.concatenate(pos_c), np.concatenate(pos_l), np.concatenate(neg_c),
+                                     np.concatenate(neg_l))
     return spec, alphabet, f
 
 
