@@ -174,7 +174,8 @@ LTL_API int ltl_core_host_times(ltl_core* h, double out[3]);
 /* out[0..1] = bytes copied host->device / device->host by this handle so far. */
 LTL_API int ltl_core_transfer_stats(ltl_core* h, uint64_t out[2]);
 /* out[0..5] = effective entry capacity, device bytes mapped for matrices, table slots, chunk candidates,
- * 1 if the store uses virtual-memory growth, words per matrix */
+ * bit 0: the store uses virtual-memory growth, bit 1: an S_OOM status came from exhausted DEVICE memory rather
+ * than from the logical budget; words per matrix */
 LTL_API int ltl_core_info(ltl_core* h, uint64_t out[6]);
 
 #ifdef __cplusplus

@@ -396,8 +396,10 @@ class CudaCore:
     def info(self) -> dict:
         out = np.zeros(6, dtype=np.uint64)
         self._check(self._L.ltl_core_info(self._h, _u64(out)))
-        keys = ("capacity_entries", "matrix_bytes_mapped", "table_slots", "chunk_candidates", "vmm", "words_per_matrix")
-        return {k: int(v) for k, v in zip(keys, out)}
+        keys = ("capacity_entries", "matrix_bytes_mapped", "table_slots", "chunk_candidates", "flags", "words_per_matrix")
+        d = {k: int(v) for k, v in zip(keys, out)}
+        d["vmm"], d["device_oom"] = bool(d["flags"] & 1), bool(d["flags"] & 2)
+        return d
 
 
 def make_core(masks, n_pos, err_max, variant, proj_rows=(), proj_offs=(), fkp_bits=0, mask_k=0,

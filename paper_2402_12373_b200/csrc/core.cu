@@ -548,6 +548,7 @@ struct ltl_core : Arena {
     int sm_count = 148;
     int max_split = 4096, force_split = 0;
     bool fuse_unary = true;
+    bool device_oom = false;      // an S_OOM came from the device, not from the logical budget
     bool store_results = true;    // false: admitted entries get records and fingerprints but no matrix
     u64 unstored_from = ~0ull;    // first entry index without a stored matrix
     bool profile = false;
@@ -1081,6 +1082,11 @@ static int run_units(ltl_core* h, const std::vector<Unit>& units, bool check_sol
     *li = *ri = -1;
     if (!units.empty()) {
         int rcf = flush_materialize(h);
+        if (rcf == LTL_ERR_DEVICE_OOM) {  // the operands of this level do not fit the device: out of memory
+            h->device_oom = true;
+            *status = LTL_S_OOM;
+            return LTL_OK;
+        }
         if (rcf) return rcf;
     }
     std::vector<Piece> pieces;
@@ -1364,12 +1370,14 @@ int ltl_core_create(const uint64_t* masks, int R, int W, int n_pos, int err_max,
         CK(cudaMemGetInfo(&free_b, &total_b));
         free_b += h->cms.mapped;  // a pooled arena's pages are ours to reuse
         // admissions allowed by the logical budget: OOM when admitted*eb + eb > budget (reference _speedups.pyx:252-253)
+        // The budget is LOGICAL, like the reference's: admissions are counted, and because matrices are written
+        // lazily the entries of the level a search ends in never occupy memory.  Physical exhaustion is reported
+        // when matrices have to be written (flush_materialize -> LTL_S_OOM from the screening call).
         u64 logical = h->budget / h->entry_bytes;
-        const double per_entry = 8.0 * (double)h->n + 9.0 + 2.5 * sizeof(Slot);
-        const double usable = (double)free_b * 0.92 - (double)h->chunk_cap * 8.0 - (double)(64u << 20);
-        u64 physical = usable > per_entry ? (u64)(usable / per_entry) : 0;
-        h->cap_entries = std::min<u64>(std::min(logical, physical), (1ull << 31) - 64);
-        const u64 cap_groups = (h->cap_entries + 63) / 32;
+        h->cap_entries = std::min<u64>(logical, (1ull << 31) - 64);
+        const double per_entry = 8.0 * (double)h->n + 9.0;
+        const u64 physical = (u64)((double)(free_b > (1ull << 30) ? free_b - (1ull << 30) : 0) / per_entry);
+        const u64 cap_groups = (std::min<u64>(h->cap_entries, physical + 64) + 63) / 32;
         // virtual reservations are generous and uniform so that pooled arenas fit the next core
         auto reserve = [&](GrowBuf& g, size_t need, size_t floor_bytes) {
             need = std::max(need, floor_bytes);
@@ -1840,7 +1848,7 @@ int ltl_core_info(ltl_core* h, uint64_t out[6]) {
     out[1] = h->cms.mapped;
     out[2] = h->table_cap;
     out[3] = (u64)h->chunk_cap;
-    out[4] = h->cms.vmm ? 1 : 0;
+    out[4] = (h->cms.vmm ? 1 : 0) | (h->device_oom ? 2 : 0);
     out[5] = (u64)h->n;
     return LTL_OK;
 }
