@@ -23,7 +23,8 @@ typedef long long i64;
 enum { OP_IDENT = 0, OP_NOT = 1, OP_AND = 2, OP_OR = 3, OP_NEXT = 4, OP_FINALLY = 5, OP_GLOBALLY = 6, OP_UNTIL = 7 };
 enum { VAR_GATHER = 0, VAR_MUELLER = 1, VAR_FKP = 2 };
 enum { PIECE_UNARY = 0, PIECE_RECT = 1, PIECE_TRI = 2 };
-enum { MODE_INSERT = 0, MODE_FP_ONLY = 1, MODE_LOOKUP = 2 };
+enum { MODE_INSERT = 0, MODE_FP_ONLY = 1, MODE_LOOKUP = 2, MODE_REWRITE = 3 };
+enum { KIND_BITS = 0, KIND_MUELLER = 1, KIND_REWRITE = 2 };  // what a k_screen instantiation does with a row
 
 #define LTL_GROUP 32
 #define LTL_NONE 0xFFFFFFFFu
@@ -123,6 +124,10 @@ struct ScreenParams {
     u64* acc_s1;
     u32* acc_err;
     Ctl* ctl;
+    // KIND_REWRITE (tile-shaped phase B): winners' matrices go to entry n_base + dest[rank]
+    const u32* dest;  // per candidate: position among the winners / NONE
+    u64* cms_out;     // same buffer as cms
+    i64 n_base;
 };
 
 struct MaterializeParams {

@@ -27,7 +27,7 @@
 // per-W launchers (screen_inst.cu)
 
 #define LTL_DECL_W(N)                                                                                  \
-    extern "C" void ltl_launch_screen_w##N(const ScreenParams&, bool, dim3, cudaStream_t);             \
+    extern "C" void ltl_launch_screen_w##N(const ScreenParams&, int, dim3, cudaStream_t);             \
     extern "C" void ltl_launch_materialize_w##N(const MaterializeParams&, dim3, cudaStream_t);
 LTL_DECL_W(1) LTL_DECL_W(2) LTL_DECL_W(3) LTL_DECL_W(4) LTL_DECL_W(5) LTL_DECL_W(6) LTL_DECL_W(7) LTL_DECL_W(8)
 LTL_DECL_W(9) LTL_DECL_W(10) LTL_DECL_W(11) LTL_DECL_W(12) LTL_DECL_W(13) LTL_DECL_W(14) LTL_DECL_W(15) LTL_DECL_W(16)
@@ -122,7 +122,8 @@ __global__ void __launch_bounds__(1024) k_scan(const u32* __restrict__ blocksum,
 __global__ void __launch_bounds__(RES_CTA) k_emit(const u32* __restrict__ flagw, const u64* __restrict__ blockoff,
                                                   const Piece* __restrict__ pieces, int n_pieces, u64 total, i64 n_base,
                                                   u64 cap_left, unsigned char* __restrict__ rec_op,
-                                                  int* __restrict__ rec_lhs, int* __restrict__ rec_rhs, Ctl* ctl) {
+                                                  int* __restrict__ rec_lhs, int* __restrict__ rec_rhs,
+                                                  u32* __restrict__ dest_out, Ctl* ctl) {
     __shared__ u32 wcnt[32];
     const u64 limit = min(total, ctl->solver_c);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(RES_CTA) k_emit(const u32* __restrict__ flagw,
     const u32 fw = flagw[c >> 5];
     if (lane == 0) wcnt[warp] = __popc(fw);
     __syncthreads();
+    if (c < total) dest_out[c] = LTL_NONE;  // every candidate gets a verdict: the tile-shaped phase B reads it
     if (!((fw >> lane) & 1u) || c >= limit) return;
     u64 dest = blockoff[blockIdx.x] + __popc(fw & ((1u << lane) - 1u));
     for (int w = 0; w < warp; w++) dest += wcnt[w];
@@ -138,6 +140,7 @@ __global__ void __launch_bounds__(RES_CTA) k_emit(const u32* __restrict__ flagw,
         ctl->oom_c = c;
         return;
     }
+    dest_out[c] = (u32)dest;
     int lo = 0, hi = n_pieces - 1;
     while (lo < hi) {
         int mid = (lo + hi + 1) >> 1;
@@ -413,6 +416,15 @@ struct PendingEvent {
     cudaEvent_t a, b;
 };
 
+// An admitted range whose matrices are still to be written.  While d_dest still holds the verdicts of the pass
+// that admitted it (`tiled`), phase B runs tile-shaped over the same pieces as phase A; otherwise from records.
+struct PendingMat {
+    u64 n_base = 0, count = 0;
+    bool tiled = false;
+    std::vector<Piece> pieces;
+    i64 total = 0, tiles = 0;
+};
+
 // a unit of enumeration before chunking
 struct Unit {
     int kind, op, seg;
@@ -437,6 +449,7 @@ struct Arena {
     u64 table_cap = 0;
     i64 scratch_cap = 0;
     u32* d_slot = nullptr;
+    u32* d_dest = nullptr;  // per candidate of the last admission pass: index among the winners / NONE
     u32* d_flagw = nullptr;
     u32* d_blocksum = nullptr;
     u64* d_blockoff = nullptr;
@@ -473,6 +486,7 @@ struct Arena {
         cudaFree(d_masks);
         cudaFree(d_deps);
         cudaFree(d_slot);
+        cudaFree(d_dest);
         cudaFree(d_flagw);
         cudaFree(d_blocksum);
         cudaFree(d_blockoff);
@@ -548,6 +562,7 @@ struct ltl_core : Arena {
     int sm_count = 148;
     int max_split = 4096, force_split = 0;
     bool fuse_unary = true;
+    bool tiled_materialize = true;  // phase B over phase A's tiles (operand lines read once) instead of per record
     bool device_oom = false;      // an S_OOM came from the device, not from the logical budget
     bool store_results = true;    // false: admitted entries get records and fingerprints but no matrix
     u64 unstored_from = ~0ull;    // first entry index without a stored matrix
@@ -555,7 +570,7 @@ struct ltl_core : Arena {
     KStat stats[LTL_K_COUNT];
     std::vector<PendingEvent> pending;
     u64* fp_ext = nullptr;  // MODE_FP_ONLY output override (device pointer owned by the caller)
-    std::vector<std::pair<u64, u64>> pending_mat;  // (first entry, count) admitted, matrices not yet written
+    std::vector<PendingMat> pending_mat;  // admitted ranges whose matrices are not yet written
     std::string err;
 
     int fail(int code, const std::string& msg) {
@@ -644,20 +659,30 @@ static int ensure_table(ltl_core* h, u64 need_keys) {
     return LTL_OK;
 }
 
+static int flush_materialize(ltl_core* h);
+
 static int ensure_scratch(ltl_core* h, i64 total) {
     if (total <= h->scratch_cap) return LTL_OK;
+    for (auto& pm : h->pending_mat)
+        if (pm.tiled) {  // the verdict array is about to be reallocated
+            int rcf = flush_materialize(h);
+            if (rcf) return rcf;
+            break;
+        }
     i64 cap = std::max<i64>(total, std::min<i64>(h->chunk_cap, std::max<i64>(h->scratch_cap * 4, 1 << 16)));
     cap = ((cap + RES_CTA - 1) / RES_CTA) * RES_CTA;
     CK(cudaStreamSynchronize(h->stream));
     cudaFree(h->d_slot);
+    cudaFree(h->d_dest);
     cudaFree(h->d_flagw);
     cudaFree(h->d_blocksum);
     cudaFree(h->d_blockoff);
-    h->d_slot = nullptr;
+    h->d_slot = h->d_dest = nullptr;
     h->d_flagw = h->d_blocksum = nullptr;
     h->d_blockoff = nullptr;
     h->scratch_cap = 0;
     CK(cudaMalloc(&h->d_slot, (size_t)cap * 4));
+    CK(cudaMalloc(&h->d_dest, (size_t)cap * 4));
     CK(cudaMalloc(&h->d_flagw, (size_t)(cap / 32) * 4));
     CK(cudaMalloc(&h->d_blocksum, (size_t)(cap / RES_CTA) * 4));
     CK(cudaMalloc(&h->d_blockoff, (size_t)(cap / RES_CTA) * 8));
@@ -849,7 +874,7 @@ struct ChunkOut {
 
 static void choose_split(ltl_core* h, i64 tiles, int* nsplit, int* rows_per_split) {
     int ns = 1;
-    const i64 target = (i64)h->sm_count * 16;  // warps wanted in flight
+    const i64 target = (i64)h->sm_count * 16 * 4;  // warps wanted: 4 waves, so uneven tiles still balance
     if (h->force_split > 0) ns = h->force_split;
     else if (tiles < target && h->R >= 2 * LTL_SPLIT_ROWS) ns = (int)std::min<i64>((target + tiles - 1) / tiles, h->max_split);
     const int max_ns = (h->R + LTL_SPLIT_ROWS - 1) / LTL_SPLIT_ROWS;
@@ -872,6 +897,9 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     int rc;
     if (total <= 0) return LTL_OK;
     if (mode == MODE_INSERT) {
+        bool tiled_pending = false;
+        for (auto& pm : h->pending_mat) tiled_pending |= pm.tiled;
+        if (tiled_pending && (rc = flush_materialize(h))) return rc;  // this pass overwrites the verdicts they need
         if ((rc = ensure_table(h, h->keys_upper + (u64)total))) return rc;
         if ((rc = ensure_scratch(h, total))) return rc;
         const u64 room = h->cap_entries > h->n_entries ? h->cap_entries - h->n_entries : 0;
@@ -949,7 +977,7 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
             dim3 grid((unsigned)((t1 - t0 + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), (unsigned)p.nsplit);
             ScreenParams q = p;
             q.total_tiles = t1;
-            SCREEN_FN[h->W](q, mueller, grid, h->stream);
+            SCREEN_FN[h->W](q, mueller ? KIND_MUELLER : KIND_BITS, grid, h->stream);
             if (per < tiles) {
                 CK(cudaMemcpyAsync(h->h_solver + (k & 1), &h->d_ctl->solver_c, sizeof(u64), cudaMemcpyDeviceToHost, h->stream));
                 CK(cudaEventRecord(h->sub_ev[k & 1], h->stream));
@@ -989,7 +1017,7 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
             ScopedTimer t(h, LTL_K_EMIT, (u64)total, (double)total * 0.125);
             k_emit<<<nb, RES_CTA, 0, h->stream>>>(h->d_flagw, h->d_blockoff, h->d_pieces, (int)pieces.size(), (u64)total,
                                                    (i64)h->n_entries, room, (unsigned char*)h->rec_op.base,
-                                                   (int*)h->rec_lhs.base, (int*)h->rec_rhs.base, h->d_ctl);
+                                                   (int*)h->rec_lhs.base, (int*)h->rec_rhs.base, h->d_dest, h->d_ctl);
         }
         CK(cudaGetLastError());
         CK(cudaMemcpyAsync(h->h_ctl, h->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
@@ -1010,7 +1038,18 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     // Matrices are written lazily: the winners' records exist now, their matrices are only needed when they
     // first serve as operands (next cost level) or are read back -- a search that ends at this level (solved,
     // ceiling) never pays for them.
-    if (count > 0 && materialize && h->store_results) h->pending_mat.push_back({h->n_entries, count});
+    if (count > 0 && materialize && h->store_results) {
+        PendingMat pm;
+        pm.n_base = h->n_entries;
+        pm.count = count;
+        pm.tiled = h->tiled_materialize;
+        if (pm.tiled) {
+            pm.pieces = pieces;
+            pm.total = total;
+            pm.tiles = tiles;
+        }
+        h->pending_mat.push_back(std::move(pm));
+    }
     // ---- counters (reference _speedups.pyx:347-354, 372-379)
     u64 offered_c;
     if (oom) {
@@ -1046,9 +1085,41 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
 // Phase B for every admitted-but-unwritten range.
 static int flush_materialize(ltl_core* h) {
     int rc;
-    for (auto& pr : h->pending_mat) {
-        const u64 n_base = pr.first, count = pr.second;
+    for (auto& pm : h->pending_mat) {
+        const u64 n_base = pm.n_base, count = pm.count;
         if ((rc = ensure_entries(h, n_base + count))) return rc;
+        const double bytes = (double)count * (8.0 * (double)h->n + 16.0 + 9.0);
+        if (pm.tiled) {
+            // tile-shaped: the same pieces / tiles as phase A; every lane looks up its candidates' verdicts
+            // (d_dest) and stores the winners, so each operand line is read once per tile
+            if ((rc = ensure_pieces(h, (int)pm.pieces.size()))) return rc;
+            CK(cudaStreamSynchronize(h->stream));
+            memcpy(h->h_pieces, pm.pieces.data(), sizeof(Piece) * pm.pieces.size());
+            CK(cudaMemcpyAsync(h->d_pieces, h->h_pieces, sizeof(Piece) * pm.pieces.size(), cudaMemcpyHostToDevice, h->stream));
+            h->h2d_bytes += sizeof(Piece) * pm.pieces.size();
+            ScreenParams p;
+            memset(&p, 0, sizeof(p));
+            p.cms = (const u64*)h->cms.base;
+            p.cms_out = (u64*)h->cms.base;
+            p.masks = h->d_masks;
+            p.pieces = h->d_pieces;
+            p.n_pieces = (int)pm.pieces.size();
+            p.R = h->R;
+            p.W = h->W;
+            p.n_pos = h->n_pos;
+            p.n = h->n;
+            p.total_tiles = pm.tiles;
+            choose_split(h, pm.tiles, &p.nsplit, &p.rows_per_split);
+            p.mode = MODE_REWRITE;
+            p.dest = h->d_dest;
+            p.n_base = (i64)n_base;
+            p.ctl = h->d_ctl;
+            ScopedTimer t(h, LTL_K_MATERIALIZE, count, bytes);
+            dim3 grid((unsigned)((pm.tiles + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), (unsigned)p.nsplit);
+            SCREEN_FN[h->W](p, KIND_REWRITE, grid, h->stream);
+            CK(cudaGetLastError());
+            continue;
+        }
         MaterializeParams m;
         memset(&m, 0, sizeof(m));
         m.cms = (u64*)h->cms.base;
@@ -1063,7 +1134,7 @@ static int flush_materialize(ltl_core* h) {
         m.rec_rhs = (const int*)h->rec_rhs.base;
         const i64 groups = (i64)((n_base + count + 31) / 32 - n_base / 32);
         choose_split(h, groups, &m.nsplit, &m.rows_per_split);
-        ScopedTimer t(h, LTL_K_MATERIALIZE, count, (double)count * (8.0 * (double)h->n + 16.0 + 9.0));
+        ScopedTimer t(h, LTL_K_MATERIALIZE, count, bytes);
         dim3 grid((unsigned)((groups + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), (unsigned)m.nsplit);
         MATERIALIZE_FN[h->W](m, grid, h->stream);
         CK(cudaGetLastError());
@@ -1649,6 +1720,8 @@ int ltl_core_set_option(ltl_core* h, const char* name, int64_t value) {
     } else if (!strcmp(name, "store_results")) {
         if (value && h->unstored_from != ~0ull) return h->fail(LTL_ERR_ARG, "matrices were already skipped: storing cannot resume");
         h->store_results = value != 0;
+    } else if (!strcmp(name, "tiled_materialize")) {
+        h->tiled_materialize = value != 0;
     } else if (!strcmp(name, "fuse_unary")) {
         h->fuse_unary = value != 0;
     } else if (!strcmp(name, "profile")) {
@@ -1806,7 +1879,12 @@ int ltl_core_stage_append(ltl_core* h, const unsigned char* d_op, const int32_t*
         CK(cudaMemcpyAsync(h->rec_lhs.base + h->n_entries * 4, d_lhs, (size_t)count * 4, cudaMemcpyDeviceToDevice, h->stream));
         CK(cudaMemcpyAsync(h->rec_rhs.base + h->n_entries * 4, d_rhs, (size_t)count * 4, cudaMemcpyDeviceToDevice, h->stream));
         CK(cudaStreamSynchronize(h->stream));
-        if (h->store_results) h->pending_mat.push_back({h->n_entries, (u64)count});
+        if (h->store_results) {
+            PendingMat pm;
+            pm.n_base = h->n_entries;
+            pm.count = (u64)count;
+            h->pending_mat.push_back(std::move(pm));
+        }
         else if (h->unstored_from == ~0ull) h->unstored_from = h->n_entries;
         h->n_entries += (u64)count;
         h->admitted += (u64)count;

@@ -1,6 +1,6 @@
 // screen.cuh -- the two hot kernels of the screening core, templated on W = words per row.
 //
-//   k_screen<W, MUELLER>   "phase A": one warp per tile of (<= 4 entries of one operand) x (32 entries of
+//   k_screen<W, KIND>      "phase A" (KIND_MUELLER / KIND_BITS), and with KIND_REWRITE the tile-shaped phase B: one warp per tile of (<= 4 entries of one operand) x (32 entries of
 //       the other); every lane evaluates its candidates' characteristic matrices row by row IN REGISTERS
 //       (nothing is written back), counts P/N classification errors (fused solve check, reference
 //       _speedups.pyx:327-333), folds the rows into the 126-bit fingerprint (reference _speedups.pyx:185-231)
@@ -190,9 +190,11 @@ __host__ __device__ constexpr bool ops_need_mask() {
                        ((OPS >> 12) & 15) == OP_NOT || ((OPS >> 12) & 15) == OP_GLOBALLY);
 }
 
-template <int W, bool MUELLER, int OP, int TI, bool XL>
+template <int W, int KIND, int OP, int TI, bool XL>
 __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc, const i64 row0, const i64 lg,
                                           const int split, const int lane, u64* __restrict__ sbuf, u64* bars) {
+    constexpr bool MUELLER = KIND == KIND_MUELLER;
+    constexpr bool REWRITE = KIND == KIND_REWRITE;
     constexpr bool FUSED = OP >= 16;
     constexpr bool BIN = !op_unary_c(slot_op<OP>(0));
     constexpr bool NEEDM = ops_need_mask<OP>();
@@ -204,6 +206,44 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
 
     const int r0 = split * p.rows_per_split;
     const int r1 = min(p.R, r0 + p.rows_per_split);
+
+    // candidate of (lane, slot t): validity and chunk-local rank
+    const bool lane_in = pc.kind == PIECE_UNARY ? (e >= pc.i0 && e < pc.i1)
+                         : pc.kind == PIECE_RECT ? (pc.swap ? (e >= pc.i0 && e < pc.i1) : (e >= pc.j0 && e < pc.j1))
+                                                 : (e < pc.j1);
+    auto slot_rank = [&](const int t, u64* c) -> bool {
+        i64 ci, cj;
+        if (pc.kind == PIECE_UNARY) {
+            ci = e;
+            cj = -1;
+        } else if (pc.kind == PIECE_RECT && pc.swap) {
+            ci = e;
+            cj = row0 + t;
+        } else {
+            ci = row0 + t;
+            cj = e;
+        }
+        if (!(lane_in && (pc.kind != PIECE_TRI || cj > ci))) return false;
+        *c = FUSED ? (u64)pc.fcbase[t] + (u64)(e - pc.i0) : piece_rank(pc, ci, cj);
+        return true;
+    };
+    u64* __restrict__ pd[TI];  // REWRITE: where this lane's slot-t matrix goes (null: not a winner)
+    if (REWRITE) {
+        bool any = false;
+#pragma unroll
+        for (int t = 0; t < TI; t++) {
+            u64 c;
+            pd[t] = nullptr;
+            if (slot_rank(t, &c)) {
+                const u32 d = p.dest[c];
+                if (d != LTL_NONE) {
+                    pd[t] = p.cms_out + cm_index(p.n_base + (i64)d, n, 0);
+                    any = true;
+                }
+            }
+        }
+        if (!__any_sync(0xFFFFFFFFu, any)) return;  // no winner in this tile
+    }
 
     u64 s0[TI], s1[TI], h0[TI], h1[TI];
     // Verdict bits (MSB of word 0 of every row) are COUNTED with one multiply-add-high per row on the FMA pipe
@@ -219,7 +259,7 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
     }
     u64 tw = ((u64)r0 * W + 1ull) * K_STEP;  // (k + 1) * STEP for the next word k
     int d = 0;                               // next deposit (bits fingerprints)
-    if (!MUELLER) {
+    if (KIND == KIND_BITS) {
         const u32 kfirst = (u32)r0 * W;
         int lo_ = 0, hi_ = p.n_dep;
         while (lo_ < hi_) {
@@ -266,6 +306,13 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
             if (!BIN) apply_slot<OP, W>(t, out, a, a, m);
             else if (XL) apply_slot<OP, W>(t, out, a, b, m);
             else apply_slot<OP, W>(t, out, b, a, m);
+            if (REWRITE) {
+                if (pd[t]) {
+#pragma unroll
+                    for (int w = 0; w < W; w++) pd[t][(kb + w) * 32] = out[w];
+                }
+                continue;
+            }
             asm("mad.hi.u32 %0, %1, 2, %0;" : "+r"(ones[t]) : "r"((u32)(out[0] >> 32)));
             if (MUELLER) {
 #pragma unroll
@@ -365,6 +412,7 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
     }
 
     // ---- per-candidate epilogue
+    if (REWRITE) return;
     u32 err[TI];
     {
         const int npos_here = max(0, min(r1, p.n_pos) - r0);  // positive rows of this split
@@ -374,25 +422,10 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
             err[t] = ((u32)npos_here - ones_pos[t]) + (ones[t] - ones_pos[t]);
         }
     }
-    const bool lane_in = pc.kind == PIECE_UNARY ? (e >= pc.i0 && e < pc.i1)
-                         : pc.kind == PIECE_RECT ? (pc.swap ? (e >= pc.i0 && e < pc.i1) : (e >= pc.j0 && e < pc.j1))
-                                                 : (e < pc.j1);
 #pragma unroll
     for (int t = 0; t < TI; t++) {
-        i64 ci, cj;
-        if (pc.kind == PIECE_UNARY) {
-            ci = e;
-            cj = -1;
-        } else if (pc.kind == PIECE_RECT && pc.swap) {
-            ci = e;
-            cj = row0 + t;
-        } else {
-            ci = row0 + t;
-            cj = e;
-        }
-        const bool valid = lane_in && (pc.kind != PIECE_TRI || cj > ci);
-        if (!valid) continue;
-        const u64 c = FUSED ? (u64)pc.fcbase[t] + (u64)(e - pc.i0) : piece_rank(pc, ci, cj);
+        u64 c;
+        if (!slot_rank(t, &c)) continue;
         if (p.nsplit > 1) {
             atomicAdd(p.acc_s0 + c, s0[t]);
             atomicAdd(p.acc_s1 + c, s1[t]);
@@ -406,7 +439,7 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
 // ------------------------------------------------------------------------------------------------
 // phase A kernel
 
-template <int W, bool MUELLER>
+template <int W, int KIND>
 __global__ void __launch_bounds__(LTL_CTA, 2) k_screen(const __grid_constant__ ScreenParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
@@ -480,10 +513,10 @@ __global__ void __launch_bounds__(LTL_CTA, 2) k_screen(const __grid_constant__ S
     }
     const bool xl = pc.swap != 0;
 
-#define LTL_TILE(OP_, TI_, XL_) tile_eval<W, MUELLER, OP_, TI_, XL_>(p, pc, row0, lg, split, lane, sbuf, bars)
+#define LTL_TILE(OP_, TI_, XL_) tile_eval<W, KIND, OP_, TI_, XL_>(p, pc, row0, lg, split, lane, sbuf, bars)
 #define LTL_TILE_TI(OP_, XL_)                       \
     do {                                            \
-        if (W == 1 && MUELLER) {                    \
+        if (W == 1 && KIND != KIND_BITS) {          \
             switch (nv) {                           \
                 case 1: LTL_TILE(OP_, 1, XL_); break; \
                 case 2: LTL_TILE(OP_, 2, XL_); break; \
@@ -495,7 +528,7 @@ __global__ void __launch_bounds__(LTL_CTA, 2) k_screen(const __grid_constant__ S
         }                                           \
     } while (0)
 
-    if (W == 1 && MUELLER && pc.kind == PIECE_UNARY && pc.nfuse > 1) {
+    if (W == 1 && KIND != KIND_BITS && pc.kind == PIECE_UNARY && pc.nfuse > 1) {
         // connectives whose every candidate of this tile ranks above a known solver are dropped (they form a
         // suffix: fused connectives are consecutive in enumeration order)
         int nf = pc.nfuse;
@@ -603,5 +636,5 @@ __global__ void __launch_bounds__(LTL_CTA) k_materialize(const __grid_constant__
 #endif  // __CUDACC__
 
 // launchers, one translation unit per W (screen_inst.cu compiled with -DLTL_W=<W>)
-typedef void (*screen_launch_fn)(const ScreenParams&, bool mueller, dim3 grid, cudaStream_t stream);
+typedef void (*screen_launch_fn)(const ScreenParams&, int kind, dim3 grid, cudaStream_t stream);
 typedef void (*materialize_launch_fn)(const MaterializeParams&, dim3 grid, cudaStream_t stream);

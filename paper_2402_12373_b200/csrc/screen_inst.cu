@@ -8,15 +8,17 @@
 #define LTL_CAT2(a, b) a##b
 #define LTL_CAT(a, b) LTL_CAT2(a, b)
 
-extern "C" void LTL_CAT(ltl_launch_screen_w, LTL_W)(const ScreenParams& p, bool mueller, dim3 grid, cudaStream_t stream) {
+extern "C" void LTL_CAT(ltl_launch_screen_w, LTL_W)(const ScreenParams& p, int kind, dim3 grid, cudaStream_t stream) {
     static bool configured = false;
     if (!configured) {  // > 48 KiB of dynamic shared memory needs an opt-in, once per process
-        cudaFuncSetAttribute(k_screen<LTL_W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Ring<LTL_W>::CTA_BYTES);
-        cudaFuncSetAttribute(k_screen<LTL_W, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, Ring<LTL_W>::CTA_BYTES);
+        cudaFuncSetAttribute(k_screen<LTL_W, KIND_MUELLER>, cudaFuncAttributeMaxDynamicSharedMemorySize, Ring<LTL_W>::CTA_BYTES);
+        cudaFuncSetAttribute(k_screen<LTL_W, KIND_BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, Ring<LTL_W>::CTA_BYTES);
+        cudaFuncSetAttribute(k_screen<LTL_W, KIND_REWRITE>, cudaFuncAttributeMaxDynamicSharedMemorySize, Ring<LTL_W>::CTA_BYTES);
         configured = true;
     }
-    if (mueller) k_screen<LTL_W, true><<<grid, LTL_CTA, Ring<LTL_W>::CTA_BYTES, stream>>>(p);
-    else k_screen<LTL_W, false><<<grid, LTL_CTA, Ring<LTL_W>::CTA_BYTES, stream>>>(p);
+    if (kind == KIND_MUELLER) k_screen<LTL_W, KIND_MUELLER><<<grid, LTL_CTA, Ring<LTL_W>::CTA_BYTES, stream>>>(p);
+    else if (kind == KIND_BITS) k_screen<LTL_W, KIND_BITS><<<grid, LTL_CTA, Ring<LTL_W>::CTA_BYTES, stream>>>(p);
+    else k_screen<LTL_W, KIND_REWRITE><<<grid, LTL_CTA, Ring<LTL_W>::CTA_BYTES, stream>>>(p);
 }
 
 extern "C" void LTL_CAT(ltl_launch_materialize_w, LTL_W)(const MaterializeParams& p, dim3 grid, cudaStream_t stream) {
