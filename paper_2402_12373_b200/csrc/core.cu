@@ -562,7 +562,7 @@ struct ltl_core : Arena {
     int sm_count = 148;
     int max_split = 4096, force_split = 0;
     bool fuse_unary = true;
-    bool tiled_materialize = true;  // phase B over phase A's tiles (operand lines read once) instead of per record
+    int tiled_materialize = -1;  // phase B over phase A's tiles instead of per record: 1 always, 0 never, -1 by size
     bool device_oom = false;      // an S_OOM came from the device, not from the logical budget
     bool store_results = true;    // false: admitted entries get records and fingerprints but no matrix
     u64 unstored_from = ~0ull;    // first entry index without a stored matrix
@@ -1042,7 +1042,9 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
         PendingMat pm;
         pm.n_base = h->n_entries;
         pm.count = count;
-        pm.tiled = h->tiled_materialize;
+        // per-record gathers waste most of each sector once matrices are long and buckets small; with short
+        // matrices and dense winners the record form reads less (losers are never evaluated) -- measured both ways
+        pm.tiled = h->tiled_materialize == 1 || (h->tiled_materialize < 0 && h->n >= 4096);
         if (pm.tiled) {
             pm.pieces = pieces;
             pm.total = total;
@@ -1721,7 +1723,7 @@ int ltl_core_set_option(ltl_core* h, const char* name, int64_t value) {
         if (value && h->unstored_from != ~0ull) return h->fail(LTL_ERR_ARG, "matrices were already skipped: storing cannot resume");
         h->store_results = value != 0;
     } else if (!strcmp(name, "tiled_materialize")) {
-        h->tiled_materialize = value != 0;
+        h->tiled_materialize = (int)value;
     } else if (!strcmp(name, "fuse_unary")) {
         h->fuse_unary = value != 0;
     } else if (!strcmp(name, "profile")) {

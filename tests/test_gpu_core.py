@@ -375,3 +375,34 @@ def test_sub_launched_levels_match_oracle(sub_tiles, chunk):
     for lv in a["levels"] + b["levels"]:
         lv.pop("ms", None)
     assert a == b
+
+
+@pytest.mark.parametrize("tiled", [0, 1])
+@pytest.mark.parametrize("R,W", [(64, 1), (300, 2), (40, 16)])
+def test_both_phase_b_forms_match_oracle(tiled, R, W):
+    """Phase B from records (one warp per 32 new entries) and tile-shaped (phase A's tiles + verdicts)."""
+    from paper_2402_12373_b200.learner import Segment
+
+    rng = np.random.default_rng(R + W + tiled)
+    masks = random_masks(rng, R, W)
+    cuda, ora = make_pair(masks, R // 2, err_max=-1, W=W)
+    cuda.set_option("tiled_materialize", tiled)
+    drive.masks = masks
+    for k in range(5):
+        cm = random_cm(rng, masks)
+        assert cuda.add_entry(cm, 0, k, -1) == ora.add_entry(cm, 0, k, -1)
+    lo = 0
+    for _ in range(2):
+        hi = ora.n_entries
+        segs = [Segment(1, lo, hi), Segment(2, 0, hi, 0, hi, True), Segment(3, 0, hi, 0, hi, True), Segment(4, lo, hi),
+                Segment(5, lo, hi), Segment(6, lo, hi), Segment(7, 0, hi, 0, hi, False)]
+        st = cuda.run_level(segs)
+        for s in segs:
+            got = ora.screen_unary(s.op, s.a0, s.a1) if s.unary else ora.screen_binary(s.op, s.a0, s.a1, s.b0, s.b1, s.tri)
+            assert got[0] == 0
+        assert st[0] == 0
+        lo = hi
+        if ora.n_entries > 3000:
+            break
+    assert_same_state(cuda, ora)
+    cuda.close()
