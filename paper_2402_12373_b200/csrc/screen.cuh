@@ -129,7 +129,9 @@ template <int W>
 struct Ring {
     static constexpr int RPC = (W <= 8) ? 8 / W : 1;      // rows per stage
     static constexpr int STAGES = (W <= 8) ? 3 : 2;
-    static constexpr int STAGE_U64 = RPC * W * 32;         // 64-bit words per stage (<= 2 KiB for W <= 8)
+    static constexpr int LANE_U64 = RPC * W * 32;          // lane operand: 64-bit words per stage (<= 2 KiB for W <= 8)
+    static constexpr int ROW_U64 = 4 * RPC * W;            // row operands: up to 4 entries x the stage's words
+    static constexpr int STAGE_U64 = LANE_U64 + ROW_U64;
     static constexpr int WARP_U64 = STAGES * STAGE_U64;
     static constexpr int CTA_BYTES = LTL_WARPS_PER_CTA * WARP_U64 * 8 + LTL_WARPS_PER_CTA * STAGES * 8;
     static constexpr bool CHUNK_FOLD = (64 % (RPC * W)) == 0;  // hash blocks end on stage boundaries
@@ -157,6 +159,13 @@ __device__ __forceinline__ void mbar_wait(u64* bar, u32 parity) {
         "LAB_DONE:\n\t}" ::"r"(smem_u32(bar)),
         "r"(parity)
         : "memory");
+}
+// 8-byte asynchronous copy (LDGSTS) whose completion is reported to an mbarrier by the issuing thread
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive(u64* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
@@ -200,9 +209,6 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
     constexpr bool NEEDM = ops_need_mask<OP>();
     const i64 n = p.n;
     const i64 e = lg * 32 + lane;  // the lane operand's entry index
-    const u64* __restrict__ pr[TI];
-#pragma unroll
-    for (int t = 0; t < TI; t++) pr[t] = p.cms + cm_index(BIN ? row0 + t : 0, n, 0);
 
     const int r0 = split * p.rows_per_split;
     const int r1 = min(p.R, r0 + p.rows_per_split);
@@ -290,8 +296,10 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
         for (int t = 0; t < TI; t++) ones_pos[t] = ones[t];
     };
 
-    // src: this lane's column of the staged row (word w at src[w * 32])
-    auto do_row = [&](const int r, const u64* __restrict__ src) {
+    // src: this lane's column of the staged row (word w at src[w * 32]); xs: the row operands' words of that row
+    // (entry t at xs[t * RG_ROWSTRIDE + w])
+    constexpr int RG_ROWSTRIDE = Ring<W>::RPC * W;
+    auto do_row = [&](const int r, const u64* __restrict__ src, const u64* __restrict__ xs) {
         u64 a[W], m[W];
         const size_t kb = (size_t)r * W;
 #pragma unroll
@@ -302,7 +310,7 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
         for (int t = 0; t < TI; t++) {
             u64 b[W], out[W];
 #pragma unroll
-            for (int w = 0; w < W; w++) b[w] = BIN ? ld_nc(pr[t] + (kb + w) * 32) : 0ull;
+            for (int w = 0; w < W; w++) b[w] = BIN ? xs[t * RG_ROWSTRIDE + w] : 0ull;
             if (!BIN) apply_slot<OP, W>(t, out, a, a, m);
             else if (XL) apply_slot<OP, W>(t, out, a, b, m);
             else apply_slot<OP, W>(t, out, b, a, m);
@@ -362,38 +370,51 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
     const int rows_total = r1 - r0;
     const int nchunks = (rows_total + RG::RPC - 1) / RG::RPC;
     const u64* __restrict__ gsrc = p.cms + ((size_t)lg * (size_t)n + (size_t)r0 * W) * 32;
+    // one stage = the lane operand's next RPC rows (one bulk copy issued by lane 0) + the same rows of the
+    // TI row operands (strided in memory: one 8-byte cp.async per lane); all 32 lanes take part
+    const int my_t = lane / RG_ROWSTRIDE, my_i = lane - my_t * RG_ROWSTRIDE;
+    const u64* __restrict__ my_row = (BIN && my_t < TI) ? p.cms + cm_index(row0 + my_t, n, 0) : nullptr;
     auto issue = [&](const int c, const int s) {
         const int rows_c = min(RG::RPC, rows_total - c * RG::RPC);
-        const u32 bytes = (u32)rows_c * W * 256u;
-        mbar_expect_tx(bars + s, bytes);
-        bulk_g2s(sbuf + s * RG::STAGE_U64, gsrc + (size_t)c * RG::STAGE_U64, bytes, bars + s);
+        u64* stage_base = sbuf + s * RG::STAGE_U64;
+        if (lane == 0) {
+            const u32 bytes = (u32)rows_c * W * 256u;
+            mbar_expect_tx(bars + s, bytes);
+            bulk_g2s(stage_base, gsrc + (size_t)c * RG::LANE_U64, bytes, bars + s);
+        }
+        if (BIN) {
+            if (my_row && my_i < rows_c * W)
+                cp_async8(stage_base + RG::LANE_U64 + lane, my_row + ((size_t)(r0 + c * RG::RPC) * W + my_i) * 32);
+            cp_async_arrive(bars + s);
+        }
     };
     if (lane == 0) {
 #pragma unroll
-        for (int s = 0; s < RG::STAGES; s++) mbar_init(bars + s, 1);
+        for (int s = 0; s < RG::STAGES; s++) mbar_init(bars + s, BIN ? 33 : 1);
         fence_mbar_init();
         fence_async_smem();
-#pragma unroll
-        for (int s = 0; s < RG::STAGES; s++)
-            if (s < nchunks) issue(s, s);
     }
     __syncwarp();
+#pragma unroll
+    for (int s = 0; s < RG::STAGES; s++)
+        if (s < nchunks) issue(s, s);
     int stage = 0;
     u32 parity = 0;
     for (int c = 0; c < nchunks; c++) {
         mbar_wait(bars + stage, parity);
         const u64* __restrict__ src = sbuf + stage * RG::STAGE_U64 + lane;
+        const u64* __restrict__ xsrc = sbuf + stage * RG::STAGE_U64 + RG::LANE_U64;
         const int rbase = r0 + c * RG::RPC;
         const int rows_c = min(RG::RPC, r1 - rbase);
         const bool straddle = p.n_pos > rbase && p.n_pos < rbase + rows_c;
         if (rbase == p.n_pos) snapshot();
         if (rows_c == RG::RPC && !straddle) {
 #pragma unroll
-            for (int rr = 0; rr < RG::RPC; rr++) do_row(rbase + rr, src + rr * W * 32);
+            for (int rr = 0; rr < RG::RPC; rr++) do_row(rbase + rr, src + rr * W * 32, xsrc + rr * W);
         } else {
             for (int rr = 0; rr < rows_c; rr++) {
                 if (rr && rbase + rr == p.n_pos) snapshot();
-                do_row(rbase + rr, src + rr * W * 32);
+                do_row(rbase + rr, src + rr * W * 32, xsrc + rr * W);
             }
         }
         if (MUELLER && RG::CHUNK_FOLD) {
@@ -401,8 +422,8 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
             if ((((u32)rend * W) & 63u) == 0 || rend == p.R) fold((((u32)rend * W - 1) >> 6) == 0);
         }
         __syncwarp();
-        if (lane == 0 && c + RG::STAGES < nchunks) {
-            fence_async_smem();
+        if (c + RG::STAGES < nchunks) {
+            if (lane == 0) fence_async_smem();
             issue(c + RG::STAGES, stage);
         }
         if (++stage == RG::STAGES) {
