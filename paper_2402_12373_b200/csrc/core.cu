@@ -974,7 +974,7 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
             p.tile_offset = t0;
             const double frac = (double)(t1 - t0) / (double)tiles;
             ScopedTimer t(h, LTL_K_SCREEN, (u64)((double)total * frac), bytes_all * frac);
-            dim3 grid((unsigned)((t1 - t0 + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), (unsigned)p.nsplit);
+            dim3 grid((unsigned)(((t1 - t0) * p.nsplit + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), 1);
             ScreenParams q = p;
             q.total_tiles = t1;
             SCREEN_FN[h->W](q, mueller ? KIND_MUELLER : KIND_BITS, grid, h->stream);
@@ -1117,7 +1117,7 @@ static int flush_materialize(ltl_core* h) {
             p.n_base = (i64)n_base;
             p.ctl = h->d_ctl;
             ScopedTimer t(h, LTL_K_MATERIALIZE, count, bytes);
-            dim3 grid((unsigned)((pm.tiles + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), (unsigned)p.nsplit);
+            dim3 grid((unsigned)((pm.tiles * p.nsplit + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), 1);
             SCREEN_FN[h->W](p, KIND_REWRITE, grid, h->stream);
             CK(cudaGetLastError());
             continue;

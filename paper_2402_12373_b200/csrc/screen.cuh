@@ -467,9 +467,17 @@ __global__ void __launch_bounds__(LTL_CTA, 2) k_screen(const __grid_constant__ S
     const int warp = threadIdx.x >> 5;
     u64* sbuf = reinterpret_cast<u64*>(smem_raw) + warp * Ring<W>::WARP_U64;
     u64* bars = reinterpret_cast<u64*>(smem_raw) + LTL_WARPS_PER_CTA * Ring<W>::WARP_U64 + warp * Ring<W>::STAGES;
-    const i64 T = p.tile_offset + (i64)blockIdx.x * LTL_WARPS_PER_CTA + warp;
+    // warps are numbered over (row split, tile) so that every CTA is full even when a level has few tiles
+    const i64 gw = (i64)blockIdx.x * LTL_WARPS_PER_CTA + warp;
+    const i64 launch_tiles = p.total_tiles - p.tile_offset;
+    int split = 0;
+    i64 T = p.tile_offset + gw;
+    if (p.nsplit > 1) {
+        split = (int)(gw / launch_tiles);
+        T = p.tile_offset + (gw - (i64)split * launch_tiles);
+        if (split >= p.nsplit) return;
+    }
     if (T >= p.total_tiles) return;
-    const int split = blockIdx.y;
     // piece of this tile: last piece with tile_base <= T
     int lo = 0, hi = p.n_pieces - 1;
     while (lo < hi) {

@@ -1,0 +1,21 @@
+import sys, time
+sys.path.insert(0, '/root/repo')
+import numpy as np, torch
+from paper_2402_12373_b200 import workloads as Wl
+from paper_2402_12373_b200.learner import learn
+from paper_2402_12373_b200.traces import Specification
+spec, al, f, cfg = Wl.make_config("c2_planted")
+pc, pl = spec.chars[:spec.n_pos].copy(), spec.lengths[:spec.n_pos].copy()
+nc, nl = spec.chars[spec.n_pos:].copy(), spec.lengths[spec.n_pos:].copy()
+flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+for rep in range(6):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    s = Specification.from_arrays(pc, pl, nc, nl)
+    t1 = time.perf_counter()
+    r = learn(s, None, al, max_cost=12, budget_bytes=150 << 30)
+    t2 = time.perf_counter()
+    flush.fill_(1)
+    torch.cuda.synchronize()
+    t3 = time.perf_counter()
+    print(f"spec {1e3*(t1-t0):.2f}  learn {1e3*(t2-t1):.2f}  (search {1e3*r.stats.search_seconds:.2f})  flush {1e3*(t3-t2):.2f}")
