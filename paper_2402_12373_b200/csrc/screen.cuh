@@ -125,6 +125,10 @@ __device__ __forceinline__ void finish_candidate(const ScreenParams& p, u64 c, u
 // one storage group are ONE contiguous stream of 256-byte lines, so a warp prefetches it with 1-D bulk
 // copies (TMA engine, cp.async.bulk) into its private shared-memory ring, completion on an mbarrier.
 
+#ifndef LTL_ROW_UNROLL
+#define LTL_ROW_UNROLL 2
+#endif
+
 template <int W>
 struct Ring {
     static constexpr int RPC = (W <= 8) ? 8 / W : 1;      // rows per stage
@@ -409,7 +413,9 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
         const bool straddle = p.n_pos > rbase && p.n_pos < rbase + rows_c;
         if (rbase == p.n_pos) snapshot();
         if (rows_c == RG::RPC && !straddle) {
-#pragma unroll
+            // partial unroll: a fully unrolled stage of a 4-slot tile is ~24 KB of code, and a level with many
+            // small pieces runs a dozen tile variants per SM -- ncu showed `no_instructions` as the top stall
+#pragma unroll LTL_ROW_UNROLL
             for (int rr = 0; rr < RG::RPC; rr++) do_row(rbase + rr, src + rr * W * 32, xsrc + rr * W);
         } else {
             for (int rr = 0; rr < rows_c; rr++) {
