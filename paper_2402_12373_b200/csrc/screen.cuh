@@ -128,6 +128,7 @@ __device__ __forceinline__ void finish_candidate(const ScreenParams& p, u64 c, u
 #ifndef LTL_ROW_UNROLL
 #define LTL_ROW_UNROLL 2
 #endif
+constexpr int kRowUnroll = LTL_ROW_UNROLL;
 
 template <int W>
 struct Ring {
@@ -415,7 +416,7 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
         if (rows_c == RG::RPC && !straddle) {
             // partial unroll: a fully unrolled stage of a 4-slot tile is ~24 KB of code, and a level with many
             // small pieces runs a dozen tile variants per SM -- ncu showed `no_instructions` as the top stall
-#pragma unroll LTL_ROW_UNROLL
+#pragma unroll kRowUnroll
             for (int rr = 0; rr < RG::RPC; rr++) do_row(rbase + rr, src + rr * W * 32, xsrc + rr * W);
         } else {
             for (int rr = 0; rr < rows_c; rr++) {
