@@ -107,13 +107,14 @@ def oracle_factory(threads: int):
     return make
 
 
-def cpu_sample(spec, alphabet, sample_cost: int, threads: int):
+def cpu_sample(spec, alphabet, sample_cost: int, threads: int, hash_name: str = "mueller"):
     """The CPU oracle port on the same specification, levels 2..sample_cost: (candidates, seconds)."""
     from paper_2402_12373_b200.learner import learn
+    from paper_2402_12373_b200.scheme import HashScheme
 
     t0 = time.perf_counter()
     res = learn(spec, None, alphabet, max_cost=sample_cost, core_factory=oracle_factory(threads),
-                overfit_on_ceiling=False, budget_bytes=48 << 30)
+                overfit_on_ceiling=False, budget_bytes=48 << 30, hash=HashScheme(hash_name))
     return res.stats.offered, time.perf_counter() - t0, res
 
 
@@ -130,10 +131,10 @@ def run_reference_arm(args, spec, alphabet, cfg):
     threads = cpu_oracle.max_threads()
     sample_cost = args.ref_sample_cost
     for _ in range(args.warmup):
-        cpu_sample(spec, alphabet, min(sample_cost, 6), threads)
+        cpu_sample(spec, alphabet, min(sample_cost, 6), threads, args.hash)
     cands = secs = 0
     for _ in range(args.steps):
-        c, s, _ = cpu_sample(spec, alphabet, sample_cost, threads)
+        c, s, _ = cpu_sample(spec, alphabet, sample_cost, threads, args.hash)
         cands += c
         secs += s
     value = cands / secs
@@ -160,6 +161,8 @@ def main():
     ap.add_argument("--ref-sample-cost", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--budget-gb", type=float, default=150.0)
+    ap.add_argument("--hash", default="mueller", choices=["mueller", "mueller_blocked", "nh", "fkp"],
+                    help="fingerprint scheme (scheme.py): 'mueller' = the reference's hash inside its domain, NH beyond")
     args = ap.parse_args()
 
     from paper_2402_12373_b200 import workloads as Wl
@@ -172,6 +175,7 @@ def main():
         "workload": f"{args.config}: {wl['n_props']} props, {wl['n_pos']}+{wl['n_neg']} traces of length "
                     f"{wl['min_len']}..{wl['max_len']}, planted '{print_formula(planted, alphabet)}', max_cost {max_cost}",
         "rows": spec.size, "words_per_row": -(-spec.max_len // 64), "max_cost": max_cost, "seed": wl["seed"],
+        "hash": args.hash,
         "l2": "inputs larger than L2 (entry store grows to GBs per step) + explicit 256 MiB L2 flush between steps",
     }
     if args.impl == "reference":
@@ -189,7 +193,9 @@ def main():
 
     torch.cuda.set_device(local_rank)
     budget = int(args.budget_gb * (1 << 30))
-    lcfg = LearnerConfig(ceiling=max_cost + 1, budget_bytes=budget, device=local_rank)
+    from paper_2402_12373_b200.scheme import HashScheme
+
+    lcfg = LearnerConfig(ceiling=max_cost + 1, budget_bytes=budget, device=local_rank, hash=HashScheme(args.hash))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def resident_search(profile: bool):
@@ -278,7 +284,8 @@ def main():
         ta = time.perf_counter()
         s = Specification.from_arrays(pos_c, pos_l, neg_c, neg_l)
         tb = time.perf_counter()
-        out = learn(s, None, alphabet, max_cost=max_cost, budget_bytes=budget, device=local_rank)
+        out = learn(s, None, alphabet, max_cost=max_cost, budget_bytes=budget, device=local_rank,
+                    hash=HashScheme(args.hash))
         e2e_parts["spec_ms"] += 1e3 * (tb - ta)
         e2e_parts["learn_ms"] += 1e3 * (time.perf_counter() - tb)
         return out
@@ -307,7 +314,7 @@ def main():
         from oracle import cpu_oracle
 
         threads = cpu_oracle.max_threads()
-        c, s, _ = cpu_sample(spec, alphabet, min(args.cpu_sample_cost, max_cost - 1), threads)
+        c, s, _ = cpu_sample(spec, alphabet, min(args.cpu_sample_cost, max_cost - 1), threads, args.hash)
         cpu = {"value": c / s, "unit": UNIT, "cores": threads, "kind": "port",
                "sample": f"cost levels 2..{min(args.cpu_sample_cost, max_cost - 1)} of the same specification "
                          f"({c} candidates, {s:.1f} s)"}

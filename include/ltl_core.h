@@ -46,6 +46,9 @@ extern "C" {
 #define LTL_V_GATHER 0
 #define LTL_V_MUELLER 1
 #define LTL_V_FKP 2
+/* not in the reference: this build's NH hash for matrices of more than 64 words, where the reference defines
+ * nothing (it refuses such inputs, enumerator.py:70-73).  Definition: oracle/ltl_oracle.c fp_nh, DESIGN.md 3. */
+#define LTL_V_NH 3
 
 /* error codes */
 #define LTL_OK 0

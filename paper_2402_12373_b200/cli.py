@@ -1,6 +1,6 @@
 """`learn` command line (the reference specifies it, `/root/reference/SPEC.md:569-608`, but ships none).
 
-    python -m paper_2402_12373_b200.cli learn TRACE_FILE [--max-cost N] [--hash mueller|fkp] [--mask-bits K]
+    python -m paper_2402_12373_b200.cli learn TRACE_FILE [--max-cost N] [--hash mueller|fkp|mueller_blocked|nh] [--mask-bits K]
         [--nnf] [--no-until] [--noise EPS] [--budget BYTES] [--costs a,n,c,d,x,f,g,u] [--timeout SECS]
         [--device D] [--json PATH] [--verify]
 
@@ -79,7 +79,7 @@ def main(argv=None) -> int:
     lp = sub.add_parser("learn", help="learn a minimal separating LTL formula from a trace file")
     lp.add_argument("trace_file")
     lp.add_argument("--max-cost", type=int, default=None, help="inclusive cost bound (default: up to the overfit cost)")
-    lp.add_argument("--hash", choices=["mueller", "fkp"], default="mueller")
+    lp.add_argument("--hash", choices=["mueller", "fkp", "mueller_blocked", "nh"], default="mueller")
     lp.add_argument("--mask-bits", type=int, default=0)
     lp.add_argument("--nnf", action="store_true")
     lp.add_argument("--no-until", action="store_true")

@@ -21,10 +21,10 @@ typedef long long i64;
 
 // opcodes (reference formula.py:13-20); 0 doubles as "identity" for add_entry / fingerprint_of.
 enum { OP_IDENT = 0, OP_NOT = 1, OP_AND = 2, OP_OR = 3, OP_NEXT = 4, OP_FINALLY = 5, OP_GLOBALLY = 6, OP_UNTIL = 7 };
-enum { VAR_GATHER = 0, VAR_MUELLER = 1, VAR_FKP = 2 };
+enum { VAR_GATHER = 0, VAR_MUELLER = 1, VAR_FKP = 2, VAR_NH = 3 };  // NH: this build's hash beyond the reference's domain
 enum { PIECE_UNARY = 0, PIECE_RECT = 1, PIECE_TRI = 2 };
 enum { MODE_INSERT = 0, MODE_FP_ONLY = 1, MODE_LOOKUP = 2, MODE_REWRITE = 3 };
-enum { KIND_BITS = 0, KIND_MUELLER = 1, KIND_REWRITE = 2 };  // what a k_screen instantiation does with a row
+enum { KIND_BITS = 0, KIND_MUELLER = 1, KIND_REWRITE = 2, KIND_NH = 3 };  // what a k_screen instantiation does with a row
 
 #define LTL_GROUP 32
 #define LTL_NONE 0xFFFFFFFFu
@@ -150,6 +150,28 @@ __host__ __device__ __forceinline__ u64 mix64(u64 x) {  // reference kernels.py:
     x ^= x >> 31;
     return x;
 }
+
+// NH fingerprint (VAR_NH): key table KEY[j] = mix64((j+1)*STEP + SEED0), j = 0..64 (definition: oracle/ltl_oracle.c
+// fp_nh).  Two Toeplitz-shifted NH accumulators per 64-word block; one 32x32->64 multiply-add each per word.
+constexpr u64 mix64_c(u64 x) {
+    x ^= x >> 30;
+    x *= K_MIX1;
+    x ^= x >> 27;
+    x *= K_MIX2;
+    x ^= x >> 31;
+    return x;
+}
+struct NhKeys {
+    u64 k[66];
+    constexpr NhKeys() : k{} {
+        for (int j = 0; j < 65; j++) k[j] = mix64_c((u64)(j + 1) * K_STEP + K_SEED0);
+        k[65] = 0;
+    }
+};
+#ifdef __CUDACC__
+static __constant__ NhKeys c_nh = NhKeys();
+#endif
+static constexpr NhKeys h_nh = NhKeys();
 
 __host__ __device__ __forceinline__ size_t cm_index(i64 e, i64 n, i64 k) {
     return ((size_t)(e >> 5) * (size_t)n + (size_t)k) * LTL_GROUP + (size_t)(e & 31);

@@ -788,7 +788,7 @@ static void push_piece(ltl_core* h, std::vector<Piece>& pieces, i64& total, i64&
         lane_hi = j1;
         rows = i1 - i0;
     }
-    if (kind != PIECE_UNARY && h->W == 1 && h->variant == VAR_MUELLER) p.ti = 4;
+    if (kind != PIECE_UNARY && h->W == 1 && (h->variant == VAR_MUELLER || h->variant == VAR_NH)) p.ti = 4;
     p.lane_g0 = lane_lo >> 5;
     p.tiles_lane = ((lane_hi - 1) >> 5) - p.lane_g0 + 1;
     const i64 row_tiles = (rows + p.ti - 1) / p.ti;
@@ -797,7 +797,7 @@ static void push_piece(ltl_core* h, std::vector<Piece>& pieces, i64& total, i64&
     p.tile_base = tiles;
     total += p.count;
     // fuse with an earlier unary piece over the same operand range (same chunk): it evaluates this connective too
-    if (kind == PIECE_UNARY && h->W == 1 && h->variant == VAR_MUELLER && h->fuse_unary && p.op != OP_IDENT) {
+    if (kind == PIECE_UNARY && h->W == 1 && (h->variant == VAR_MUELLER || h->variant == VAR_NH) && h->fuse_unary && p.op != OP_IDENT) {
         for (auto& q : pieces) {
             if (q.kind != PIECE_UNARY || q.i0 != i0 || q.i1 != i1 || q.nfuse == 0 || q.nfuse >= 4) continue;
             if (((q.fops >> (4 * (q.nfuse - 1))) & 15) >= p.op) continue;  // keep nibbles in ascending opcode order
@@ -946,7 +946,8 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
         CK(cudaMemsetAsync(h->d_acc_s1, 0, (size_t)total * 8, h->stream));
         CK(cudaMemsetAsync(h->d_acc_err, 0, (size_t)total * 4, h->stream));
     }
-    const bool mueller = h->variant == VAR_MUELLER;
+    const bool mueller = h->variant == VAR_MUELLER || h->variant == VAR_NH;  // hashed variants: two 64-bit sums
+    const int screen_kind = h->variant == VAR_MUELLER ? KIND_MUELLER : h->variant == VAR_NH ? KIND_NH : KIND_BITS;
     // Phase A goes out in launches of sub_tiles warp tiles, in enumeration order, with no host wait in
     // between (two in flight); after each one the solver rank is copied to pinned memory, and once a solver is
     // known no launch is issued whose first tile lies above it.
@@ -977,7 +978,7 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
             dim3 grid((unsigned)(((t1 - t0) * p.nsplit + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), 1);
             ScreenParams q = p;
             q.total_tiles = t1;
-            SCREEN_FN[h->W](q, mueller ? KIND_MUELLER : KIND_BITS, grid, h->stream);
+            SCREEN_FN[h->W](q, screen_kind, grid, h->stream);
             if (per < tiles) {
                 CK(cudaMemcpyAsync(h->h_solver + (k & 1), &h->d_ctl->solver_c, sizeof(u64), cudaMemcpyDeviceToHost, h->stream));
                 CK(cudaEventRecord(h->sub_ev[k & 1], h->stream));
@@ -1407,7 +1408,7 @@ int ltl_core_create(const uint64_t* masks, int R, int W, int n_pos, int err_max,
     if (!masks || R < 1) return bad("need at least one row");
     if (W < 1 || W > LTL_MAX_W) return bad("words per row must lie in [1, 16]");
     if (n_pos < 0 || n_pos > R) return bad("n_pos outside [0, R]");
-    if (variant < 0 || variant > 2) return bad("unknown fingerprint variant");
+    if (variant < 0 || variant > VAR_NH) return bad("unknown fingerprint variant");
     if (n_proj < 0 || n_proj > 126) return bad("projection wider than the fingerprint");  // reference _speedups.pyx:92-93
     if (mask_k < 0 || mask_k > 126) return bad("mask_k outside [0, 126]");
     if ((int64_t)R * W > (int64_t)1 << 31) return bad("matrix too large");

@@ -76,7 +76,7 @@ __device__ __forceinline__ u64 mix64_hot(u64 x) {
 // ------------------------------------------------------------------------------------------------
 // fingerprint finalisation + table filing for one candidate
 
-template <bool MUELLER>
+template <bool MUELLER>  // true for both hashed variants (Mueller, NH): the two sums are finalised the same way
 __device__ __forceinline__ void finish_candidate(const ScreenParams& p, u64 c, u64 s0, u64 s1, u32 err) {
     u64 hi, lo;
     if (MUELLER) {  // reference _speedups.pyx:203-204
@@ -208,6 +208,8 @@ template <int W, int KIND, int OP, int TI, bool XL>
 __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc, const i64 row0, const i64 lg,
                                           const int split, const int lane, u64* __restrict__ sbuf, u64* bars) {
     constexpr bool MUELLER = KIND == KIND_MUELLER;
+    constexpr bool NH = KIND == KIND_NH;
+    constexpr bool HASHED = MUELLER || NH;
     constexpr bool REWRITE = KIND == KIND_REWRITE;
     constexpr bool FUSED = OP >= 16;
     constexpr bool BIN = !op_unary_c(slot_op<OP>(0));
@@ -264,8 +266,8 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
 #pragma unroll
     for (int t = 0; t < TI; t++) {
         s0[t] = s1[t] = 0;
-        h0[t] = K_SEED0;
-        h1[t] = K_SEED1;
+        h0[t] = NH ? 0ull : K_SEED0;  // NH: the block's two accumulators d_0, d_1
+        h1[t] = NH ? 0ull : K_SEED1;
         ones[t] = ones_pos[t] = 0;
     }
     u64 tw = ((u64)r0 * W + 1ull) * K_STEP;  // (k + 1) * STEP for the next word k
@@ -281,9 +283,17 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
         d = lo_;
     }
 
-    auto fold = [&](const bool first) {  // blocked Mueller: block 0 enters as is (== reference for n <= 64)
+    auto fold = [&](const u32 blk) {  // blocked Mueller: block 0 enters as is (== reference for n <= 64)
+        const bool first = blk == 0;
 #pragma unroll
         for (int t = 0; t < TI; t++) {
+            if (NH) {  // oracle fp_nh: s0 += mix64(d0 ^ u), s1 += mix64(d1 + u), u = (block + 1) * STEP
+                const u64 u = (u64)(blk + 1) * K_STEP;
+                s0[t] += mix64(h0[t] ^ u);
+                s1[t] += mix64(h1[t] + u);
+                h0[t] = h1[t] = 0;
+                continue;
+            }
             if (first) {
                 s0[t] += h0[t];
                 s1[t] += h1[t];
@@ -309,6 +319,17 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
         const size_t kb = (size_t)r * W;
 #pragma unroll
         for (int w = 0; w < W; w++) a[w] = src[w * 32];
+        // NH keys of this row's words (warp-uniform constant loads): word k uses KEY[k mod 64] and KEY[k mod 64 + 1]
+        u64 key0[W], key1[W];
+        if (NH) {
+#pragma unroll
+            for (int w = 0; w < W; w++) {
+                // when hash blocks end on stage boundaries no row straddles a block: one base + constant offsets
+                const u32 pk = Ring<W>::CHUNK_FOLD ? (((u32)kb & 63u) + w) : (((u32)kb + w) & 63u);
+                key0[w] = c_nh.k[pk];
+                key1[w] = c_nh.k[pk + 1];
+            }
+        }
 #pragma unroll
         for (int w = 0; w < W; w++) m[w] = NEEDM ? ld_nc(p.masks + kb + w) : 0ull;
 #pragma unroll
@@ -327,7 +348,23 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
                 continue;
             }
             asm("mad.hi.u32 %0, %1, 2, %0;" : "+r"(ones[t]) : "r"((u32)(out[0] >> 32)));
-            if (MUELLER) {
+            if (NH) {
+#pragma unroll
+                for (int w = 0; w < W; w++) {  // oracle fp_nh
+                    const u32 xl = (u32)out[w], xh = (u32)(out[w] >> 32);
+                    h0[t] += (u64)(xl + (u32)key0[w]) * (u64)(xh + (u32)(key0[w] >> 32));
+                    h1[t] += (u64)(xl + (u32)key1[w]) * (u64)(xh + (u32)(key1[w] >> 32));
+                    if (!Ring<W>::CHUNK_FOLD) {
+                        const u64 k1 = kb + w + 1;
+                        if ((k1 & 63) == 0 || k1 == (u64)n) {
+                            const u64 u = (((k1 - 1) >> 6) + 1) * K_STEP;
+                            s0[t] += mix64(h0[t] ^ u);
+                            s1[t] += mix64(h1[t] + u);
+                            h0[t] = h1[t] = 0;
+                        }
+                    }
+                }
+            } else if (MUELLER) {
 #pragma unroll
                 for (int w = 0; w < W; w++) {  // reference _speedups.pyx:196-202
                     u64 mm = mix64_hot(out[w] ^ (tw + (u64)w * K_STEP));
@@ -367,7 +404,7 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
                 if (t == TI - 1) d = dd;
             }
         }
-        tw += (u64)W * K_STEP;
+        if (MUELLER) tw += (u64)W * K_STEP;
     };
 
     // ---- stream the lane operand through the shared-memory ring
@@ -424,9 +461,9 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
                 do_row(rbase + rr, src + rr * W * 32, xsrc + rr * W);
             }
         }
-        if (MUELLER && RG::CHUNK_FOLD) {
+        if (HASHED && RG::CHUNK_FOLD) {
             const int rend = rbase + rows_c;
-            if ((((u32)rend * W) & 63u) == 0 || rend == p.R) fold((((u32)rend * W - 1) >> 6) == 0);
+            if ((((u32)rend * W) & 63u) == 0 || rend == p.R) fold(((u32)rend * W - 1) >> 6);
         }
         __syncwarp();
         if (c + RG::STAGES < nchunks) {
@@ -459,7 +496,7 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
             atomicAdd(p.acc_s1 + c, s1[t]);
             if (err[t]) atomicAdd(p.acc_err + c, err[t]);
         } else {
-            finish_candidate<MUELLER>(p, c, s0[t], s1[t], err[t]);
+            finish_candidate<HASHED>(p, c, s0[t], s1[t], err[t]);
         }
     }
 }

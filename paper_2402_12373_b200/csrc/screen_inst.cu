@@ -12,11 +12,13 @@ extern "C" void LTL_CAT(ltl_launch_screen_w, LTL_W)(const ScreenParams& p, int k
     static bool configured = false;
     if (!configured) {  // > 48 KiB of dynamic shared memory needs an opt-in, once per process
         cudaFuncSetAttribute(k_screen<LTL_W, KIND_MUELLER>, cudaFuncAttributeMaxDynamicSharedMemorySize, Ring<LTL_W>::CTA_BYTES);
+        cudaFuncSetAttribute(k_screen<LTL_W, KIND_NH>, cudaFuncAttributeMaxDynamicSharedMemorySize, Ring<LTL_W>::CTA_BYTES);
         cudaFuncSetAttribute(k_screen<LTL_W, KIND_BITS>, cudaFuncAttributeMaxDynamicSharedMemorySize, Ring<LTL_W>::CTA_BYTES);
         cudaFuncSetAttribute(k_screen<LTL_W, KIND_REWRITE>, cudaFuncAttributeMaxDynamicSharedMemorySize, Ring<LTL_W>::CTA_BYTES);
         configured = true;
     }
     if (kind == KIND_MUELLER) k_screen<LTL_W, KIND_MUELLER><<<grid, LTL_CTA, Ring<LTL_W>::CTA_BYTES, stream>>>(p);
+    else if (kind == KIND_NH) k_screen<LTL_W, KIND_NH><<<grid, LTL_CTA, Ring<LTL_W>::CTA_BYTES, stream>>>(p);
     else if (kind == KIND_BITS) k_screen<LTL_W, KIND_BITS><<<grid, LTL_CTA, Ring<LTL_W>::CTA_BYTES, stream>>>(p);
     else k_screen<LTL_W, KIND_REWRITE><<<grid, LTL_CTA, Ring<LTL_W>::CTA_BYTES, stream>>>(p);
 }

@@ -253,7 +253,7 @@ class Enumeration:
                     self.outcome = Solved(Not(Atom(p)), atom_c + h.of(OP_NOT), stats)
                     return
 
-        rs = resolve_scheme(cfg.hash, ctx.lengths, SuffixTable.from_spec(spec, limit=126))
+        rs = resolve_scheme(cfg.hash, ctx.lengths, SuffixTable.from_spec(spec, limit=126), words_per_row=ctx.words)
         stats.precise = rs.precise
         if core_factory is None:
             from .core import make_core as core_factory  # CUDA core; raises BackendUnavailable

@@ -3,22 +3,30 @@
 Exact bit gathering ("precise mode") is used whenever the specification has at most 126 distinct
 non-empty suffixes; otherwise the configured hash (MuellerHash by default, or the deliberately
 weak first-k-positions scheme).  All variants then zero the lowest ``mask_bits`` bits.
+
+Beyond the reference's domain (a characteristic matrix of more than 64 words: the reference refuses such
+inputs, `enumerator.py:70-73`) the reference defines no hash.  There ``"mueller"`` resolves to this build's
+NH fingerprint (`V_NH`; definition `oracle/ltl_oracle.c` fp_nh): two multiply-adds per word instead of
+MuellerHash's four 64-bit multiplies, which is what bounds the screening kernel.  ``"mueller_blocked"``
+keeps the blocked MuellerHash extension at every size, ``"nh"`` forces NH at every size (tests, A/B runs).
+Inside the reference's domain ``"mueller"`` is the reference's MuellerHash bit for bit.
 """
 from __future__ import annotations
 
 from dataclasses import dataclass
 
 FP_BITS = 126
-V_GATHER, V_MUELLER, V_FKP = 0, 1, 2
+V_GATHER, V_MUELLER, V_FKP, V_NH = 0, 1, 2, 3
+REFERENCE_WORDS = 64  # the reference's largest matrix: 64 rows x one word
 
 
 @dataclass(frozen=True)
 class HashScheme:
-    variant: str = "mueller"  # "mueller" | "fkp"
+    variant: str = "mueller"  # "mueller" | "fkp" | "mueller_blocked" | "nh"
     mask_bits: int = 0
 
     def __post_init__(self):
-        if self.variant not in ("mueller", "fkp"):
+        if self.variant not in ("mueller", "fkp", "mueller_blocked", "nh"):
             raise ValueError(f"unknown hash variant {self.variant!r}")
         if not 0 <= self.mask_bits <= FP_BITS:
             raise ValueError("mask_bits must lie in [0, 126]")
@@ -45,7 +53,7 @@ def fkp_bits_per_row(n_rows: int) -> int:
     return min(lo, 64)
 
 
-def resolve_scheme(scheme: HashScheme, lengths, suffix_table=None) -> ResolvedScheme:
+def resolve_scheme(scheme: HashScheme, lengths, suffix_table=None, words_per_row: int = 1) -> ResolvedScheme:
     if suffix_table is not None:
         if suffix_table.count <= FP_BITS:
             return ResolvedScheme(V_GATHER, tuple(suffix_table.rows), tuple(suffix_table.offsets), mask_k=scheme.mask_bits)
@@ -53,6 +61,8 @@ def resolve_scheme(scheme: HashScheme, lengths, suffix_table=None) -> ResolvedSc
         rows = tuple(r for r, n in enumerate(lengths) for _ in range(int(n)))
         offs = tuple(j for n in lengths for j in range(int(n)))
         return ResolvedScheme(V_GATHER, rows, offs, mask_k=scheme.mask_bits)
-    if scheme.variant == "mueller":
-        return ResolvedScheme(V_MUELLER, mask_k=scheme.mask_bits)
+    if scheme.variant in ("mueller", "mueller_blocked", "nh"):
+        big = len(lengths) * int(words_per_row) > REFERENCE_WORDS
+        nh = scheme.variant == "nh" or (scheme.variant == "mueller" and big)
+        return ResolvedScheme(V_NH if nh else V_MUELLER, mask_k=scheme.mask_bits)
     return ResolvedScheme(V_FKP, fkp_bits=fkp_bits_per_row(len(lengths)), mask_k=scheme.mask_bits)

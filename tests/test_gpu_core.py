@@ -7,7 +7,7 @@ from helpers import (cfg_from_golden, golden, oracle_factory, random_spec, recor
                      unhex)
 from oracle import cpu_oracle
 from paper_2402_12373_b200 import learner as L
-from paper_2402_12373_b200.core import CudaCore, V_FKP, V_GATHER, V_MUELLER
+from paper_2402_12373_b200.core import CudaCore, V_FKP, V_GATHER, V_MUELLER, V_NH
 from paper_2402_12373_b200.errors import CoreOOM
 from paper_2402_12373_b200.formula import print_formula
 from paper_2402_12373_b200.packing import length_masks
@@ -64,11 +64,12 @@ def drive(cuda, ora, rng, n_seed=5, rounds=2):
 
 @pytest.mark.parametrize("R,W", [(2, 1), (16, 1), (64, 1), (65, 1), (200, 1), (1024, 1), (7, 2), (33, 3), (20, 4),
                                  (9, 5), (12, 7), (40, 8), (5, 11), (24, 16), (130, 16)])
-def test_differential_random(R, W):
+@pytest.mark.parametrize("variant", [V_MUELLER, V_NH], ids=["mueller", "nh"])
+def test_differential_random(R, W, variant):
     rng = np.random.default_rng(1000 * R + W)
     masks = random_masks(rng, R, W)
     n_pos = int(rng.integers(1, R)) if R > 1 else 1
-    cuda, ora = make_pair(masks, n_pos, err_max=-1, W=W)  # err_max -1: nothing ever solves
+    cuda, ora = make_pair(masks, n_pos, err_max=-1, variant=variant, W=W)  # err_max -1: nothing ever solves
     drive.masks = masks
     drive(cuda, ora, rng, n_seed=4, rounds=2 if R * W <= 2048 else 1)
     assert_same_state(cuda, ora)
@@ -84,11 +85,12 @@ def test_differential_random(R, W):
 
 @pytest.mark.parametrize("R,W,split,chunk", [(200, 1, 3, 97), (1024, 1, 16, 1000), (130, 16, 2, 333), (64, 3, 1, 50),
                                              (300, 2, 4, 1 << 20)])
-def test_differential_split_and_chunked(R, W, split, chunk):
+@pytest.mark.parametrize("variant", [V_MUELLER, V_NH], ids=["mueller", "nh"])
+def test_differential_split_and_chunked(R, W, split, chunk, variant):
     """Row-split evaluation (partial fingerprints combined by atomics) and tiny chunks (rows cut mid-way)."""
     rng = np.random.default_rng(77 * R + W)
     masks = random_masks(rng, R, W)
-    cuda, ora = make_pair(masks, R // 2, err_max=-1, W=W, chunk_candidates=chunk)
+    cuda, ora = make_pair(masks, R // 2, err_max=-1, variant=variant, W=W, chunk_candidates=chunk)
     cuda.set_option("force_split", split)
     drive.masks = masks
     drive(cuda, ora, rng, n_seed=4, rounds=1)
@@ -263,12 +265,13 @@ def test_learn_matches_oracle_beyond_reference_limits(n_props, n_pos, n_neg, len
         c._real_close()
 
 
-def test_many_rows_row_split():
+@pytest.mark.parametrize("variant", [V_MUELLER, V_NH], ids=["mueller", "nh"])
+def test_many_rows_row_split(variant):
     """BASELINE config 4 shape, scaled: many short traces => row-split evaluation with combined fingerprints."""
     rng = np.random.default_rng(4)
     R = 1 << 14
     masks = random_masks(rng, R, 1)
-    cuda, ora = make_pair(masks, R // 2, err_max=-1, budget=4 << 30)
+    cuda, ora = make_pair(masks, R // 2, err_max=-1, variant=variant, budget=4 << 30)
     drive.masks = masks
     for k in range(4):
         cm = random_cm(rng, masks)
@@ -385,7 +388,7 @@ def test_both_phase_b_forms_match_oracle(tiled, R, W):
 
     rng = np.random.default_rng(R + W + tiled)
     masks = random_masks(rng, R, W)
-    cuda, ora = make_pair(masks, R // 2, err_max=-1, W=W)
+    cuda, ora = make_pair(masks, R // 2, err_max=-1, variant=V_NH if tiled else V_MUELLER, W=W)
     cuda.set_option("tiled_materialize", tiled)
     drive.masks = masks
     for k in range(5):

@@ -120,3 +120,62 @@ def _check_learn(case, threads):
         assert core.n_entries == g["n_entries"]
         assert sha(core.export_cms()) == g["cms_sha"]
         assert sha(records_array(core)) == g["records_sha"]
+
+
+# ---- NH fingerprint (this build's hash beyond the reference's domain; no reference counterpart)
+
+_M = (1 << 64) - 1
+
+
+def _mix64(x):
+    x ^= x >> 30
+    x = x * 0xBF58476D1CE4E5B9 & _M
+    x ^= x >> 27
+    x = x * 0x94D049BB133111EB & _M
+    return x ^ (x >> 31)
+
+
+def _nh_python(cm):
+    """Independent restatement of oracle/ltl_oracle.c fp_nh on Python ints."""
+    step, seed0 = 0x9E3779B97F4A7C15, 0x243F6A8885A308D3
+    key = [_mix64(((j + 1) * step + seed0) & _M) for j in range(65)]
+    s0 = s1 = d0 = d1 = 0
+    for k, x in enumerate(int(v) for v in cm):
+        p, xl, xh = k & 63, x & 0xFFFFFFFF, x >> 32
+        d0 = (d0 + ((xl + (key[p] & 0xFFFFFFFF)) & 0xFFFFFFFF) * ((xh + (key[p] >> 32)) & 0xFFFFFFFF)) & _M
+        d1 = (d1 + ((xl + (key[p + 1] & 0xFFFFFFFF)) & 0xFFFFFFFF) * ((xh + (key[p + 1] >> 32)) & 0xFFFFFFFF)) & _M
+        if p == 63 or k + 1 == len(cm):
+            u = ((k >> 6) + 1) * step & _M
+            s0 = (s0 + _mix64(d0 ^ u)) & _M
+            s1 = (s1 + _mix64((d1 + u) & _M)) & _M
+            d0 = d1 = 0
+    return ((_mix64(s0) & ((1 << 62) - 1)) << 64) | _mix64(s1)
+
+
+def test_nh_fingerprint_known_answers_and_restatement():
+    assert _nh_python(np.zeros(1, dtype=np.uint64)) == 0x347E3C3F0D6351A09671A12CA210CF9D
+    assert _nh_python(np.arange(100, dtype=np.uint64)) == 0x1922593D4DD0549A2DB84339420886A9
+    rng = np.random.default_rng(0)
+    for R, W in [(1, 1), (3, 1), (64, 1), (65, 1), (200, 3), (1024, 1), (33, 16)]:
+        core = cpu_oracle.OracleCore(np.full(R * W, 2**64 - 1, dtype=np.uint64), 1, 0, cpu_oracle.V_NH, words_per_row=W)
+        for _ in range(3):
+            cm = rng.integers(0, 1 << 63, size=R * W, dtype=np.uint64) * np.uint64(2) + rng.integers(0, 2, size=R * W, dtype=np.uint64)
+            assert core.fingerprint_of(cm) == _nh_python(cm)
+            # position dependence: swapping two different words changes the value
+            sw = cm.copy()
+            if R * W > 1 and sw[0] != sw[-1]:
+                sw[0], sw[-1] = cm[-1], cm[0]
+                assert core.fingerprint_of(sw) != core.fingerprint_of(cm)
+
+
+def test_scheme_selects_nh_only_beyond_the_reference_domain():
+    from paper_2402_12373_b200 import scheme as S
+
+    long_rows = [63] * 64
+    assert S.resolve_scheme(S.HashScheme(), long_rows).variant == S.V_MUELLER          # 64 words: the reference's hash
+    assert S.resolve_scheme(S.HashScheme(), [63] * 65).variant == S.V_NH               # 65 words: outside its domain
+    assert S.resolve_scheme(S.HashScheme(), long_rows, words_per_row=2).variant == S.V_NH
+    assert S.resolve_scheme(S.HashScheme("mueller_blocked"), [63] * 65).variant == S.V_MUELLER
+    assert S.resolve_scheme(S.HashScheme("nh"), long_rows).variant == S.V_NH
+    assert S.resolve_scheme(S.HashScheme("fkp"), [63] * 65).variant == S.V_FKP
+    assert S.resolve_scheme(S.HashScheme(), [5] * 8).variant == S.V_GATHER              # precise mode is unaffected
