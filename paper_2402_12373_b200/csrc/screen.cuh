@@ -73,6 +73,13 @@ __device__ __forceinline__ u64 mix64_hot(u64 x) {
 #endif
 }
 
+// a * b + c with a 64-bit accumulator: exactly one IMAD.WIDE.U32 (the C form made ptxas split the add)
+__device__ __forceinline__ u64 mad_wide(u32 a, u32 b, u64 c) {
+    u64 d;
+    asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(d) : "r"(a), "r"(b), "l"(c));
+    return d;
+}
+
 // ------------------------------------------------------------------------------------------------
 // fingerprint finalisation + table filing for one candidate
 
@@ -352,8 +359,8 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
 #pragma unroll
                 for (int w = 0; w < W; w++) {  // oracle fp_nh
                     const u32 xl = (u32)out[w], xh = (u32)(out[w] >> 32);
-                    h0[t] += (u64)(xl + (u32)key0[w]) * (u64)(xh + (u32)(key0[w] >> 32));
-                    h1[t] += (u64)(xl + (u32)key1[w]) * (u64)(xh + (u32)(key1[w] >> 32));
+                    h0[t] = mad_wide(xl + (u32)key0[w], xh + (u32)(key0[w] >> 32), h0[t]);
+                    h1[t] = mad_wide(xl + (u32)key1[w], xh + (u32)(key1[w] >> 32), h1[t]);
                     if (!Ring<W>::CHUNK_FOLD) {
                         const u64 k1 = kb + w + 1;
                         if ((k1 & 63) == 0 || k1 == (u64)n) {

@@ -1,21 +1,33 @@
-import sys, time
+"""Where does learn() spend host time?  cProfile of one warm end-to-end call on the bench workload."""
+import cProfile
+import pstats
+import sys
+import time
+
 sys.path.insert(0, '/root/repo')
-import numpy as np, torch
-from paper_2402_12373_b200 import workloads as Wl
-from paper_2402_12373_b200.learner import learn
-from paper_2402_12373_b200.traces import Specification
-spec, al, f, cfg = Wl.make_config("c2_planted")
+import torch  # noqa: E402
+from paper_2402_12373_b200 import workloads as Wl  # noqa: E402
+from paper_2402_12373_b200.learner import learn  # noqa: E402
+from paper_2402_12373_b200.traces import Specification  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "c2_planted"
+spec, al, f, cfg = Wl.make_config(name)
 pc, pl = spec.chars[:spec.n_pos].copy(), spec.lengths[:spec.n_pos].copy()
 nc, nl = spec.chars[spec.n_pos:].copy(), spec.lengths[spec.n_pos:].copy()
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-for rep in range(6):
+for rep in range(5):
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     s = Specification.from_arrays(pc, pl, nc, nl)
     t1 = time.perf_counter()
-    r = learn(s, None, al, max_cost=12, budget_bytes=150 << 30)
+    r = learn(s, None, al, max_cost=cfg["max_cost"], budget_bytes=150 << 30)
     t2 = time.perf_counter()
     flush.fill_(1)
     torch.cuda.synchronize()
     t3 = time.perf_counter()
     print(f"spec {1e3*(t1-t0):.2f}  learn {1e3*(t2-t1):.2f}  (search {1e3*r.stats.search_seconds:.2f})  flush {1e3*(t3-t2):.2f}")
+pr = cProfile.Profile()
+pr.enable()
+r = learn(s, None, al, max_cost=cfg["max_cost"], budget_bytes=150 << 30)
+pr.disable()
+pstats.Stats(pr).sort_stats("cumulative").print_stats(30)
