@@ -2,11 +2,13 @@
 
     python -m paper_2402_12373_b200.cli learn TRACE_FILE [--max-cost N] [--hash mueller|fkp|mueller_blocked|nh] [--mask-bits K]
         [--nnf] [--no-until] [--noise EPS] [--budget BYTES] [--costs a,n,c,d,x,f,g,u] [--timeout SECS]
-        [--device D] [--json PATH] [--verify]
+        [--device D] [--json PATH] [--verify] [--dnc --window N --strategy det|rand --seed S --min-window M]
 
 Reads a trace file (format `traces.py`, reference `traces.py:180-253`), runs the enumerative learner on the
 B200 core and writes the JSON report of `SPEC.md:158`: {formula, cost, wall_ms, mode, hash, stats}.  Only the
-`learn` subcommand is in scope (component 13); D&C (`--window`, `--strategy`) is not built.
+`learn` subcommand is in scope (component 13).  With `--dnc` the specification is learned by divide
+and conquer (`dnc.py`, reference `dnc.py:205-224`); without it by one enumeration (the reference needs D&C above
+64 traces, this core does not).
 """
 from __future__ import annotations
 
@@ -33,6 +35,8 @@ def cmd_learn(args) -> int:
     report = {"input": args.trace_file, "n_pos": spec.n_pos, "n_neg": spec.n_neg, "max_len": spec.max_len,
               "config": {"max_cost": args.max_cost, "hash": args.hash, "mask_bits": args.mask_bits, "nnf": args.nnf,
                          "no_until": args.no_until, "noise": args.noise, "budget": args.budget, "costs": costs}}
+    if args.dnc:
+        return _learn_dnc(args, spec, alphabet, costs, report, t0)
     try:
         res = learn(spec, None, alphabet, max_cost=args.max_cost, costs=costs, require_nnf=args.nnf,
                     forbid_until=args.no_until, noise=args.noise,
@@ -64,6 +68,49 @@ def cmd_learn(args) -> int:
     return rc
 
 
+def _learn_dnc(args, spec, alphabet, costs, report, t0) -> int:
+    """--dnc: divide and conquer (reference `dnc.py`) with every leaf on the device."""
+    from . import dnc
+    from .formula import CostHomomorphism, UNIFORM, cost as formula_cost, overfit_cost
+    from .learner import LearnerConfig
+
+    h = UNIFORM if costs is None else CostHomomorphism(tuple(costs))
+    cfg = LearnerConfig(cost=h, require_nnf=args.nnf, forbid_until=args.no_until, noise=args.noise,
+                        hash=HashScheme(args.hash, args.mask_bits), device=args.device,
+                        ceiling=None if args.max_cost is None else args.max_cost + 1,
+                        deadline=None if args.timeout is None else time.monotonic() + args.timeout,
+                        **({} if args.budget is None else {"budget_bytes": args.budget}))
+    split = dnc.SplitConfig(args.strategy, args.window, min(args.min_window, args.window), args.seed)
+    report["config"].update(dnc=True, window=args.window, strategy=args.strategy, seed=args.seed)
+    try:
+        res = dnc.dnc_learn(spec, alphabet, cfg, split)
+    except BackendUnavailable as exc:
+        print(f"error: {exc}", file=sys.stderr)
+        return 3
+    except TimeoutExceeded:
+        report.update(status="timeout", wall_ms=round(1e3 * (time.perf_counter() - t0), 3))
+        _emit(report, args)
+        return 4
+    except dnc.WindowExhausted as exc:
+        report.update(status="oom", error=str(exc), wall_ms=round(1e3 * (time.perf_counter() - t0), 3))
+        _emit(report, args)
+        return 1
+    c, oc = formula_cost(res.formula, h), overfit_cost(spec, alphabet, h)
+    report.update(status="solved", formula=print_formula(res.formula, alphabet), cost=c, overfit_cost=oc,
+                  ratio=c / max(oc, 1), wall_ms=round(1e3 * (time.perf_counter() - t0), 3), hash=args.hash,
+                  dnc={"nodes": res.nodes, "enum_calls": res.enum_calls})
+    rc = 0
+    if args.verify:
+        reparsed = parse_formula(report["formula"], alphabet)
+        ok = dnc.separates(reparsed, spec, alphabet)
+        report["verified"] = ok
+        if not ok and args.noise == 0.0:
+            print("error: the recombined formula does not separate the input", file=sys.stderr)
+            rc = 5
+    _emit(report, args)
+    return rc
+
+
 def _emit(report, args):
     text = json.dumps(report, sort_keys=True)
     if args.json:
@@ -90,6 +137,11 @@ def main(argv=None) -> int:
     lp.add_argument("--device", type=int, default=0)
     lp.add_argument("--json", default=None, help="write the report here instead of stdout")
     lp.add_argument("--verify", action="store_true", help="re-evaluate the learned formula on the input")
+    lp.add_argument("--dnc", action="store_true", help="divide and conquer over windows of --window traces")
+    lp.add_argument("--window", type=int, default=64)
+    lp.add_argument("--min-window", type=int, default=4)
+    lp.add_argument("--strategy", choices=["det", "rand"], default="rand")
+    lp.add_argument("--seed", type=int, default=0)
     lp.set_defaults(fn=cmd_learn)
     args = ap.parse_args(argv)
     return args.fn(args)
