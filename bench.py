@@ -195,7 +195,8 @@ def main():
     budget = int(args.budget_gb * (1 << 30))
     from paper_2402_12373_b200.scheme import HashScheme
 
-    lcfg = LearnerConfig(ceiling=max_cost + 1, budget_bytes=budget, device=local_rank, hash=HashScheme(args.hash))
+    lcfg = LearnerConfig(ceiling=max_cost + 1, budget_bytes=budget, device=local_rank, hash=HashScheme(args.hash),
+                         pack_on_device=True)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
     def resident_search(profile: bool):

@@ -87,6 +87,14 @@ LTL_API int ltl_abi_version(void);
 /* Number of CUDA devices visible, or a negative LTL_ERR_* code. */
 LTL_API int ltl_device_count(void);
 
+/* Trace packing on the device -- replaces TraceContext.from_traces (reference bitsem.py:73-88; length masks
+ * bitsem.py:51-55), generalised to W words per row (position j -> word j/64, bit 63 - j%64).
+ * chars: R rows of L characters (uint16 proposition bitmasks, row-major; entries at positions >= lengths[r] are
+ * ignored), lengths: R trace lengths.  Writes masks_out[R*W] and atoms_out[n_props][R*W] (host buffers).
+ * 1 <= n_props <= 16, L <= 64*W.  No core handle is involved; errors via ltl_core_last_error(NULL). */
+LTL_API int ltl_pack_traces(const uint16_t* chars, const int64_t* lengths, int64_t R, int L, int n_props, int W, int device,
+                            uint64_t* masks_out, uint64_t* atoms_out);
+
 /* Constructor: reference _speedups.pyx:79-111 (Core.__cinit__) / kernels.py:140-172 (make_core).
  * masks: uint64[R*W] length masks.  proj_rows/proj_offs (n_proj <= 126 pairs): gather projection
  * (row, position).  fkp_bits: per-row prefix width of the fkp variant.  mask_k: low fingerprint bits

@@ -84,6 +84,8 @@ def load_library():
     L.ltl_core_host_times.argtypes = [vp, C.POINTER(C.c_double)]
     L.ltl_core_host_times.restype = C.c_int
     L.ltl_pool_trim.restype = C.c_uint64
+    L.ltl_pack_traces.argtypes = [C.POINTER(C.c_uint16), i64p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, u64p, u64p]
+    L.ltl_pack_traces.restype = C.c_int
     L.ltl_core_level_size.argtypes = [vp, C.POINTER(Segment), C.c_int, i64p]
     L.ltl_core_stage_eval.argtypes = [vp, C.POINTER(Segment), C.c_int, C.c_int64, C.c_int64, vp, i64p]
     L.ltl_core_stage_file.argtypes = [vp, vp, C.c_int64, vp, i64p]
@@ -115,6 +117,31 @@ def device_count() -> int:
 
 def _u64(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_uint64))
+
+
+def pack_traces(chars: np.ndarray, lengths: np.ndarray, n_props: int, words_per_row: int, device: int = 0):
+    """Pack a padded character matrix ``uint16[R, L]`` into length masks ``uint64[R, W]`` and per-proposition
+    characteristic sequences ``uint64[n_props, R, W]`` on the device (`k_pack`; replaces the reference's
+    `TraceContext.from_traces` triple loop, `bitsem.py:73-88`)."""
+    L = load_library()
+    if device_count() <= 0:
+        raise BackendUnavailable("no CUDA device visible (there is no CPU fallback)")
+    chars = np.ascontiguousarray(chars, dtype=np.uint16)
+    lengths = np.ascontiguousarray(lengths, dtype=np.int64)
+    R, width = chars.shape if chars.ndim == 2 else (len(lengths), 0)
+    W = int(words_per_row)
+    if width > 64 * W:
+        chars, width = np.ascontiguousarray(chars[:, : 64 * W]), 64 * W
+    masks = np.empty((R, W), dtype=np.uint64)
+    atoms = np.empty((int(n_props), R, W), dtype=np.uint64)
+    rc = L.ltl_pack_traces(chars.ctypes.data_as(C.POINTER(C.c_uint16)), lengths.ctypes.data_as(C.POINTER(C.c_int64)), R,
+                           int(width), int(n_props), W, int(device), _u64(masks), _u64(atoms))
+    if rc != 0:
+        msg = (L.ltl_core_last_error(None) or b"").decode()
+        if rc == ERR_ARG:
+            raise ValueError(msg)
+        raise CoreError(f"ltl_pack_traces failed ({rc}): {msg}")
+    return masks, atoms
 
 
 class CudaCore:

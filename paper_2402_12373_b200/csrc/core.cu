@@ -57,6 +57,46 @@ __global__ void k_finalize(const __grid_constant__ ScreenParams p, u64 total) {
     finish_candidate<MUELLER>(p, c, p.acc_s0[c], p.acc_s1[c], p.acc_err[c]);
 }
 
+// ------------------------------------------------------------------------------------------------
+// trace packing (reference bitsem.py:73-88, TraceContext.from_traces; layout rule N2)
+//
+// One thread per (row, word): 64 consecutive characters of the row (128 contiguous bytes, read as eight 16-byte
+// vectors) become one word of the length mask and one word of every proposition's characteristic sequence --
+// position j at bit 63 - j%64, positions >= length zero.  Outputs are row-major [R, W] per proposition.
+template <int NP>
+__global__ void __launch_bounds__(256) k_pack(const uint16_t* __restrict__ chars, const i64* __restrict__ lengths, i64 R, int L,
+                                             int Lpad, int W, int n_props, u64* __restrict__ masks, u64* __restrict__ atoms) {
+    const i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= R * W) return;
+    const i64 r = t / W;
+    const int w = (int)(t - r * W);
+    const i64 len64 = lengths[r];
+    const int len = len64 < (i64)L ? (int)len64 : L;
+    const int j0 = w * 64;
+    const int live = max(0, min(64, len - j0));
+    u64 acc[NP];
+#pragma unroll
+    for (int p = 0; p < NP; p++) acc[p] = 0;
+    const uint16_t* row = chars + (size_t)r * Lpad + j0;
+    for (int v = 0; v < 8 && v * 8 < live; v++) {
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(row) + v);  // Lpad is a multiple of 64: always in bounds
+        const u32 c[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int k = 0; k < 8; k++) {
+            const int j = v * 8 + k;
+            const u32 ch = (c[k >> 1] >> ((k & 1) * 16)) & 0xFFFFu;
+            if (j < live) {
+#pragma unroll
+                for (int p = 0; p < NP; p++)
+                    if (p < n_props) acc[p] |= (u64)((ch >> p) & 1u) << (63 - j);
+            }
+        }
+    }
+    masks[t] = live == 0 ? 0ull : (~0ull << ((64 - live) & 63));  // live = 64: shift by 0
+    for (int p = 0; p < NP; p++)
+        if (p < n_props) atoms[(size_t)p * (size_t)(R * W) + (size_t)t] = acc[p];
+}
+
 // winner flags (one bit per candidate) + winners per 1024-candidate block
 __global__ void __launch_bounds__(RES_CTA) k_resolve(const u32* __restrict__ slot, const Slot* __restrict__ table,
                                                      u64 gbase, u64 total, const Ctl* __restrict__ ctl,
@@ -1370,6 +1410,61 @@ static int build_deposits(ltl_core* h, const int32_t* proj_rows, const int32_t* 
 // C ABI
 
 extern "C" {
+
+int ltl_pack_traces(const uint16_t* chars, const int64_t* lengths, int64_t R, int L, int n_props, int W, int device,
+                    uint64_t* masks_out, uint64_t* atoms_out) {
+    g_create_error.clear();
+    auto bad = [&](const char* m) {
+        g_create_error = m;
+        return LTL_ERR_ARG;
+    };
+    if (R < 0 || L < 0 || W < 1 || W > LTL_MAX_W || n_props < 1 || n_props > 16) return bad("pack: bad shape");
+    if (L > 64 * W) return bad("pack: traces do not fit W words");
+    if (R == 0) return LTL_OK;
+    if (!chars || !lengths || !masks_out || !atoms_out) return bad("pack: null buffer");
+    auto cuda_fail = [&](cudaError_t e) {
+        g_create_error = std::string("pack: ") + cudaGetErrorString(e);
+        cudaGetLastError();
+        return LTL_ERR_CUDA;
+    };
+    cudaError_t e;
+    if ((e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail(e);
+    const int Lpad = 64 * W;  // device rows are padded to whole words so that the 16-byte loads stay in bounds
+    uint16_t* d_chars = nullptr;
+    i64* d_len = nullptr;
+    u64* d_out = nullptr;
+    const size_t words = (size_t)R * W;
+    int rc = LTL_OK;
+    cudaStream_t st = nullptr;
+    do {
+        if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess) { rc = cuda_fail(e); break; }
+        if ((e = cudaMalloc(&d_chars, (size_t)R * Lpad * 2)) != cudaSuccess) { rc = cuda_fail(e); break; }
+        if ((e = cudaMalloc(&d_len, (size_t)R * 8)) != cudaSuccess) { rc = cuda_fail(e); break; }
+        if ((e = cudaMalloc(&d_out, words * 8 * (size_t)(n_props + 1))) != cudaSuccess) { rc = cuda_fail(e); break; }
+        if (L == Lpad) {
+            e = cudaMemcpyAsync(d_chars, chars, (size_t)R * L * 2, cudaMemcpyHostToDevice, st);
+        } else {
+            if ((e = cudaMemsetAsync(d_chars, 0, (size_t)R * Lpad * 2, st)) != cudaSuccess) { rc = cuda_fail(e); break; }
+            e = L ? cudaMemcpy2DAsync(d_chars, (size_t)Lpad * 2, chars, (size_t)L * 2, (size_t)L * 2, (size_t)R, cudaMemcpyHostToDevice, st)
+                  : cudaSuccess;
+        }
+        if (e != cudaSuccess) { rc = cuda_fail(e); break; }
+        if ((e = cudaMemcpyAsync(d_len, lengths, (size_t)R * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) { rc = cuda_fail(e); break; }
+        const unsigned nb = (unsigned)((words + 255) / 256);
+        if (n_props <= 4) k_pack<4><<<nb, 256, 0, st>>>(d_chars, d_len, R, L, Lpad, W, n_props, d_out, d_out + words);
+        else if (n_props <= 8) k_pack<8><<<nb, 256, 0, st>>>(d_chars, d_len, R, L, Lpad, W, n_props, d_out, d_out + words);
+        else k_pack<16><<<nb, 256, 0, st>>>(d_chars, d_len, R, L, Lpad, W, n_props, d_out, d_out + words);
+        if ((e = cudaGetLastError()) != cudaSuccess) { rc = cuda_fail(e); break; }
+        if ((e = cudaMemcpyAsync(masks_out, d_out, words * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) { rc = cuda_fail(e); break; }
+        if ((e = cudaMemcpyAsync(atoms_out, d_out + words, words * 8 * (size_t)n_props, cudaMemcpyDeviceToHost, st)) != cudaSuccess) { rc = cuda_fail(e); break; }
+        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { rc = cuda_fail(e); break; }
+    } while (0);
+    cudaFree(d_chars);
+    cudaFree(d_len);
+    cudaFree(d_out);
+    if (st) cudaStreamDestroy(st);
+    return rc;
+}
 
 int ltl_abi_version(void) { return LTL_ABI_VERSION; }
 

@@ -80,6 +80,8 @@ class LearnerConfig:
     #: keep the characteristic matrices of the last cost level too.  They are never operands (the search
     #: ends there), so by default only their fingerprints and records are kept; results are identical.
     store_last_level: bool = False
+    #: pack the traces with the CUDA library's k_pack (None: yes unless a core factory is injected)
+    pack_on_device: Optional[bool] = None
 
     def __post_init__(self):
         if not 0.0 <= self.noise <= 1.0:
@@ -231,7 +233,10 @@ class Enumeration:
         cfg = cfg or LearnerConfig()
         _validate(spec, alphabet, cfg)
         self.spec, self.alphabet, self.cfg = spec, alphabet, cfg
-        self.ctx = ctx = TraceContext.from_spec(spec, alphabet)
+        # product path (no injected core): packing runs on the device too; an injected core factory (tests with
+        # the CPU oracle, the sharded wrapper) gets host-packed inputs
+        on_device = cfg.pack_on_device if cfg.pack_on_device is not None else core_factory is None
+        self.ctx = ctx = TraceContext.from_spec(spec, alphabet, device=cfg.device if on_device else None)
         n_pos, err_max, h = spec.n_pos, cfg.err_max(spec), cfg.cost
         self.stats = stats = EnumStats()
         stats.ceiling = overfit_cost(spec, alphabet, h)

@@ -5,8 +5,10 @@ per row): position j of a trace lives in word ``j // 64`` at bit ``63 - j % 64``
 left shift moves position j+k to position j); bits at positions >= the trace length are 0.  One
 characteristic matrix is ``uint64[R, W]`` with rows in specification order, positives first.
 
-The reference packs with a Python triple loop (`bitsem.py:79-87`); here the whole specification
-is packed with `np.packbits` over the padded character matrix, O(R*L*props) bit operations in C.
+The reference packs with a Python triple loop (`bitsem.py:79-87`).  On the product path
+(`TraceContext.from_spec(..., device=d)`, what `learn()` uses) the padded character matrix is packed by the
+`k_pack` kernel of the CUDA library (`core.pack_traces`); without a device argument (host tools, workload
+generators, tests that drive the learner with the CPU oracle) it is packed with `np.packbits`.  Same bits.
 """
 from __future__ import annotations
 
@@ -52,11 +54,16 @@ class TraceContext:
     words: int
 
     @staticmethod
-    def from_spec(spec, alphabet, words: int | None = None) -> "TraceContext":
+    def from_spec(spec, alphabet, words: int | None = None, device: int | None = None) -> "TraceContext":
         W = words_for_length(spec.max_len) if words is None else int(words)
         if spec.max_len > W * WORD:
             raise ValueError(f"trace of length {spec.max_len} does not fit {W} word(s)")
         R, n_props = spec.size, alphabet.size
+        if device is not None:
+            from .core import pack_traces
+
+            masks, atoms = pack_traces(spec.chars, spec.lengths, n_props, W, device)
+            return TraceContext(spec.lengths.copy(), masks, spec.n_pos, atoms, W)
         chars = np.zeros((R, W * WORD), dtype=np.uint16)
         chars[:, : spec.chars.shape[1]] = spec.chars[:, : W * WORD]
         live = np.arange(W * WORD)[None, :] < spec.lengths[:, None]

@@ -192,9 +192,8 @@ class Specification:
         closed-form overfit cost needs."""
         pc = self.chars[: self.n_pos]
         n_positions = int(self.lengths[: self.n_pos].sum())
-        hist = np.bincount(pc.reshape(-1), minlength=1 << 16)  # characters are 16-bit masks
-        popcount = np.array([bin(v).count("1") for v in np.nonzero(hist)[0]], dtype=np.int64)
-        return n_positions, int((hist[np.nonzero(hist)[0]] * popcount).sum())
+        # padding beyond each length is canonical zero, so the set bits of the whole matrix are the census
+        return n_positions, int(np.bitwise_count(pc).sum(dtype=np.int64))
 
     def __repr__(self):
         return f"Specification(|P|={self.n_pos}, |N|={self.n_neg}, max_len={self.max_len})"

@@ -409,3 +409,27 @@ def test_both_phase_b_forms_match_oracle(tiled, R, W):
             break
     assert_same_state(cuda, ora)
     cuda.close()
+
+
+@pytest.mark.parametrize("R,L,n_props,W", [(1, 1, 1, 1), (37, 5, 2, 1), (200, 64, 3, 1), (64, 63, 16, 1), (50, 100, 5, 2),
+                                           (33, 1024, 3, 16), (9, 700, 7, 11), (5000, 32, 4, 1), (20, 130, 9, 4)])
+def test_device_packing_matches_host_packing(R, L, n_props, W):
+    """k_pack (reference bitsem.py:73-88 on the device) against the np.packbits path, ragged lengths, empty rows."""
+    from paper_2402_12373_b200.core import pack_traces
+    from paper_2402_12373_b200.packing import TraceContext
+    from paper_2402_12373_b200.traces import Alphabet, Specification
+
+    rng = np.random.default_rng(R * 31 + L)
+    lengths = rng.integers(1, L + 1, size=R).astype(np.int64)
+    if R > 3:
+        lengths[-1] = 0  # an empty (negative) trace
+        lengths[0] = L
+    chars = rng.integers(0, 1 << n_props, size=(R, L)).astype(np.uint16)  # junk beyond the lengths must be ignored
+    masks, atoms = pack_traces(chars, lengths, n_props, W)
+    clean = chars.copy()
+    clean[np.arange(L)[None, :] >= lengths[:, None]] = 0
+    spec = Specification.__new__(Specification)
+    spec.chars, spec.lengths, spec.n_pos, spec.n_neg = clean, lengths, max(R - 1, 1), R - max(R - 1, 1)
+    want = TraceContext.from_spec(spec, Alphabet.default(n_props), words=W)
+    assert (masks == want.masks).all()
+    assert (atoms == want.atoms).all()
