@@ -262,17 +262,34 @@ def main():
     scr_bytes = sum(ks["screen"]["alg_bytes"] for ks in kstats)
     scr_launch = sum(ks["screen"]["launches"] for ks in kstats)
     achieved = scr_bytes / (scr_ms / 1e3) / 1e9 if scr_ms > 0 else 0.0
-    traffic = None
+    traffic = insts = None
     try:
         with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as fh:
-            traffic = json.load(fh).get("k_screen_dram_bytes_per_launch")
+            prof = json.load(fh)
+        traffic = prof.get("k_screen_dram_bytes_per_launch")
+        if args.config == "c2_planted" and args.hash in ("mueller", "nh") and max_cost == wl["max_cost"]:
+            insts = prof.get("k_screen_warp_instructions_per_step")  # deterministic for this workload (ncu count)
     except Exception:
         pass
     kernel_share = {k: round(sum(ks[k]["ms"] for ks in kstats), 3) for k in kstats[0]} if kstats else {}
     roofline = {"bound": "hbm", "kernel": "k_screen", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
                 "alg_bytes_per_launch": scr_bytes / max(scr_launch, 1), "ms_per_launch": scr_ms / max(scr_launch, 1),
-                "kernel_ms_by_class": kernel_share}
+                "kernel_ms_by_class": kernel_share,
+                "note": "algorithmic bytes = candidates x (arity x 8n + 16) (SURVEY 8d); operand lines are reused from "
+                        "shared memory / L1 across the 128 candidates of a warp tile, so DRAM traffic is a fraction of "
+                        "it and frac can exceed 1: the kernel is bound by integer issue, see `issue`"}
+    if traffic and scr_ms > 0:
+        dram = traffic * scr_launch / (scr_ms / 1e3) / 1e9
+        roofline["dram"] = {"achieved": dram, "unit": "GB/s", "frac": dram / peak,
+                            "source": "ncu dram__bytes_read+write per launch (profiles/roofline_traffic.json)"}
+    if insts and scr_ms > 0 and clocks.get("sm_mhz"):
+        sm_count = torch.cuda.get_device_properties(local_rank).multi_processor_count
+        ipeak = sm_count * 4 * clocks["sm_mhz"] * 1e6  # one warp instruction per cycle per SM sub-partition
+        iach = insts * args.steps / (scr_ms / 1e3)
+        roofline["issue"] = {"bound": "warp-instruction issue", "achieved": iach, "peak": ipeak, "unit": "warp-inst/s",
+                             "frac": iach / ipeak, "source": "ncu smsp__inst_executed.sum of one search "
+                                                             "(profiles/roofline_traffic.json) / CUDA-event kernel time"}
 
     # ---- end to end through the public API, host buffers in, formula out
     pos_c, pos_l = spec.chars[: spec.n_pos].copy(), spec.lengths[: spec.n_pos].copy()

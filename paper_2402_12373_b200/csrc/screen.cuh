@@ -511,8 +511,15 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
 // ------------------------------------------------------------------------------------------------
 // phase A kernel
 
+// Resident CTAs per SM asked of ptxas.  One-word rows keep every hot loop spill-free below 85 registers (checked in
+// the SASS), and with 16 warps per SM ncu showed `wait` (fixed-latency dependencies) as the top stall, so W = 1 runs
+// 3 CTAs = 24 warps per SM (bench: k_screen 16.4 -> 14.8 ms per search; 4 CTAs: 15.5 ms); wider rows hold whole
+// rows in registers and stay at 2.
+#ifndef LTL_MIN_CTAS_W1
+#define LTL_MIN_CTAS_W1 3
+#endif
 template <int W, int KIND>
-__global__ void __launch_bounds__(LTL_CTA, 2) k_screen(const __grid_constant__ ScreenParams p) {
+__global__ void __launch_bounds__(LTL_CTA, (W == 1 ? LTL_MIN_CTAS_W1 : 2)) k_screen(const __grid_constant__ ScreenParams p) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
