@@ -323,11 +323,13 @@ def main():
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    e2e_wall = []
+    e2e_wall, e2e_search, e2e_phase = [], [], []
     for _ in range(args.steps):
         tw = time.perf_counter()
         r = e2e_once()
         e2e_wall.append(round(1e3 * (time.perf_counter() - tw), 2))
+        e2e_search.append(round(1e3 * r.stats.search_seconds, 2))
+        e2e_phase.append({k: round(v, 2) for k, v in r.stats.phase_ms.items()})
         h2d, d2h = r.stats.h2d_bytes, r.stats.d2h_bytes
         flush.fill_(1)
     e1.record()
@@ -336,7 +338,8 @@ def main():
     e2e = {"value": offered_per_step * args.steps / (e2e_ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d,
            "d2h_bytes_per_step": d2h, "ms_per_step": e2e_ms / args.steps,
            "host_ms_per_step": {k: v / (args.steps + 1) for k, v in e2e_parts.items()},
-           "search_ms_last": 1e3 * r.stats.search_seconds, "host_ms_each_step": e2e_wall}
+           "search_ms_last": 1e3 * r.stats.search_seconds, "host_ms_each_step": e2e_wall,
+           "search_ms_each_step": e2e_search, "phase_ms_each_step": e2e_phase}
 
     # ---- CPU baseline on a bounded sample
     cpu = None

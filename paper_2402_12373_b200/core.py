@@ -29,7 +29,7 @@ ERR_ARG, ERR_CUDA, ERR_BUDGET, ERR_DEVICE_OOM = -1, -2, -3, -4
 KERNEL_CLASSES = ("screen", "finalize", "resolve", "scan", "emit", "materialize", "rehash", "purge", "misc")
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "csrc", "libltlcore.so")
+LIB_PATH = os.environ.get("LTL_CORE_LIB") or os.path.join(_HERE, "csrc", "libltlcore.so")  # override: A/B builds
 
 
 class Segment(C.Structure):
@@ -183,6 +183,9 @@ class CudaCore:
             self.set_option("chunk_candidates", chunk_candidates)
         if profile:
             self.set_option("profile", 1)
+        for kv in filter(None, os.environ.get("LTL_CORE_OPTIONS", "").split(",")):  # A/B switches: "name=value,..."
+            name, _, value = kv.partition("=")
+            self.set_option(name.strip(), int(value))
 
     # -- lifetime ----------------------------------------------------------------------
     def close(self):

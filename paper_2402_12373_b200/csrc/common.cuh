@@ -63,7 +63,9 @@ struct Piece {
     int swap;       // RECT only: lanes run over the left operand i, row tiles over j
     int ti;         // max rows per warp tile (1..4)
     int seg;        // index of the caller's segment this piece belongs to
-    int owns_tiles; // 0: a fused sibling, evaluated by the primary unary piece of its range
+    int owns_tiles; // 0: a fused sibling, evaluated by the primary unary piece of its range -- or (ext) by phase B
+    int ext;        // UNARY NOT over entries whose matrices are written in this very pass: k_materialize evaluates it
+    int pad_;
     i64 i0, i1;
     i64 j0, j1;
     i64 cbase;      // chunk-local rank of this piece's first candidate
@@ -140,6 +142,10 @@ struct MaterializeParams {
     const int* rec_lhs;
     const int* rec_rhs;
     int nsplit, rows_per_split;
+    // fused NOT (k_materialize<W, FK != 0>): while a new entry's rows are in registers, the candidate NOT(entry) of
+    // the NEXT cost level is evaluated too -- its chunk-local rank is not_cbase + (entry - not_i0)
+    int n_pos;
+    i64 not_cbase, not_i0;
 };
 
 __host__ __device__ __forceinline__ u64 mix64(u64 x) {  // reference kernels.py:50-57

@@ -26,9 +26,11 @@
 // ------------------------------------------------------------------------------------------------
 // per-W launchers (screen_inst.cu)
 
+#define LTL_MAX_DEVICES 64
+
 #define LTL_DECL_W(N)                                                                                  \
     extern "C" void ltl_launch_screen_w##N(const ScreenParams&, int, dim3, cudaStream_t);             \
-    extern "C" void ltl_launch_materialize_w##N(const MaterializeParams&, dim3, cudaStream_t);
+    extern "C" void ltl_launch_materialize_w##N(const MaterializeParams&, const ScreenParams&, int, dim3, cudaStream_t);
 LTL_DECL_W(1) LTL_DECL_W(2) LTL_DECL_W(3) LTL_DECL_W(4) LTL_DECL_W(5) LTL_DECL_W(6) LTL_DECL_W(7) LTL_DECL_W(8)
 LTL_DECL_W(9) LTL_DECL_W(10) LTL_DECL_W(11) LTL_DECL_W(12) LTL_DECL_W(13) LTL_DECL_W(14) LTL_DECL_W(15) LTL_DECL_W(16)
 #undef LTL_DECL_W
@@ -602,6 +604,7 @@ struct ltl_core : Arena {
     int sm_count = 148;
     int max_split = 4096, force_split = 0;
     bool fuse_unary = true;
+    bool fuse_not = true;  // phase B of a level also screens NOT(new entry) for the next level (k_materialize<W, FK>)
     int tiled_materialize = -1;  // phase B over phase A's tiles instead of per record: 1 always, 0 never, -1 by size
     bool device_oom = false;      // an S_OOM came from the device, not from the logical budget
     bool store_results = true;    // false: admitted entries get records and fingerprints but no matrix
@@ -699,7 +702,7 @@ static int ensure_table(ltl_core* h, u64 need_keys) {
     return LTL_OK;
 }
 
-static int flush_materialize(ltl_core* h);
+static int flush_materialize(ltl_core* h, const ScreenParams* sp = nullptr, int fuse_kind = 0, i64 not_cbase = 0, i64 not_i0 = 0);
 
 static int ensure_scratch(ltl_core* h, i64 total) {
     if (total <= h->scratch_cap) return LTL_OK;
@@ -797,7 +800,7 @@ static int ensure_records(ltl_core* h, u64 entries) {
 static inline bool is_binary(int op) { return op == OP_AND || op == OP_OR || op == OP_UNTIL; }
 
 static void push_piece(ltl_core* h, std::vector<Piece>& pieces, i64& total, i64& tiles, const Unit& u, i64 i0, i64 i1,
-                       i64 j0, i64 j1, int kind) {
+                       i64 j0, i64 j1, int kind, bool ext = false) {
     Piece p;
     memset(&p, 0, sizeof(p));
     p.op = u.op;
@@ -836,6 +839,12 @@ static void push_piece(ltl_core* h, std::vector<Piece>& pieces, i64& total, i64&
     p.cbase = total;
     p.tile_base = tiles;
     total += p.count;
+    if (ext) {  // evaluated by phase B of the entries it ranges over (fused NOT): ranks, but no tiles
+        p.ext = 1;
+        p.owns_tiles = 0;
+        pieces.push_back(p);
+        return;
+    }
     // fuse with an earlier unary piece over the same operand range (same chunk): it evaluates this connective too
     if (kind == PIECE_UNARY && h->W == 1 && (h->variant == VAR_MUELLER || h->variant == VAR_NH) && h->fuse_unary && p.op != OP_IDENT) {
         for (auto& q : pieces) {
@@ -928,12 +937,15 @@ static void choose_split(ltl_core* h, i64 tiles, int* nsplit, int* rows_per_spli
 static double screen_bytes(ltl_core* h, const std::vector<Piece>& pieces) {
     double b = 0;
     const double B = 8.0 * (double)h->n;
-    for (auto& p : pieces) b += (double)p.count * ((p.kind == PIECE_UNARY ? 1.0 : 2.0) * B + 16.0);
+    for (auto& p : pieces)
+        if (!p.ext) b += (double)p.count * ((p.kind == PIECE_UNARY ? 1.0 : 2.0) * B + 16.0);
     return b;
 }
 
+// fused_not >= 0: index of the piece (ext) whose candidates NOT(entry) are screened by phase B of the pending entries,
+// which this pass therefore issues itself, right before its own phase A launches
 static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 tiles, int mode, bool check_solve,
-                     bool materialize, ChunkOut* out) {
+                     bool materialize, ChunkOut* out, int fused_not = -1) {
     int rc;
     if (total <= 0) return LTL_OK;
     if (mode == MODE_INSERT) {
@@ -988,6 +1000,10 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     }
     const bool mueller = h->variant == VAR_MUELLER || h->variant == VAR_NH;  // hashed variants: two 64-bit sums
     const int screen_kind = h->variant == VAR_MUELLER ? KIND_MUELLER : h->variant == VAR_NH ? KIND_NH : KIND_BITS;
+    if (fused_not >= 0) {
+        const Piece& fp = pieces[(size_t)fused_not];
+        if ((rc = flush_materialize(h, &p, screen_kind, fp.cbase, fp.i0))) return rc;
+    }
     // Phase A goes out in launches of sub_tiles warp tiles, in enumeration order, with no host wait in
     // between (two in flight); after each one the solver rank is copied to pinned memory, and once a solver is
     // known no launch is issued whose first tile lies above it.
@@ -1125,8 +1141,9 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     return LTL_OK;
 }
 
-// Phase B for every admitted-but-unwritten range.
-static int flush_materialize(ltl_core* h) {
+// Phase B for every admitted-but-unwritten range.  With `sp` (the admission pass being issued) and fuse_kind != 0 it
+// also screens NOT(entry) for every entry it writes: candidate not_cbase + (entry - not_i0) of that pass.
+static int flush_materialize(ltl_core* h, const ScreenParams* sp, int fuse_kind, i64 not_cbase, i64 not_i0) {
     int rc;
     for (auto& pm : h->pending_mat) {
         const u64 n_base = pm.n_base, count = pm.count;
@@ -1177,9 +1194,20 @@ static int flush_materialize(ltl_core* h) {
         m.rec_rhs = (const int*)h->rec_rhs.base;
         const i64 groups = (i64)((n_base + count + 31) / 32 - n_base / 32);
         choose_split(h, groups, &m.nsplit, &m.rows_per_split);
-        ScopedTimer t(h, LTL_K_MATERIALIZE, count, bytes);
+        ScreenParams none;
+        memset(&none, 0, sizeof(none));
+        int fk = 0;
+        if (sp && fuse_kind) {  // every lane folds all rows of its entry: no row split
+            m.nsplit = 1;
+            m.rows_per_split = h->R;
+            m.n_pos = h->n_pos;
+            m.not_cbase = not_cbase;
+            m.not_i0 = not_i0;
+            fk = fuse_kind;
+        }
+        ScopedTimer t(h, LTL_K_MATERIALIZE, count, bytes + (fk ? (double)count * 16.0 : 0.0));
         dim3 grid((unsigned)((groups + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), (unsigned)m.nsplit);
-        MATERIALIZE_FN[h->W](m, grid, h->stream);
+        MATERIALIZE_FN[h->W](m, fk ? *sp : none, fk, grid, h->stream);
         CK(cudaGetLastError());
     }
     h->pending_mat.clear();
@@ -1194,14 +1222,29 @@ static int run_units(ltl_core* h, const std::vector<Unit>& units, bool check_sol
     *status = LTL_S_DONE;
     *seg_index = -1;
     *li = *ri = -1;
+    // Phase B of the newest cost level is due now (its matrices are first needed by this level).  When this level
+    // starts with NOT over exactly those entries (it does unless negation is disabled), phase B screens NOT(entry)
+    // itself while the entry's rows are in registers, and that unit gets ranks but no tiles of its own.
+    i64 fuse_from = -1;
     if (!units.empty()) {
-        int rcf = flush_materialize(h);
-        if (rcf == LTL_ERR_DEVICE_OOM) {  // the operands of this level do not fit the device: out of memory
-            h->device_oom = true;
-            *status = LTL_S_OOM;
-            return LTL_OK;
+        if (h->fuse_not && h->W == 1 && check_solve && (h->variant == VAR_MUELLER || h->variant == VAR_NH) && !h->pending_mat.empty()) {
+            const u64 pend0 = h->pending_mat.front().n_base;
+            const u64 pend1 = h->pending_mat.back().n_base + h->pending_mat.back().count;
+            const Unit& u0 = units[0];
+            bool ok = u0.kind == PIECE_UNARY && u0.op == OP_NOT && (u64)u0.i1 == pend1 && (u64)u0.i0 <= pend0 &&
+                      pend1 == h->n_entries && u0.i1 - u0.i0 <= h->chunk_cap;
+            for (auto& pm : h->pending_mat) ok = ok && !pm.tiled;
+            if (ok) fuse_from = (i64)pend0;
         }
-        if (rcf) return rcf;
+        if (fuse_from < 0) {
+            int rcf = flush_materialize(h);
+            if (rcf == LTL_ERR_DEVICE_OOM) {  // the operands of this level do not fit the device: out of memory
+                h->device_oom = true;
+                *status = LTL_S_OOM;
+                return LTL_OK;
+            }
+            if (rcf) return rcf;
+        }
     }
     std::vector<Piece> pieces;
     size_t ui = 0;
@@ -1210,14 +1253,18 @@ static int run_units(ltl_core* h, const std::vector<Unit>& units, bool check_sol
     while (ui < units.size()) {
         pieces.clear();
         i64 total = 0, tiles = 0;
+        int fused_piece = -1;
         const i64 cap = h->chunk_cap;
         while (ui < units.size() && total < cap) {
             const Unit& u = units[ui];
             const i64 room = cap - total;
             bool unit_done = false;
             if (u.kind == PIECE_UNARY) {
-                const i64 take = std::min(room, u.i1 - row);
-                push_piece(h, pieces, total, tiles, u, row, row + take, -1, -1, PIECE_UNARY);
+                i64 take = std::min(room, u.i1 - row);
+                const bool fused_part = fuse_from >= 0 && ui == 0 && row >= fuse_from;
+                if (fuse_from >= 0 && ui == 0 && row < fuse_from) take = std::min(take, fuse_from - row);  // written part first
+                push_piece(h, pieces, total, tiles, u, row, row + take, -1, -1, PIECE_UNARY, fused_part);
+                if (fused_part) fused_piece = (int)pieces.size() - 1;
                 row += take;
                 unit_done = row == u.i1;
             } else {
@@ -1266,7 +1313,12 @@ static int run_units(ltl_core* h, const std::vector<Unit>& units, bool check_sol
             }
         }
         ChunkOut co;
-        int rc = run_chunk(h, pieces, total, tiles, MODE_INSERT, check_solve, true, &co);
+        int rc = run_chunk(h, pieces, total, tiles, MODE_INSERT, check_solve, true, &co, fused_piece);
+        if (rc == LTL_ERR_DEVICE_OOM && fused_piece >= 0) {  // phase B of the operands did not fit the device
+            h->device_oom = true;
+            *status = LTL_S_OOM;
+            return LTL_OK;
+        }
         if (rc) return rc;
         if (co.status != LTL_S_DONE) {
             *status = co.status;
@@ -1409,6 +1461,12 @@ static int build_deposits(ltl_core* h, const int32_t* proj_rows, const int32_t* 
 // ------------------------------------------------------------------------------------------------
 // C ABI
 
+struct PackScratch {
+    void* buf = nullptr;
+    size_t cap = 0;
+    cudaStream_t st = nullptr;
+};
+
 extern "C" {
 
 int ltl_pack_traces(const uint16_t* chars, const int64_t* lengths, int64_t R, int L, int n_props, int W, int device,
@@ -1430,40 +1488,46 @@ int ltl_pack_traces(const uint16_t* chars, const int64_t* lengths, int64_t R, in
     cudaError_t e;
     if ((e = cudaSetDevice(device)) != cudaSuccess) return cuda_fail(e);
     const int Lpad = 64 * W;  // device rows are padded to whole words so that the 16-byte loads stay in bounds
-    uint16_t* d_chars = nullptr;
-    i64* d_len = nullptr;
-    u64* d_out = nullptr;
     const size_t words = (size_t)R * W;
-    int rc = LTL_OK;
-    cudaStream_t st = nullptr;
-    do {
-        if ((e = cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking)) != cudaSuccess) { rc = cuda_fail(e); break; }
-        if ((e = cudaMalloc(&d_chars, (size_t)R * Lpad * 2)) != cudaSuccess) { rc = cuda_fail(e); break; }
-        if ((e = cudaMalloc(&d_len, (size_t)R * 8)) != cudaSuccess) { rc = cuda_fail(e); break; }
-        if ((e = cudaMalloc(&d_out, words * 8 * (size_t)(n_props + 1))) != cudaSuccess) { rc = cuda_fail(e); break; }
-        if (L == Lpad) {
-            e = cudaMemcpyAsync(d_chars, chars, (size_t)R * L * 2, cudaMemcpyHostToDevice, st);
-        } else {
-            if ((e = cudaMemsetAsync(d_chars, 0, (size_t)R * Lpad * 2, st)) != cudaSuccess) { rc = cuda_fail(e); break; }
-            e = L ? cudaMemcpy2DAsync(d_chars, (size_t)Lpad * 2, chars, (size_t)L * 2, (size_t)L * 2, (size_t)R, cudaMemcpyHostToDevice, st)
-                  : cudaSuccess;
-        }
-        if (e != cudaSuccess) { rc = cuda_fail(e); break; }
-        if ((e = cudaMemcpyAsync(d_len, lengths, (size_t)R * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) { rc = cuda_fail(e); break; }
-        const unsigned nb = (unsigned)((words + 255) / 256);
-        if (n_props <= 4) k_pack<4><<<nb, 256, 0, st>>>(d_chars, d_len, R, L, Lpad, W, n_props, d_out, d_out + words);
-        else if (n_props <= 8) k_pack<8><<<nb, 256, 0, st>>>(d_chars, d_len, R, L, Lpad, W, n_props, d_out, d_out + words);
-        else k_pack<16><<<nb, 256, 0, st>>>(d_chars, d_len, R, L, Lpad, W, n_props, d_out, d_out + words);
-        if ((e = cudaGetLastError()) != cudaSuccess) { rc = cuda_fail(e); break; }
-        if ((e = cudaMemcpyAsync(masks_out, d_out, words * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) { rc = cuda_fail(e); break; }
-        if ((e = cudaMemcpyAsync(atoms_out, d_out + words, words * 8 * (size_t)n_props, cudaMemcpyDeviceToHost, st)) != cudaSuccess) { rc = cuda_fail(e); break; }
-        if ((e = cudaStreamSynchronize(st)) != cudaSuccess) { rc = cuda_fail(e); break; }
-    } while (0);
-    cudaFree(d_chars);
-    cudaFree(d_len);
-    cudaFree(d_out);
-    if (st) cudaStreamDestroy(st);
-    return rc;
+    // one grow-only device scratch and one stream per device, kept for the life of the process: a learn() call makes
+    // no memory-management call for packing (cudaMalloc / cudaFree synchronise the whole device)
+    static std::mutex mu;
+    static PackScratch scratch[LTL_MAX_DEVICES];
+    if (device < 0 || device >= LTL_MAX_DEVICES) return bad("pack: bad device");
+    std::lock_guard<std::mutex> lock(mu);
+    PackScratch& ps = scratch[device];
+    auto up = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const size_t b_chars = up((size_t)R * Lpad * 2), b_len = up((size_t)R * 8), b_out = up(words * 8 * (size_t)(n_props + 1));
+    if (!ps.st && (e = cudaStreamCreateWithFlags(&ps.st, cudaStreamNonBlocking)) != cudaSuccess) return cuda_fail(e);
+    if (ps.cap < b_chars + b_len + b_out) {
+        if (ps.buf) cudaFree(ps.buf);
+        ps.buf = nullptr;
+        ps.cap = 0;
+        if ((e = cudaMalloc(&ps.buf, b_chars + b_len + b_out)) != cudaSuccess) return cuda_fail(e);
+        ps.cap = b_chars + b_len + b_out;
+    }
+    cudaStream_t st = ps.st;
+    uint16_t* d_chars = (uint16_t*)ps.buf;
+    i64* d_len = (i64*)((char*)ps.buf + b_chars);
+    u64* d_out = (u64*)((char*)ps.buf + b_chars + b_len);
+    if (L == Lpad) {
+        e = cudaMemcpyAsync(d_chars, chars, (size_t)R * L * 2, cudaMemcpyHostToDevice, st);
+    } else {
+        if ((e = cudaMemsetAsync(d_chars, 0, (size_t)R * Lpad * 2, st)) != cudaSuccess) return cuda_fail(e);
+        e = L ? cudaMemcpy2DAsync(d_chars, (size_t)Lpad * 2, chars, (size_t)L * 2, (size_t)L * 2, (size_t)R, cudaMemcpyHostToDevice, st)
+              : cudaSuccess;
+    }
+    if (e != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaMemcpyAsync(d_len, lengths, (size_t)R * 8, cudaMemcpyHostToDevice, st)) != cudaSuccess) return cuda_fail(e);
+    const unsigned nb = (unsigned)((words + 255) / 256);
+    if (n_props <= 4) k_pack<4><<<nb, 256, 0, st>>>(d_chars, d_len, R, L, Lpad, W, n_props, d_out, d_out + words);
+    else if (n_props <= 8) k_pack<8><<<nb, 256, 0, st>>>(d_chars, d_len, R, L, Lpad, W, n_props, d_out, d_out + words);
+    else k_pack<16><<<nb, 256, 0, st>>>(d_chars, d_len, R, L, Lpad, W, n_props, d_out, d_out + words);
+    if ((e = cudaGetLastError()) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaMemcpyAsync(masks_out, d_out, words * 8, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaMemcpyAsync(atoms_out, d_out + words, words * 8 * (size_t)n_props, cudaMemcpyDeviceToHost, st)) != cudaSuccess) return cuda_fail(e);
+    if ((e = cudaStreamSynchronize(st)) != cudaSuccess) return cuda_fail(e);
+    return LTL_OK;
 }
 
 int ltl_abi_version(void) { return LTL_ABI_VERSION; }
@@ -1532,12 +1596,22 @@ int ltl_core_create(const uint64_t* masks, int R, int W, int n_pos, int err_max,
         CK(cudaSetDevice(device));
         CK(cudaDeviceGetAttribute(&h->sm_count, cudaDevAttrMultiProcessorCount, device));
         Arena pooled;
-        if (pool_enabled() && pool_take(device, pooled)) static_cast<Arena&>(*h) = pooled;
+        const bool reused = pool_enabled() && pool_take(device, pooled);
+        if (reused) static_cast<Arena&>(*h) = pooled;
         h->device = device;
         if (!h->stream) CK(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+        // cudaMemGetInfo stalls for milliseconds now and then (measured: up to 80 ms with tens of GB mapped), so a core
+        // that starts from a pooled arena sizes its (virtual) reservations from the device's total memory instead;
+        // physical exhaustion is detected where pages are mapped, not here
+        static size_t total_mem[LTL_MAX_DEVICES];
         size_t free_b = 0, total_b = 0;
-        CK(cudaMemGetInfo(&free_b, &total_b));
-        free_b += h->cms.mapped;  // a pooled arena's pages are ours to reuse
+        if (reused && device < LTL_MAX_DEVICES && total_mem[device]) {
+            free_b = total_b = total_mem[device];
+        } else {
+            CK(cudaMemGetInfo(&free_b, &total_b));
+            if (device < LTL_MAX_DEVICES) total_mem[device] = total_b;
+            free_b += h->cms.mapped;  // a pooled arena's pages are ours to reuse
+        }
         // admissions allowed by the logical budget: OOM when admitted*eb + eb > budget (reference _speedups.pyx:252-253)
         // The budget is LOGICAL, like the reference's: admissions are counted, and because matrices are written
         // lazily the entries of the level a search ends in never occupy memory.  Physical exhaustion is reported
@@ -1822,6 +1896,8 @@ int ltl_core_set_option(ltl_core* h, const char* name, int64_t value) {
         h->tiled_materialize = (int)value;
     } else if (!strcmp(name, "fuse_unary")) {
         h->fuse_unary = value != 0;
+    } else if (!strcmp(name, "fuse_not")) {
+        h->fuse_not = value != 0;
     } else if (!strcmp(name, "profile")) {
         h->profile = value != 0;
     } else if (!strcmp(name, "max_split")) {

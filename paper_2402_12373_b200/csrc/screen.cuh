@@ -720,8 +720,137 @@ __global__ void __launch_bounds__(LTL_CTA) k_materialize(const __grid_constant__
     }
 }
 
+// ------------------------------------------------------------------------------------------------
+// phase B with the next level's NOT fused in (one-word rows)
+//
+// Phase B is bound by HBM (it writes every new matrix once) and leaves the integer pipes idle, while the first
+// thing the next cost level does with the new entries is a pass that reads them all back to screen NOT(entry)
+// (connective order formula.py:24).  Here that candidate is evaluated from the row that is in registers anyway:
+// error count (reference _speedups.pyx:327-333), fingerprint fold (KIND_MUELLER: _speedups.pyx:196-202, blocked;
+// KIND_NH: oracle fp_nh), and at the end the same table filing as phase A.  Rows go in blocks of 64 (the
+// fingerprint's block length) so the block epilogue stays out of the row loop.
+
+#ifndef LTL_MATF_UNROLL
+#define LTL_MATF_UNROLL 16
+#endif
+#ifndef LTL_MATF_MINB
+#define LTL_MATF_MINB 2
+#endif
+
+template <int FK>
+struct NotFold {
+    u64 s0, s1, h0, h1;
+    u32 err;
+    __device__ __forceinline__ void begin_block() {
+        h0 = FK == KIND_NH ? 0ull : K_SEED0;
+        h1 = FK == KIND_NH ? 0ull : K_SEED1;
+    }
+    // v = word k (= row k, W = 1) of NOT(entry); pk = k mod 64
+    __device__ __forceinline__ void word(const u64 v, const u32 k, const u32 pk, const bool positive) {
+        const u32 bit = (u32)(v >> 63);
+        err += positive ? 1u - bit : bit;
+        if (FK == KIND_NH) {
+            const u64 key0 = c_nh.k[pk], key1 = c_nh.k[pk + 1];
+            const u32 xl = (u32)v, xh = (u32)(v >> 32);
+            h0 = mad_wide(xl + (u32)key0, xh + (u32)(key0 >> 32), h0);
+            h1 = mad_wide(xl + (u32)key1, xh + (u32)(key1 >> 32), h1);
+        } else {
+            const u64 mm = mix64(v ^ ((u64)(k + 1) * K_STEP));
+            h0 = (h0 ^ mm) * K_FOLD0;
+            h1 = (h1 ^ ((mm << 32) | (mm >> 32))) * K_FOLD1;
+        }
+    }
+    __device__ __forceinline__ void end_block(const u32 blk) {
+        if (FK == KIND_NH) {
+            const u64 u = (u64)(blk + 1) * K_STEP;
+            s0 += mix64(h0 ^ u);
+            s1 += mix64(h1 + u);
+        } else {
+            s0 += blk == 0 ? h0 : mix64(h0);
+            s1 += blk == 0 ? h1 : mix64(h1);
+        }
+    }
+};
+
+template <int OP, int FK>
+__device__ __forceinline__ void mat_rows_not(const MaterializeParams& p, const bool mine, const i64 dst, const int lhs,
+                                             const int rhs, NotFold<FK>& f) {
+    constexpr bool BIN = !(OP == OP_IDENT || OP == OP_NOT || OP == OP_NEXT || OP == OP_FINALLY || OP == OP_GLOBALLY);
+    if (!mine) return;
+    const i64 n = p.n;
+    const u64* __restrict__ px = p.cms + cm_index(lhs, n, 0);
+    const u64* __restrict__ py = p.cms + cm_index(BIN ? rhs : lhs, n, 0);
+    u64* __restrict__ po = p.cms + cm_index(dst, n, 0);
+    const u64* __restrict__ pm = p.masks;
+    const int R = p.R, n_pos = p.n_pos;
+    auto row = [&](const int r, const u32 pk) {
+        u64 x[1], y[1], m[1], out[1];
+        x[0] = ld_nc(px + (size_t)r * 32);
+        y[0] = BIN ? ld_nc(py + (size_t)r * 32) : 0ull;
+        m[0] = ld_nc(pm + r);
+        apply_row<OP, 1>(out, x, y, m);
+        po[(size_t)r * 32] = out[0];
+        f.word(~out[0] & m[0], (u32)r, pk, r < n_pos);
+    };
+    constexpr int UNROLL = LTL_MATF_UNROLL;
+    for (int rb = 0; rb < R; rb += 64) {
+        f.begin_block();
+        if (rb + 64 <= R) {
+#pragma unroll UNROLL
+            for (int i = 0; i < 64; i++) row(rb + i, (u32)i);
+        } else {
+            for (int i = 0; rb + i < R; i++) row(rb + i, (u32)i);
+        }
+        f.end_block((u32)rb >> 6);
+    }
+}
+
+template <int FK>
+__global__ void __launch_bounds__(LTL_CTA, LTL_MATF_MINB) k_materialize_not(const __grid_constant__ MaterializeParams p,
+                                                                            const __grid_constant__ ScreenParams sp) {
+    const int lane = threadIdx.x & 31;
+    const i64 g = (p.n_base >> 5) + (i64)blockIdx.x * LTL_WARPS_PER_CTA + (threadIdx.x >> 5);
+    const i64 dst = g * 32 + lane;
+    if (g * 32 >= p.n_base + p.count) return;
+    const bool valid = dst >= p.n_base && dst < p.n_base + p.count;
+    const int op = valid ? (int)p.rec_op[dst] : -1;
+    const int lhs = valid ? p.rec_lhs[dst] : 0;
+    const int rhs = valid ? p.rec_rhs[dst] : 0;
+    NotFold<FK> f;
+    f.s0 = f.s1 = 0;
+    f.err = 0;
+    unsigned remaining = __ballot_sync(0xFFFFFFFFu, valid);
+    while (remaining) {
+        const int leader = __ffs(remaining) - 1;
+        const int cur = __shfl_sync(0xFFFFFFFFu, op, leader);
+        const bool mine = valid && op == cur;
+        remaining &= ~__ballot_sync(0xFFFFFFFFu, mine);
+        switch (cur) {
+            case OP_NOT: mat_rows_not<OP_NOT, FK>(p, mine, dst, lhs, rhs, f); break;
+            case OP_AND: mat_rows_not<OP_AND, FK>(p, mine, dst, lhs, rhs, f); break;
+            case OP_OR: mat_rows_not<OP_OR, FK>(p, mine, dst, lhs, rhs, f); break;
+            case OP_NEXT: mat_rows_not<OP_NEXT, FK>(p, mine, dst, lhs, rhs, f); break;
+            case OP_FINALLY: mat_rows_not<OP_FINALLY, FK>(p, mine, dst, lhs, rhs, f); break;
+            case OP_GLOBALLY: mat_rows_not<OP_GLOBALLY, FK>(p, mine, dst, lhs, rhs, f); break;
+            case OP_UNTIL: mat_rows_not<OP_UNTIL, FK>(p, mine, dst, lhs, rhs, f); break;
+            default: mat_rows_not<OP_IDENT, FK>(p, mine, dst, lhs, rhs, f); break;
+        }
+        __syncwarp();
+    }
+    if (valid) {  // file NOT(dst) as candidate not_cbase + (dst - not_i0) of the pass in flight
+        const u64 c = (u64)p.not_cbase + (u64)(dst - p.not_i0);
+        if (sp.nsplit > 1) {  // the pass combines row splits: hand the (complete) sums to k_finalize
+            atomicAdd(sp.acc_s0 + c, f.s0);
+            atomicAdd(sp.acc_s1 + c, f.s1);
+            if (f.err) atomicAdd(sp.acc_err + c, f.err);
+        } else {
+            finish_candidate<true>(sp, c, f.s0, f.s1, f.err);
+        }
+    }
+}
+
 #endif  // __CUDACC__
 
 // launchers, one translation unit per W (screen_inst.cu compiled with -DLTL_W=<W>)
 typedef void (*screen_launch_fn)(const ScreenParams&, int kind, dim3 grid, cudaStream_t stream);
-typedef void (*materialize_launch_fn)(const MaterializeParams&, dim3 grid, cudaStream_t stream);
+typedef void (*materialize_launch_fn)(const MaterializeParams&, const ScreenParams&, int fuse_kind, dim3 grid, cudaStream_t stream);

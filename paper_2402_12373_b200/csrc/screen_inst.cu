@@ -23,6 +23,20 @@ extern "C" void LTL_CAT(ltl_launch_screen_w, LTL_W)(const ScreenParams& p, int k
     else k_screen<LTL_W, KIND_REWRITE><<<grid, LTL_CTA, Ring<LTL_W>::CTA_BYTES, stream>>>(p);
 }
 
-extern "C" void LTL_CAT(ltl_launch_materialize_w, LTL_W)(const MaterializeParams& p, dim3 grid, cudaStream_t stream) {
+// fuse_kind != 0 (one-word rows only; the host never asks otherwise): phase B that also screens NOT(new entry)
+extern "C" void LTL_CAT(ltl_launch_materialize_w, LTL_W)(const MaterializeParams& p, const ScreenParams& sp, int fuse_kind,
+                                                          dim3 grid, cudaStream_t stream) {
+#if LTL_W == 1
+    if (fuse_kind == KIND_NH) {
+        k_materialize_not<KIND_NH><<<grid, LTL_CTA, 0, stream>>>(p, sp);
+        return;
+    }
+    if (fuse_kind == KIND_MUELLER) {
+        k_materialize_not<KIND_MUELLER><<<grid, LTL_CTA, 0, stream>>>(p, sp);
+        return;
+    }
+#endif
+    (void)sp;
+    (void)fuse_kind;
     k_materialize<LTL_W><<<grid, LTL_CTA, 0, stream>>>(p);
 }

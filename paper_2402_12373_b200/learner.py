@@ -106,6 +106,7 @@ class EnumStats:
     search_seconds: float = 0.0
     h2d_bytes: int = 0  # host->device / device->host bytes moved by the device core for this search
     d2h_bytes: int = 0
+    phase_ms: dict = field(default_factory=dict)  # host wall time of the call's phases (pack, scheme, create, close)
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k in ("offered", "admitted", "duplicates", "peak_bytes", "precise",
@@ -236,9 +237,11 @@ class Enumeration:
         # product path (no injected core): packing runs on the device too; an injected core factory (tests with
         # the CPU oracle, the sharded wrapper) gets host-packed inputs
         on_device = cfg.pack_on_device if cfg.pack_on_device is not None else core_factory is None
+        t_pack = time.perf_counter()
         self.ctx = ctx = TraceContext.from_spec(spec, alphabet, device=cfg.device if on_device else None)
         n_pos, err_max, h = spec.n_pos, cfg.err_max(spec), cfg.cost
         self.stats = stats = EnumStats()
+        stats.phase_ms["pack"] = 1e3 * (time.perf_counter() - t_pack)
         stats.ceiling = overfit_cost(spec, alphabet, h)
         self.ceiling = stats.ceiling if cfg.ceiling is None else min(cfg.ceiling, stats.ceiling)
         self.outcome: EnumOutcome | None = None
@@ -258,14 +261,18 @@ class Enumeration:
                     self.outcome = Solved(Not(Atom(p)), atom_c + h.of(OP_NOT), stats)
                     return
 
+        t_scheme = time.perf_counter()
         rs = resolve_scheme(cfg.hash, ctx.lengths, SuffixTable.from_spec(spec, limit=126), words_per_row=ctx.words)
         stats.precise = rs.precise
+        t_create = time.perf_counter()
+        stats.phase_ms["scheme"] = 1e3 * (t_create - t_scheme)
         if core_factory is None:
             from .core import make_core as core_factory  # CUDA core; raises BackendUnavailable
         self.core = core_factory(ctx.masks, n_pos, err_max, rs.variant, rs.proj_rows, rs.proj_offs, rs.fkp_bits,
                                  rs.mask_k, cfg.budget_bytes, words_per_row=ctx.words, device=cfg.device)
         self.cache = cache = LanguageCache(self.core)
         self._t_search = time.perf_counter()
+        stats.phase_ms["create"] = 1e3 * (self._t_search - t_create)
         try:
             admitted_atoms = [p for p in range(alphabet.size)
                               if cache.try_admit(ctx.atoms[p], (OP_ATOM, p, -1), atom_c)]
@@ -287,7 +294,9 @@ class Enumeration:
         if not self.keep_core:
             close = getattr(core, "close", None)
             if close:
+                t_close = time.perf_counter()
                 close()
+                stats.phase_ms["close"] = 1e3 * (time.perf_counter() - t_close)
         return outcome
 
     keep_core = False

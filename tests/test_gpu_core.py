@@ -433,3 +433,42 @@ def test_device_packing_matches_host_packing(R, L, n_props, W):
     want = TraceContext.from_spec(spec, Alphabet.default(n_props), words=W)
     assert (masks == want.masks).all()
     assert (atoms == want.atoms).all()
+
+
+@pytest.mark.parametrize("R,err_max,budget_entries,chunk", [(16, -1, None, None), (64, -1, None, None), (100, -1, None, None),
+                                                            (200, -1, None, None), (1024, -1, None, None),
+                                                            (100, 40, None, None), (64, 27, None, None),
+                                                            (100, -1, 700, None), (130, -1, None, 500), (256, 110, None, 3000)])
+@pytest.mark.parametrize("variant", [V_MUELLER, V_NH], ids=["mueller", "nh"])
+def test_fused_not_levels_match_unfused(R, err_max, budget_entries, chunk, variant):
+    """Phase B of a level also screens NOT(new entry) for the next level (k_materialize_not): identical statuses,
+    counters, matrices and records to screening NOT in a pass of its own -- with partial 64-row fingerprint blocks,
+    a solver among the fused candidates, the budget running out inside them, and chunks that cut the NOT unit."""
+    from paper_2402_12373_b200.learner import Segment
+
+    rng = np.random.default_rng(9000 + R)
+    masks = random_masks(rng, R, 1)
+    budget = (1 << 40) if budget_entries is None else budget_entries * (8 * R + 16)
+    kw = {} if chunk is None else {"chunk_candidates": chunk}
+    a, b = (CudaCore(masks, R // 2, err_max, variant, budget_bytes=budget, **kw) for _ in range(2))
+    b.set_option("fuse_not", 0)
+    for k in range(5):
+        cm = random_cm(rng, masks)
+        assert a.add_entry(cm, 0, k, -1) == b.add_entry(cm, 0, k, -1)
+    lo = 0
+    for _ in range(3):
+        hi = a.n_entries
+        if hi > 200:  # the next level would have millions of entries
+            break
+        segs = [Segment(1, lo, hi), Segment(2, 0, hi, 0, hi, True), Segment(3, 0, hi, 0, hi, True), Segment(4, lo, hi),
+                Segment(5, lo, hi), Segment(6, lo, hi), Segment(7, 0, hi, 0, hi, False)]
+        ra, rb = a.run_level(segs), b.run_level(segs)
+        assert ra == rb
+        assert a.counters() == b.counters()
+        if ra[0] != 0:
+            break
+        lo = hi
+    assert (a.export_cms() == b.export_cms()).all()
+    assert (records_array(a) == records_array(b)).all()
+    a.close()
+    b.close()
