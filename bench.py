@@ -283,6 +283,23 @@ def main():
         dram = traffic * scr_launch / (scr_ms / 1e3) / 1e9
         roofline["dram"] = {"achieved": dram, "unit": "GB/s", "frac": dram / peak,
                             "source": "ncu dram__bytes_read+write per launch (profiles/roofline_traffic.json)"}
+    mat_ms = sum(ks["materialize"]["ms"] for ks in kstats)
+    mat_bytes = sum(ks["materialize"]["alg_bytes"] for ks in kstats)
+    if mat_ms > 0:  # second kernel of the step: phase B (k_materialize / k_materialize_not), bound by HBM
+        roofline["materialize"] = {"bound": "hbm", "kernel": "k_materialize_not + k_materialize",
+                                   "achieved": mat_bytes / (mat_ms / 1e3) / 1e9, "peak": peak, "unit": "GB/s",
+                                   "frac": mat_bytes / (mat_ms / 1e3) / 1e9 / peak,
+                                   "note": "algorithmic bytes = admitted entries x (8n + 16 + 9) written (SURVEY 8d) + "
+                                           "16 per fused NOT candidate; the operand matrices it re-reads are not counted"}
+        try:
+            mt = prof.get("k_materialize_dram_bytes_per_step")
+            if mt and args.config == "c2_planted" and max_cost == wl["max_cost"]:
+                roofline["materialize"]["dram"] = {"achieved": mt * args.steps / (mat_ms / 1e3) / 1e9, "unit": "GB/s",
+                                                   "frac": mt * args.steps / (mat_ms / 1e3) / 1e9 / peak,
+                                                   "source": "ncu dram__bytes_read+write of one search "
+                                                             "(profiles/roofline_traffic.json) / CUDA-event kernel time"}
+        except Exception:
+            pass
     if insts and scr_ms > 0 and clocks.get("sm_mhz"):
         sm_count = torch.cuda.get_device_properties(local_rank).multi_processor_count
         ipeak = sm_count * 4 * clocks["sm_mhz"] * 1e6  # one warp instruction per cycle per SM sub-partition

@@ -604,7 +604,9 @@ struct ltl_core : Arena {
     int sm_count = 148;
     int max_split = 4096, force_split = 0;
     bool fuse_unary = true;
-    bool fuse_not = true;  // phase B of a level also screens NOT(new entry) for the next level (k_materialize<W, FK>)
+    bool fuse_not = true;  // phase B of a level also screens NOT(new entry) for the next level (k_materialize_not)
+    i64 fuse_not_min = 32768;  // ... when it writes at least this many entries: the fused kernel folds all rows of an
+                               // entry in one lane (no row split), which is slow on a launch that cannot fill the SMs
     int tiled_materialize = -1;  // phase B over phase A's tiles instead of per record: 1 always, 0 never, -1 by size
     bool device_oom = false;      // an S_OOM came from the device, not from the logical budget
     bool store_results = true;    // false: admitted entries get records and fingerprints but no matrix
@@ -1232,7 +1234,7 @@ static int run_units(ltl_core* h, const std::vector<Unit>& units, bool check_sol
             const u64 pend1 = h->pending_mat.back().n_base + h->pending_mat.back().count;
             const Unit& u0 = units[0];
             bool ok = u0.kind == PIECE_UNARY && u0.op == OP_NOT && (u64)u0.i1 == pend1 && (u64)u0.i0 <= pend0 &&
-                      pend1 == h->n_entries && u0.i1 - u0.i0 <= h->chunk_cap;
+                      pend1 == h->n_entries && u0.i1 - u0.i0 <= h->chunk_cap && (i64)(pend1 - pend0) >= h->fuse_not_min;
             for (auto& pm : h->pending_mat) ok = ok && !pm.tiled;
             if (ok) fuse_from = (i64)pend0;
         }
@@ -1898,6 +1900,8 @@ int ltl_core_set_option(ltl_core* h, const char* name, int64_t value) {
         h->fuse_unary = value != 0;
     } else if (!strcmp(name, "fuse_not")) {
         h->fuse_not = value != 0;
+    } else if (!strcmp(name, "fuse_not_min")) {
+        h->fuse_not_min = value;
     } else if (!strcmp(name, "profile")) {
         h->profile = value != 0;
     } else if (!strcmp(name, "max_split")) {

@@ -19,9 +19,14 @@ ap.add_argument("--max-cost", type=int, default=None)
 ap.add_argument("--budget-gb", type=float, default=150.0)
 ap.add_argument("--stats", action="store_true")
 ap.add_argument("--repeat", type=int, default=1)
+ap.add_argument("--unsolvable", action="store_true", help="random traces of the config's shape: every level is exhaustive")
 a = ap.parse_args()
 t0 = time.time()
-spec, alphabet, planted, wl = Wl.make_config(a.config)
+if a.unsolvable:
+    wl = dict(Wl.CONFIGS[a.config])
+    spec, alphabet = Wl.random_spec(wl["n_props"], wl["n_pos"], wl["n_neg"], wl["min_len"], wl["max_len"], wl["seed"])
+else:
+    spec, alphabet, planted, wl = Wl.make_config(a.config)
 print(f"workload {a.config}: {spec.n_pos}+{spec.n_neg} traces, max_len {spec.max_len}, generated in {time.time() - t0:.1f} s")
 cores = []
 
@@ -46,7 +51,8 @@ for rep in range(a.repeat):
     dt = time.time() - t0
     print(f"run {rep}: {res.status} {res.text!r} cost={res.cost} offered={res.stats.offered} admitted={res.stats.admitted} "
           f"wall={dt * 1e3:.1f} ms  search={res.stats.search_seconds * 1e3:.1f} ms  "
-          f"{res.stats.offered / max(res.stats.search_seconds, 1e-9) / 1e6:.1f} M cand/s")
+          f"{res.stats.offered / max(res.stats.search_seconds, 1e-9) / 1e6:.1f} M cand/s  "
+          f"phases {({k: round(v, 1) for k, v in res.stats.phase_ms.items()})}")
 print([(lv["cost"], lv["offered"], lv["admitted"], lv.get("ms")) for lv in res.stats.levels])
 if a.stats and cores:
     ks, ht, info = cores[-1]

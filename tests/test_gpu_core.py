@@ -451,6 +451,7 @@ def test_fused_not_levels_match_unfused(R, err_max, budget_entries, chunk, varia
     budget = (1 << 40) if budget_entries is None else budget_entries * (8 * R + 16)
     kw = {} if chunk is None else {"chunk_candidates": chunk}
     a, b = (CudaCore(masks, R // 2, err_max, variant, budget_bytes=budget, **kw) for _ in range(2))
+    a.set_option("fuse_not_min", 0)  # by default only launches that fill the device are fused
     b.set_option("fuse_not", 0)
     for k in range(5):
         cm = random_cm(rng, masks)
