@@ -161,6 +161,9 @@ def main():
     ap.add_argument("--ref-sample-cost", type=int, default=8)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--budget-gb", type=float, default=150.0)
+    ap.add_argument("--sharding", default="auto", choices=["auto", "rows", "candidates"],
+                    help="N > 1: row shards (partial fingerprints all-reduced, store partitioned) or candidate ranges "
+                         "(hash-owner all-to-all, store replicated); auto = rows when the rows cut into whole blocks")
     ap.add_argument("--hash", default="mueller", choices=["mueller", "mueller_blocked", "nh", "fkp"],
                     help="fingerprint scheme (scheme.py): 'mueller' = the reference's hash inside its domain, NH beyond")
     args = ap.parse_args()
@@ -186,7 +189,7 @@ def main():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
-    if args.gpus > 1 or world > 1:
+    if args.gpus > 1 or world > 1 or os.environ.get("LTL_FORCE_SHARDED"):  # the env switch: NCCL path on one GPU (tests)
         from paper_2402_12373_b200 import sharded
 
         return sharded.bench_main(args, spec, alphabet, planted, cfg_desc)

@@ -140,6 +140,20 @@ LTL_API int ltl_core_entry_fingerprints(ltl_core* h, int64_t first, int64_t coun
 /* out[0..4] = n_entries, bytes_used, offered, admitted, duplicates: reference _speedups.pyx:68, 113-115. */
 LTL_API int ltl_core_counters(ltl_core* h, uint64_t out[5]);
 
+/* Row-sharded cores (the alternative for specifications with many rows): G cores, one per GPU, each
+ * created over a contiguous slice of the ROWS of the specification (masks of its rows, n_pos = its number of
+ * positive rows).  Every core enumerates every candidate on its rows; the per-candidate partial fingerprint sums and
+ * error counts (device arrays: uint64 s0[count], uint64 s1[count], uint32 err[count]) are handed to `fn`, which must
+ * replace them by their element-wise sums over all shards (wrapping 64-bit / 32-bit adds; NCCL all-reduce) and
+ * return 0 once the result is visible to the device; every core then completes identical candidates, admits the
+ * same entries in the same order and writes its rows of the new matrices.  No reference counterpart (the reference
+ * is one process); the results are those of one core over all rows.
+ * word_base: index of this shard's first word in the whole matrix (rows before it x W), a multiple of 64;
+ * total_words: words of the whole matrix (the budget counts whole matrices: reference _speedups.pyx:100, 252-253).
+ * Call once, right after ltl_core_create.  Needs a block-combinable fingerprint (LTL_V_MUELLER / LTL_V_NH). */
+typedef int (*ltl_exchange_fn)(void* ctx, void* d_s0, void* d_s1, void* d_err, int64_t count);
+LTL_API int ltl_core_set_row_shard(ltl_core* h, int64_t word_base, int64_t total_words, ltl_exchange_fn fn, void* ctx);
+
 /* Tuning / measurement (no reference counterpart).
  * options: "chunk_candidates" (candidates per device pass), "profile" (1: time every kernel with CUDA
  * events on the launching stream), "max_split" (cap on row splits), "force_split" (tests),

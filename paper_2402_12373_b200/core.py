@@ -37,6 +37,9 @@ class Segment(C.Structure):
                 ("b1", C.c_int64)]
 
 
+#: row-shard exchange callback (include/ltl_core.h: ltl_exchange_fn)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64)
+
 _lib = None
 
 
@@ -76,6 +79,7 @@ def load_library():
     L.ltl_core_entry_fingerprints.argtypes = [vp, C.c_int64, C.c_int64, u64p, u64p]
     L.ltl_core_counters.argtypes = [vp, u64p]
     L.ltl_core_set_option.argtypes = [vp, C.c_char_p, C.c_int64]
+    L.ltl_core_set_row_shard.argtypes = [vp, C.c_int64, C.c_int64, EXCHANGE_FN, vp]
     L.ltl_core_kernel_stats.argtypes = [vp, C.c_int, u64p, C.POINTER(C.c_double), C.POINTER(C.c_double), u64p]
     L.ltl_core_reset_kernel_stats.argtypes = [vp]
     L.ltl_core_info.argtypes = [vp, u64p]
@@ -98,7 +102,7 @@ def load_library():
     for name in ("ltl_core_create", "ltl_core_add_entry", "ltl_core_screen_unary", "ltl_core_screen_binary",
                  "ltl_core_run_level", "ltl_core_contains", "ltl_core_fingerprint_of", "ltl_core_get_cm",
                  "ltl_core_get_record", "ltl_core_export_cms", "ltl_core_export_records",
-                 "ltl_core_entry_fingerprints", "ltl_core_counters", "ltl_core_set_option", "ltl_core_kernel_stats",
+                 "ltl_core_entry_fingerprints", "ltl_core_counters", "ltl_core_set_option", "ltl_core_set_row_shard", "ltl_core_kernel_stats",
                  "ltl_core_reset_kernel_stats", "ltl_core_info", "ltl_core_stream", "ltl_core_transfer_stats"):
         getattr(L, name).restype = C.c_int
     _lib = L
@@ -198,6 +202,9 @@ class CudaCore:
     def _check(self, rc):
         if rc == 0:
             return
+        exc, self._exchange_error = getattr(self, "_exchange_error", None), None
+        if exc is not None:  # raised inside the row-shard exchange callback
+            raise exc
         msg = (self._L.ltl_core_last_error(self._h) or b"").decode()
         if rc == ERR_BUDGET:
             raise CoreOOM(msg)
@@ -309,6 +316,34 @@ class CudaCore:
         self._check(self._L.ltl_core_run_level(self._h, arr, len(segments), C.byref(st), C.byref(seg), C.byref(li),
                                                C.byref(ri)))
         return st.value, seg.value, li.value, ri.value
+
+    # -- row shard (see sharded.RowShardedCore) --------------------------------------------
+    def set_row_shard(self, word_base: int, total_words: int, all_reduce_sum):
+        """Make this core one row shard of a larger specification.  ``all_reduce_sum(tensors)`` must add, in place
+        and across all shards, the given device tensors (int64, int64, int32: wrapping sums) and return once the
+        result is visible to the device."""
+        import torch
+
+        dev = torch.device("cuda", self.device_index)
+
+        class _Dev:  # zero-copy view of a device array of the library (CUDA array interface)
+            def __init__(self, ptr, n, typestr):
+                self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (int(ptr), False), "version": 2}
+
+        def hook(_ctx, s0, s1, err, count):
+            try:
+                n = int(count)
+                ts = [torch.as_tensor(_Dev(s0, n, "<i8"), device=dev), torch.as_tensor(_Dev(s1, n, "<i8"), device=dev),
+                      torch.as_tensor(_Dev(err, n, "<i4"), device=dev)]
+                all_reduce_sum(ts)
+                return 0
+            except BaseException as exc:  # noqa: BLE001 -- no exception may cross the C ABI
+                self._exchange_error = exc
+                return 1
+
+        self._exchange_error = None
+        self._exchange_cb = EXCHANGE_FN(hook)  # keep the trampoline alive as long as the core
+        self._check(self._L.ltl_core_set_row_shard(self._h, int(word_base), int(total_words), self._exchange_cb, None))
 
     # -- multi-GPU stages (device tensors in / out; see sharded.py) -----------------------
     @staticmethod

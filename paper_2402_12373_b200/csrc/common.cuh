@@ -130,6 +130,11 @@ struct ScreenParams {
     const u32* dest;  // per candidate: position among the winners / NONE
     u64* cms_out;     // same buffer as cms
     i64 n_base;
+    // row-sharded cores (one GPU holds rows [row_base, row_base + R) of every matrix): this core's first word is word
+    // 64 * blk_base of the whole matrix (fingerprint blocks and tweaks are numbered globally), and partial sums always
+    // go to acc_* -- they are summed across GPUs before k_finalize completes the candidates
+    u32 blk_base;
+    int defer;
 };
 
 struct MaterializeParams {
@@ -146,6 +151,8 @@ struct MaterializeParams {
     // the NEXT cost level is evaluated too -- its chunk-local rank is not_cbase + (entry - not_i0)
     int n_pos;
     i64 not_cbase, not_i0;
+    u32 blk_base;  // as in ScreenParams
+    u32 pad_;
 };
 
 __host__ __device__ __forceinline__ u64 mix64(u64 x) {  // reference kernels.py:50-57

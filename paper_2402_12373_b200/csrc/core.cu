@@ -600,10 +600,16 @@ struct ltl_core : Arena {
     i64 sub_tiles = 1 << 15;  // warp tiles per phase-A launch: little work is issued after a solver shows up
     u64 n_entries = 0, offered = 0, admitted = 0, duplicates = 0;
     u64 h2d_bytes = 0, d2h_bytes = 0;  // host<->device traffic of this handle
+    double exchange_ms = 0;  // host wall time inside the row-shard exchange callback
     double grow_ms = 0, sync_ms = 0, plan_ms = 0;  // host wall time: store growth, waiting for the device, planning
     int sm_count = 148;
     int max_split = 4096, force_split = 0;
     bool fuse_unary = true;
+    // row shard (ltl_core_set_row_shard): this core holds rows of every matrix starting at word 64 * blk_base of the
+    // whole matrix; partial sums are summed across the shards by `exchange` before candidates are completed
+    u32 blk_base = 0;
+    ltl_exchange_fn exchange = nullptr;
+    void* exchange_ctx = nullptr;
     bool fuse_not = true;  // phase B of a level also screens NOT(new entry) for the next level (k_materialize_not)
     i64 fuse_not_min = 32768;  // ... when it writes at least this many entries: the fused kernel folds all rows of an
                                // entry in one lane (no row split), which is slow on a launch that cannot fill the SMs
@@ -991,7 +997,10 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     p.slot = h->d_slot;
     p.fp_out = mode == MODE_FP_ONLY ? (h->fp_ext ? h->fp_ext : h->d_fp) : nullptr;
     p.ctl = h->d_ctl;
-    if (p.nsplit > 1) {
+    p.blk_base = h->blk_base;
+    p.defer = h->exchange ? 1 : 0;
+    const bool acc_path = p.nsplit > 1 || p.defer;
+    if (acc_path) {
         if ((rc = ensure_acc(h, total))) return rc;
         p.acc_s0 = h->d_acc_s0;
         p.acc_s1 = h->d_acc_s1;
@@ -1010,7 +1019,9 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     // between (two in flight); after each one the solver rank is copied to pinned memory, and once a solver is
     // known no launch is issued whose first tile lies above it.
     {
-        const i64 per = (p.nsplit > 1 || mode != MODE_INSERT) ? tiles : std::max<i64>(h->sub_tiles, LTL_WARPS_PER_CTA);
+        // (fingerprint-only passes that look for a solver -- the sharded evaluation stage -- stop early too)
+        const bool whole = acc_path || mode == MODE_LOOKUP || (mode == MODE_FP_ONLY && !check_solve);
+        const i64 per = whole ? tiles : std::max<i64>(h->sub_tiles, LTL_WARPS_PER_CTA);
         const double bytes_all = screen_bytes(h, pieces);
         u64 known_solver = ~0ull;
         int k = 0;
@@ -1044,7 +1055,16 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
         }
     }
     CK(cudaGetLastError());
-    if (p.nsplit > 1) {
+    if (p.defer) {  // row shards: every shard adds its partial sums, then all of them complete identical candidates
+        {
+            HostTimer ht(&h->sync_ms);
+            CK(cudaStreamSynchronize(h->stream));
+        }
+        HostTimer ht(&h->exchange_ms);
+        if (h->exchange(h->exchange_ctx, h->d_acc_s0, h->d_acc_s1, h->d_acc_err, (int64_t)total))
+            return h->fail(LTL_ERR_CUDA, "row-shard exchange failed");
+    }
+    if (acc_path) {
         ScopedTimer t(h, LTL_K_FINALIZE, (u64)total, (double)total * 36.0);
         if (mueller) k_finalize<true><<<(unsigned)((total + 255) / 256), 256, 0, h->stream>>>(p, (u64)total);
         else k_finalize<false><<<(unsigned)((total + 255) / 256), 256, 0, h->stream>>>(p, (u64)total);
@@ -1194,6 +1214,7 @@ static int flush_materialize(ltl_core* h, const ScreenParams* sp, int fuse_kind,
         m.rec_op = (const unsigned char*)h->rec_op.base;
         m.rec_lhs = (const int*)h->rec_lhs.base;
         m.rec_rhs = (const int*)h->rec_rhs.base;
+        m.blk_base = h->blk_base;
         const i64 groups = (i64)((n_base + count + 31) / 32 - n_base / 32);
         choose_split(h, groups, &m.nsplit, &m.rows_per_split);
         ScreenParams none;
@@ -1951,6 +1972,24 @@ int ltl_core_level_size(ltl_core* h, const ltl_segment* segs, int n_segs, int64_
     i64 t = 0;
     for (auto& u : units) t += unit_count(u);
     *total = t;
+    return LTL_OK;
+}
+
+int ltl_core_set_row_shard(ltl_core* h, int64_t word_base, int64_t total_words, ltl_exchange_fn fn, void* ctx) {
+    ENTER(h);
+    if (h->n_entries || h->offered) return h->fail(LTL_ERR_ARG, "set_row_shard: the core is already in use");
+    if (!fn || word_base < 0 || (word_base & 63) || total_words < word_base + h->n)
+        return h->fail(LTL_ERR_ARG, "set_row_shard: word_base must be a multiple of 64 and the shard must lie inside the matrix");
+    if (word_base + h->n < total_words && (h->n & 63))
+        return h->fail(LTL_ERR_ARG, "set_row_shard: only the last shard may end inside a 64-word fingerprint block");
+    if (h->variant != VAR_MUELLER && h->variant != VAR_NH)
+        return h->fail(LTL_ERR_ARG, "set_row_shard: needs a block-combinable fingerprint (mueller / nh)");
+    h->blk_base = (u32)(word_base >> 6);
+    h->exchange = fn;
+    h->exchange_ctx = ctx;
+    // the budget counts whole matrices, like the reference's (reference _speedups.pyx:100, 252-253)
+    h->entry_bytes = (u64)total_words * 8 + 16;
+    h->cap_entries = std::min<u64>(h->cap_entries, h->budget / h->entry_bytes);
     return LTL_OK;
 }
 

@@ -277,7 +277,7 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
         h1[t] = NH ? 0ull : K_SEED1;
         ones[t] = ones_pos[t] = 0;
     }
-    u64 tw = ((u64)r0 * W + 1ull) * K_STEP;  // (k + 1) * STEP for the next word k
+    u64 tw = ((u64)p.blk_base * 64ull + (u64)r0 * W + 1ull) * K_STEP;  // (k + 1) * STEP for the next (global) word k
     int d = 0;                               // next deposit (bits fingerprints)
     if (KIND == KIND_BITS) {
         const u32 kfirst = (u32)r0 * W;
@@ -290,7 +290,8 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
         d = lo_;
     }
 
-    auto fold = [&](const u32 blk) {  // blocked Mueller: block 0 enters as is (== reference for n <= 64)
+    auto fold = [&](const u32 blk_local) {  // blocked Mueller: block 0 enters as is (== reference for n <= 64)
+        const u32 blk = blk_local + p.blk_base;
         const bool first = blk == 0;
 #pragma unroll
         for (int t = 0; t < TI; t++) {
@@ -364,7 +365,7 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
                     if (!Ring<W>::CHUNK_FOLD) {
                         const u64 k1 = kb + w + 1;
                         if ((k1 & 63) == 0 || k1 == (u64)n) {
-                            const u64 u = (((k1 - 1) >> 6) + 1) * K_STEP;
+                            const u64 u = (((k1 - 1) >> 6) + p.blk_base + 1) * K_STEP;
                             s0[t] += mix64(h0[t] ^ u);
                             s1[t] += mix64(h1[t] + u);
                             h0[t] = h1[t] = 0;
@@ -380,7 +381,7 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
                     if (!Ring<W>::CHUNK_FOLD) {  // per-word block boundary check (rows straddle hash blocks)
                         const u64 k1 = kb + w + 1;
                         if ((k1 & 63) == 0 || k1 == (u64)n) {
-                            if (((k1 - 1) >> 6) == 0) {
+                            if (((k1 - 1) >> 6) + p.blk_base == 0) {
                                 s0[t] += h0[t];
                                 s1[t] += h1[t];
                             } else {
@@ -498,7 +499,7 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
     for (int t = 0; t < TI; t++) {
         u64 c;
         if (!slot_rank(t, &c)) continue;
-        if (p.nsplit > 1) {
+        if (p.nsplit > 1 || p.defer) {
             atomicAdd(p.acc_s0 + c, s0[t]);
             atomicAdd(p.acc_s1 + c, s1[t]);
             if (err[t]) atomicAdd(p.acc_err + c, err[t]);
@@ -755,7 +756,7 @@ struct NotFold {
             h0 = mad_wide(xl + (u32)key0, xh + (u32)(key0 >> 32), h0);
             h1 = mad_wide(xl + (u32)key1, xh + (u32)(key1 >> 32), h1);
         } else {
-            const u64 mm = mix64(v ^ ((u64)(k + 1) * K_STEP));
+            const u64 mm = mix64(v ^ ((u64)(k + 1) * K_STEP));  // k: global word index
             h0 = (h0 ^ mm) * K_FOLD0;
             h1 = (h1 ^ ((mm << 32) | (mm >> 32))) * K_FOLD1;
         }
@@ -783,6 +784,7 @@ __device__ __forceinline__ void mat_rows_not(const MaterializeParams& p, const b
     u64* __restrict__ po = p.cms + cm_index(dst, n, 0);
     const u64* __restrict__ pm = p.masks;
     const int R = p.R, n_pos = p.n_pos;
+    const u32 kbase = p.blk_base * 64u;
     auto row = [&](const int r, const u32 pk) {
         u64 x[1], y[1], m[1], out[1];
         x[0] = ld_nc(px + (size_t)r * 32);
@@ -790,7 +792,7 @@ __device__ __forceinline__ void mat_rows_not(const MaterializeParams& p, const b
         m[0] = ld_nc(pm + r);
         apply_row<OP, 1>(out, x, y, m);
         po[(size_t)r * 32] = out[0];
-        f.word(~out[0] & m[0], (u32)r, pk, r < n_pos);
+        f.word(~out[0] & m[0], kbase + (u32)r, pk, r < n_pos);
     };
     constexpr int UNROLL = LTL_MATF_UNROLL;
     for (int rb = 0; rb < R; rb += 64) {
@@ -801,7 +803,7 @@ __device__ __forceinline__ void mat_rows_not(const MaterializeParams& p, const b
         } else {
             for (int i = 0; rb + i < R; i++) row(rb + i, (u32)i);
         }
-        f.end_block((u32)rb >> 6);
+        f.end_block(((u32)rb >> 6) + p.blk_base);
     }
 }
 
@@ -839,7 +841,7 @@ __global__ void __launch_bounds__(LTL_CTA, LTL_MATF_MINB) k_materialize_not(cons
     }
     if (valid) {  // file NOT(dst) as candidate not_cbase + (dst - not_i0) of the pass in flight
         const u64 c = (u64)p.not_cbase + (u64)(dst - p.not_i0);
-        if (sp.nsplit > 1) {  // the pass combines row splits: hand the (complete) sums to k_finalize
+        if (sp.nsplit > 1 || sp.defer) {  // the pass combines row splits (or GPUs): hand the sums to k_finalize
             atomicAdd(sp.acc_s0 + c, f.s0);
             atomicAdd(sp.acc_s1 + c, f.s1);
             if (f.err) atomicAdd(sp.acc_err + c, f.err);

@@ -94,6 +94,15 @@ class TorchComm:
         self.dist.all_gather_into_tensor(out, padded.contiguous(), group=self.group)
         return torch.cat([out[r * width: r * width + sizes[r]] for r in range(self.world)], 0)
 
+    def all_reduce_sum(self, tensors):
+        """In-place wrapping integer sums over the ranks; returns once the results are visible to the device."""
+        import torch
+
+        for t in tensors:
+            self.dist.all_reduce(t, op=self.dist.ReduceOp.SUM, group=self.group)
+        if tensors and tensors[0].is_cuda:
+            torch.cuda.current_stream(tensors[0].device).synchronize()
+
     def barrier(self):
         self.dist.barrier(group=self.group)
 
@@ -145,6 +154,24 @@ class ThreadComm:
 
         return torch.cat([p.to(t.device) for p in self._exchange(t)], 0)
 
+    def all_reduce_sum(self, tensors):
+        import torch
+
+        everything = self._exchange(tensors)  # every rank sees every rank's tensors (same device or CPU)
+        totals = []
+        for k, mine in enumerate(tensors):
+            acc = torch.zeros_like(mine)
+            for r in range(self.world):
+                acc += everything[r][k].to(mine.device)
+            totals.append(acc)
+        if tensors and tensors[0].is_cuda:
+            torch.cuda.synchronize()
+        self._s.barrier.wait()  # nobody overwrites an input another rank is still reading
+        for mine, acc in zip(tensors, totals):
+            mine.copy_(acc)
+        if tensors and tensors[0].is_cuda:
+            torch.cuda.synchronize()
+
     def barrier(self):
         self._s.barrier.wait()
 
@@ -165,6 +192,21 @@ class ShardedCore:
 
     def __init__(self, local, comm):
         self.local, self.comm = local, comm
+        self.stage_ms = {} if os.environ.get("LTL_SHARDED_TIMERS") else None  # per-stage wall time (device-synchronised)
+
+    def _tick(self, name, t0):
+        """Profiling aid (LTL_SHARDED_TIMERS=1): synchronise the device and add the time since t0 to `name`."""
+        import time
+
+        if self.stage_ms is None:
+            return 0.0
+        import torch
+
+        if torch.cuda.is_available():
+            torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        self.stage_ms[name] = self.stage_ms.get(name, 0.0) + 1e3 * (t1 - t0)
+        return t1
 
     # replicated single-matrix calls: every rank performs the same call on its replica
     def add_entry(self, cm, op, lhs, rhs):
@@ -213,25 +255,37 @@ class ShardedCore:
         lo, hi = total * g // G, total * (g + 1) // G
 
         # 1-2: evaluate the slice, agree on the first solver
+        import time
+
+        tk = time.perf_counter() if self.stage_ms is not None else 0.0
         fp, solver_local = local.stage_eval(segments, lo, hi)
+        tk = self._tick("eval", tk)
         dev = fp.device
         solver = comm.all_reduce_min(solver_local if solver_local >= 0 else _INF, device=dev)
         limit = min(total, solver)
         keep = max(0, min(hi, limit) - lo)
         fp = fp[:keep]
+        tk = self._tick("solver_allreduce", tk)
 
         # 3: route to hash owners, file, route the verdicts back
         owner = owner_of(fp, G)
-        order = torch.argsort(owner, stable=True)
-        counts = torch.bincount(owner, minlength=G).tolist()
+        # stable grouping by destination: one radix pass over byte keys (G <= 255 ranks on a box)
+        order = torch.sort(owner.to(torch.uint8), stable=True)[1] if G > 1 else torch.arange(keep, device=dev)
+        # per-destination counts: G compare-and-sum passes (bincount funnels 10^7 atomics into G addresses)
+        counts = torch.stack([(owner == d).sum() for d in range(G)]).tolist() if keep else [0] * G
         ranks_global = gbase + lo + torch.arange(keep, dtype=torch.int64, device=dev)
         send = torch.cat([fp[order], ranks_global[order].unsqueeze(1)], 1).contiguous()
+        tk = self._tick("route_sort", tk)
         recv, recv_counts = comm.all_to_all(send, counts)
+        tk = self._tick("all_to_all", tk)
         win_recv = local.stage_file(recv)
+        tk = self._tick("file", tk)
         win_sorted, _ = comm.all_to_all(win_recv, recv_counts)
+        tk = self._tick("all_to_all_back", tk)
         win = torch.zeros(keep, dtype=torch.uint8, device=dev)
         win[order] = win_sorted
         winners = lo + torch.nonzero(win, as_tuple=False).flatten()  # ascending level ranks
+        tk = self._tick("winners", tk)
 
         # 4: global numbering in rank order, budget cut
         n_local = int(winners.shape[0])
@@ -245,8 +299,10 @@ class ShardedCore:
             oom_rank = comm.all_reduce_min(mine, device=dev)
             winners = winners[: max(0, min(n_local, room - base))]
         op, lhs, rhs = local.stage_decode(segments, winners)
+        tk = self._tick("decode", tk)
         packed = torch.stack([op.to(torch.int32), lhs, rhs], 1)
         packed = comm.all_gather_cat(packed)
+        tk = self._tick("all_gather", tk)
         count = min(total_w, room)
         assert packed.shape[0] == count, (packed.shape, count)
 
@@ -262,6 +318,7 @@ class ShardedCore:
             offered_delta, dup_delta = total, total - count
         local.stage_append(packed[:, 0].to(torch.uint8), packed[:, 1].contiguous(), packed[:, 2].contiguous(),
                            offered_delta, dup_delta)
+        tk = self._tick("append", tk)
         if status == S_DONE:
             return S_DONE, -1, -1, -1
         local.stage_purge(gbase + cut)
@@ -269,6 +326,122 @@ class ShardedCore:
             return S_OOM, -1, -1, -1
         sop, sl, sr = local.stage_decode(segments, torch.tensor([solver], dtype=torch.int64, device=dev))
         return S_SOLVED, self._segment_of(segments, solver), int(sl.item()), int(sr.item())
+
+
+# ------------------------------------------------------------------------------------------------ row shards
+
+
+def row_slices(n_rows: int, words_per_row: int, world: int):
+    """Row range of every shard: equal slices whose word offsets are multiples of 64 (fingerprint blocks must not
+    straddle shards); trailing shards may be short or -- if there are too few rows -- empty (then: ValueError)."""
+    import math
+
+    unit = 64 // math.gcd(64, words_per_row)  # rows per whole number of 64-word blocks
+    per = -(-n_rows // world)
+    per = -(-per // unit) * unit
+    out = [(min(n_rows, g * per), min(n_rows, (g + 1) * per)) for g in range(world)]
+    if any(a == b for a, b in out):
+        raise ValueError(f"{n_rows} rows x {words_per_row} words cannot be cut into {world} shards of whole 64-word blocks")
+    return out
+
+
+class RowShardedCore:
+    """The screening-core contract over G GPUs that each hold a slice of the ROWS of every characteristic matrix
+    (the alternative for many-row specifications; `include/ltl_core.h: ltl_core_set_row_shard`).
+
+    Every rank enumerates every candidate on its rows (1/G of the words), the per-candidate partial fingerprint sums
+    and error counts are all-reduced (20 bytes per candidate over NVLink), and every rank then takes identical
+    decisions: same winners, same entry order, same records and counters as one core over all rows.  Unlike the
+    candidate-sharded core the entry store is partitioned, not replicated: G GPUs hold G times the language cache,
+    and phase B (writing the new matrices) scales with G as well."""
+
+    def __init__(self, local, comm, r0: int, r1: int, n_rows: int, words_per_row: int):
+        self.local, self.comm = local, comm
+        self.r0, self.r1, self.n_rows, self.W = r0, r1, n_rows, words_per_row
+        self.stage_ms = None
+
+    def _mine(self, cm):
+        a = np.ascontiguousarray(cm, dtype=np.uint64).reshape(-1)
+        if len(a) != self.n_rows * self.W:
+            raise ValueError(f"expected {self.n_rows * self.W} words, got {len(a)}")
+        return a[self.r0 * self.W: self.r1 * self.W]
+
+    def _gather_rows(self, local_rows):
+        import torch
+
+        t = torch.from_numpy(np.ascontiguousarray(local_rows).view(np.int64).reshape(-1))
+        dev = self.comm._dev() if hasattr(self.comm, "_dev") else t.device
+        out = self.comm.all_gather_cat(t.to(dev))
+        return out.cpu().numpy().view(np.uint64)
+
+    # collective calls: every rank makes the same call at the same time
+    def add_entry(self, cm, op, lhs, rhs):
+        return self.local.add_entry(self._mine(cm), op, lhs, rhs)
+
+    def run_level(self, segments):
+        return self.local.run_level(segments)
+
+    def screen_unary(self, op, c0, c1):
+        return self.local.screen_unary(op, c0, c1)
+
+    def screen_binary(self, op, a0, a1, b0, b1, tri):
+        return self.local.screen_binary(op, a0, a1, b0, b1, tri)
+
+    def contains(self, cm):
+        return self.local.contains(self._mine(cm))
+
+    def fingerprint_of(self, cm):
+        return self.local.fingerprint_of(self._mine(cm))
+
+    def get_cm(self, idx):
+        return self._gather_rows(self.local.get_cm(idx))
+
+    # replicated state
+    def get_record(self, idx):
+        return self.local.get_record(idx)
+
+    def counters(self):
+        return self.local.counters()
+
+    n_entries = property(lambda s: s.local.counters()[0])
+
+    def set_option(self, name, value):
+        self.local.set_option(name, value)
+
+    def transfer_stats(self):
+        return self.local.transfer_stats()
+
+    def kernel_stats(self):
+        return self.local.kernel_stats()
+
+    def level_size(self, segments):
+        return self.local.level_size(segments)
+
+    def close(self):
+        self.local.close()
+
+
+def row_sharded_core_factory(comm, **options):
+    """A `core_factory` for `learner.Enumeration` / `learn`: this rank's `CudaCore` over its slice of the rows."""
+
+    def make(masks, n_pos, err_max, variant, proj_rows, proj_offs, fkp_bits, mask_k, budget_bytes, *,
+             words_per_row=1, device=0):
+        from .core import make_core
+
+        W = int(words_per_row)
+        m = np.ascontiguousarray(masks, dtype=np.uint64).reshape(-1)
+        n_rows = len(m) // W
+        r0, r1 = row_slices(n_rows, W, comm.world)[comm.rank]
+        local = make_core(m[r0 * W: r1 * W], max(0, min(int(n_pos), r1) - r0), err_max, variant, proj_rows, proj_offs,
+                          fkp_bits, mask_k, budget_bytes, words_per_row=W, device=device, **options)
+        local.set_row_shard(r0 * W, n_rows * W, comm.all_reduce_sum)
+        # A solver is only known after the exchange, so a pass cannot stop early inside a chunk: keep chunks at 2^22
+        # candidates (the search stops after the first chunk that holds a solver; the level it ends in is the largest)
+        if "chunk_candidates" not in options:
+            local.set_option("chunk_candidates", 1 << 22)
+        return RowShardedCore(local, comm, r0, r1, n_rows, W)
+
+    return make
 
 
 def sharded_core_factory(comm, local_factory: Callable | None = None, **options):
@@ -311,8 +484,17 @@ def bench_main(args, spec, alphabet, planted, cfg_desc):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     comm = TorchComm()
     max_cost = cfg_desc["max_cost"]
-    lcfg = LearnerConfig(ceiling=max_cost + 1, budget_bytes=int(args.budget_gb * (1 << 30)), device=local_rank)
-    factory = sharded_core_factory(comm, profile=True)
+    lcfg = LearnerConfig(ceiling=max_cost + 1, budget_bytes=int(args.budget_gb * (1 << 30)), device=local_rank,
+                         pack_on_device=True)
+    mode = getattr(args, "sharding", "auto")
+    if mode == "auto":
+        try:
+            row_slices(spec.size, -(-spec.max_len // 64), comm.world)
+            mode = "rows"
+        except ValueError:
+            mode = "candidates"
+    make = row_sharded_core_factory if mode == "rows" else sharded_core_factory
+    factory = make(comm, profile=True)
 
     def search():
         en = Enumeration(spec, alphabet, lcfg, core_factory=factory)
@@ -342,21 +524,53 @@ def bench_main(args, spec, alphabet, planted, cfg_desc):
         torch.cuda.synchronize()
         dev_ms += ev0.elapsed_time(ev1)
         launches += sum(v["launches"] for v in en.core.local.kernel_stats().values())
+        if getattr(en.core, "stage_ms", None) is not None and comm.rank == 0:
+            import sys
+
+            print("stage ms:", {k: round(v, 2) for k, v in en.core.stage_ms.items()},
+                  {k: round(v["ms"], 2) for k, v in en.core.local.kernel_stats().items() if v["launches"]}, file=sys.stderr)
         en.core.close()
-    t = torch.tensor([dev_ms], dtype=torch.float64, device="cuda")
+    # end to end: host trace arrays in (every rank packs and uploads its replica), formula text out
+    from .traces import Specification
+
+    pos_c, pos_l = spec.chars[: spec.n_pos].copy(), spec.lengths[: spec.n_pos].copy()
+    neg_c, neg_l = spec.chars[spec.n_pos:].copy(), spec.lengths[spec.n_pos:].copy()
+    e2e_factory = make(comm)
+
+    def e2e_once():
+        s = Specification.from_arrays(pos_c, pos_l, neg_c, neg_l)
+        out = Enumeration(s, alphabet, lcfg, core_factory=e2e_factory).run()
+        assert isinstance(out, Solved) and print_formula(out.formula, alphabet) == text
+        return out
+
+    e2e_once()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    comm.barrier()
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(args.steps):
+        out = e2e_once()
+    e1.record()
+    comm.barrier()
+    torch.cuda.synchronize()
+    t = torch.tensor([dev_ms, e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms = float(t.item())
+    total_ms, e2e_ms = float(t[0].item()), float(t[1].item())
     if comm.rank == 0:
         value = offered * args.steps / (total_ms / 1e3)
-        cfg_desc = dict(cfg_desc, parallelism=f"candidate ranges sharded over {comm.world} GPUs, hash-owner all-to-all")
+        cfg_desc = dict(cfg_desc, parallelism=(
+            f"rows sharded over {comm.world} GPUs ({spec.size // comm.world} rows each), per-candidate partial fingerprints "
+            f"all-reduced, entry store partitioned" if mode == "rows" else
+            f"candidate ranges sharded over {comm.world} GPUs, hash-owner all-to-all, entry store replicated"))
         print(json.dumps({
             "metric": "candidates_per_sec", "value": value, "unit": "candidates/s", "n_gpus": comm.world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
             "config": cfg_desc, "gpu_launches": launches, "formula": text, "cost": res.cost,
-            "e2e": {"value": value, "unit": "candidates/s", "h2d_bytes_per_step": res.stats.h2d_bytes,
-                    "d2h_bytes_per_step": res.stats.d2h_bytes,
-                    "note": "sharded run: atoms are uploaded by every rank inside the step"},
+            "e2e": {"value": offered * args.steps / (e2e_ms / 1e3), "unit": "candidates/s",
+                    "ms_per_step": e2e_ms / args.steps, "h2d_bytes_per_step": out.stats.h2d_bytes,
+                    "d2h_bytes_per_step": out.stats.d2h_bytes,
+                    "note": "host trace arrays -> device packing -> sharded search -> formula text, per rank bytes"},
             "candidates_per_step": offered, "unique_cs_per_step": res.stats.admitted,
         }))
     dist.barrier()
