@@ -17,6 +17,9 @@ same replicated entry store and counters; the uniqueness table is sharded by fin
      receiving 7/8 of the delta at <= 0.9 TB/s);
   5. every rank appends the same records and advances the same counters (`stage_append`).
 
+`RowShardedCore` (further down) is the second sharding: every GPU holds a slice of the ROWS of every matrix, the
+per-candidate partial fingerprint sums are all-reduced, the store is partitioned instead of replicated.
+
 Results (entry order, records, counters, statuses, formula text) are identical to the 1-GPU path and to the
 CPU oracle; `tests/test_sharded_*.py` check that with G virtual ranks on threads (1 GPU) and with gloo
 processes over a CPU stand-in for the stages.
