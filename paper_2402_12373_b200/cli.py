@@ -3,6 +3,7 @@
     python -m paper_2402_12373_b200.cli learn TRACE_FILE [--max-cost N] [--hash mueller|fkp|mueller_blocked|nh] [--mask-bits K]
         [--nnf] [--no-until] [--noise EPS] [--budget BYTES] [--costs a,n,c,d,x,f,g,u] [--timeout SECS]
         [--device D] [--json PATH] [--verify] [--dnc --window N --strategy det|rand --seed S --min-window M]
+    torchrun --nproc-per-node G -m paper_2402_12373_b200.cli learn TRACE_FILE ... [--sharding auto|rows|candidates]
 
 Reads a trace file (format `traces.py`, reference `traces.py:180-253`), runs the enumerative learner on the
 B200 core and writes the JSON report of `SPEC.md:158`: {formula, cost, wall_ms, mode, hash, stats}.  Only the
@@ -14,6 +15,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import os
 import sys
 import time
 
@@ -38,10 +40,14 @@ def cmd_learn(args) -> int:
     if args.dnc:
         return _learn_dnc(args, spec, alphabet, costs, report, t0)
     try:
+        core_factory, device, rank = _distributed_factory(args, spec)
+        report["config"]["gpus"] = int(os.environ.get("WORLD_SIZE", "1"))
         res = learn(spec, None, alphabet, max_cost=args.max_cost, costs=costs, require_nnf=args.nnf,
                     forbid_until=args.no_until, noise=args.noise,
                     hash=HashScheme(args.hash, args.mask_bits), budget_bytes=args.budget, deadline_s=args.timeout,
-                    device=args.device)
+                    device=device, **({} if core_factory is None else {"core_factory": core_factory}))
+        if rank != 0:  # every rank holds the same result; rank 0 reports it
+            return 0 if res.status in ("solved", "ceiling") else 1
     except BackendUnavailable as exc:
         print(f"error: {exc}", file=sys.stderr)
         return 3
@@ -66,6 +72,36 @@ def cmd_learn(args) -> int:
             rc = 5
     _emit(report, args)
     return rc
+
+
+def _distributed_factory(args, spec):
+    """Under torchrun (WORLD_SIZE > 1): one process per GPU, the search sharded over them (`sharded.py`).
+    Returns (core_factory or None, device index, rank)."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world <= 1 and not os.environ.get("LTL_FORCE_SHARDED"):  # the env switch: NCCL path on one GPU (tests)
+        return None, args.device, 0
+    import torch
+    import torch.distributed as dist
+
+    from . import sharded
+
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local_rank)
+    if not dist.is_initialized():
+        import atexit
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        atexit.register(lambda: dist.is_initialized() and dist.destroy_process_group())
+    comm = sharded.TorchComm()
+    mode = args.sharding
+    if mode == "auto":
+        try:
+            sharded.row_slices(spec.size, -(-spec.max_len // 64), world)
+            mode = "rows"
+        except ValueError:
+            mode = "candidates"
+    make = sharded.row_sharded_core_factory if mode == "rows" else sharded.sharded_core_factory
+    return make(comm), local_rank, comm.rank
 
 
 def _learn_dnc(args, spec, alphabet, costs, report, t0) -> int:
@@ -135,6 +171,8 @@ def main(argv=None) -> int:
     lp.add_argument("--costs", default=None, help="8 weights: atom,not,and,or,next,finally,globally,until")
     lp.add_argument("--timeout", type=float, default=None)
     lp.add_argument("--device", type=int, default=0)
+    lp.add_argument("--sharding", choices=["auto", "rows", "candidates"], default="auto",
+                    help="under torchrun with several GPUs: row shards or candidate ranges (DESIGN.md section 8)")
     lp.add_argument("--json", default=None, help="write the report here instead of stdout")
     lp.add_argument("--verify", action="store_true", help="re-evaluate the learned formula on the input")
     lp.add_argument("--dnc", action="store_true", help="divide and conquer over windows of --window traces")

@@ -181,3 +181,30 @@ def test_row_sharded_matrices_and_membership():
     for got in out:
         assert got == want
     ref.close()
+
+
+@pytest.mark.parametrize("sharding", ["rows", "candidates"])
+def test_cli_learn_under_torchrun(tmp_path, sharding):
+    """`torchrun -m paper_2402_12373_b200.cli learn` (one process per GPU): process group of size 1 forced through the
+    sharded cores; the report is the single-core one."""
+    import json
+    import os
+    import subprocess
+    import sys
+
+    from paper_2402_12373_b200 import workloads as Wl
+    from paper_2402_12373_b200.traces import save_spec
+
+    spec, al, _, _ = Wl.make_config("c1_tiny")
+    path, out = tmp_path / "c1.trace", tmp_path / "report.json"
+    save_spec(spec, path, al)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, LTL_FORCE_SHARDED="1", PYTHONPATH=root)
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1", "--master-addr", "127.0.0.1",
+           "--master-port", "29547", "-m", "paper_2402_12373_b200.cli", "learn", str(path), "--max-cost", "10", "--json",
+           str(out), "--verify", "--sharding", sharding]
+    res = subprocess.run(cmd, cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    assert res.returncode == 0, res.stderr[-3000:]
+    rep = json.loads(out.read_text())
+    assert rep["status"] == "solved" and rep["formula"] == "F G p0 & (p0 U p1)" and rep["cost"] == 7
+    assert rep["verified_errors"] == 0 and rep["stats"]["offered"] == 5762
