@@ -424,19 +424,22 @@ class RowShardedCore:
         self.local.close()
 
 
-def row_sharded_core_factory(comm, **options):
-    """A `core_factory` for `learner.Enumeration` / `learn`: this rank's `CudaCore` over its slice of the rows."""
+def row_sharded_core_factory(comm, local_factory: Callable | None = None, **options):
+    """A `core_factory` for `learner.Enumeration` / `learn`: this rank's `CudaCore` over its slice of the rows
+    (``local_factory``: a CPU stand-in with the same `set_row_shard` contract, for the gloo tests)."""
 
     def make(masks, n_pos, err_max, variant, proj_rows, proj_offs, fkp_bits, mask_k, budget_bytes, *,
              words_per_row=1, device=0):
-        from .core import make_core
-
         W = int(words_per_row)
         m = np.ascontiguousarray(masks, dtype=np.uint64).reshape(-1)
         n_rows = len(m) // W
         r0, r1 = row_slices(n_rows, W, comm.world)[comm.rank]
-        local = make_core(m[r0 * W: r1 * W], max(0, min(int(n_pos), r1) - r0), err_max, variant, proj_rows, proj_offs,
-                          fkp_bits, mask_k, budget_bytes, words_per_row=W, device=device, **options)
+        if local_factory is None:
+            from .core import make_core as factory
+        else:
+            factory = local_factory
+        local = factory(m[r0 * W: r1 * W], max(0, min(int(n_pos), r1) - r0), err_max, variant, proj_rows, proj_offs,
+                        fkp_bits, mask_k, budget_bytes, words_per_row=W, device=device, **options)
         local.set_row_shard(r0 * W, n_rows * W, comm.all_reduce_sum)
         # A solver is only known after the exchange, so a pass cannot stop early inside a chunk: keep chunks at 2^22
         # candidates (the search stops after the first chunk that holds a solver; the level it ends in is the largest)

@@ -160,3 +160,88 @@ class OracleStageCore:
 
     def stage_purge(self, cut):
         self.table = {k: v for k, v in self.table.items() if v < cut}
+
+
+class OracleRowShard:
+    """TEST INFRASTRUCTURE: CPU stand-in for one ROW SHARD of `CudaCore` (`set_row_shard`), on the CPU oracle's
+    operator / error / fingerprint functions over this shard's rows.  Per candidate it contributes the fingerprint
+    and the error count of its rows; the sums over the shards (the exchange) decide admission, identically on every
+    rank.  (The sum of the shards' local fingerprints is not the device's value -- the device sums per 64-word block
+    -- but admission only needs a collision-free function of all rows.)"""
+
+    def __init__(self, masks, n_pos, err_max, variant, proj_rows=(), proj_offs=(), fkp_bits=0, mask_k=0,
+                 budget_bytes=2 << 30, *, words_per_row=1, device=None):
+        self.o = cpu_oracle.OracleCore(masks, n_pos, 0, variant, proj_rows, proj_offs, fkp_bits, mask_k, 1 << 60,
+                                       words_per_row=words_per_row)
+        self.err_max, self.budget = err_max, int(budget_bytes)
+        self.cms, self.records, self.table = [], [], set()
+        self.offered = self.admitted = self.duplicates = 0
+        self.exchange, self.entry_bytes = None, 8 * self.o.n + 16
+
+    def set_row_shard(self, word_base, total_words, all_reduce_sum):
+        assert word_base % 64 == 0
+        self.exchange, self.entry_bytes = all_reduce_sum, 8 * int(total_words) + 16
+
+    def set_option(self, name, value):
+        pass
+
+    def close(self):
+        pass
+
+    def _sums(self, cms):
+        fps = [self.o.fingerprint_of(cm) for cm in cms]
+        s0 = torch.tensor([_i64(f >> 64) for f in fps], dtype=torch.int64)
+        s1 = torch.tensor([_i64(f) for f in fps], dtype=torch.int64)
+        err = torch.tensor([self.o.errors(cm) for cm in cms], dtype=torch.int32)
+        self.exchange([s0, s1, err])
+        return s0.tolist(), s1.tolist(), err.tolist()
+
+    def _offer(self, cm, key, record):
+        """First-wins admission (reference _speedups.pyx:245-262): index, -1 duplicate, -3 over budget."""
+        self.offered += 1
+        if key in self.table:
+            self.duplicates += 1
+            return -1
+        if self.admitted * self.entry_bytes + self.entry_bytes > self.budget:
+            return -3
+        self.table.add(key)
+        self.cms.append(cm)
+        self.records.append(record)
+        self.admitted += 1
+        return self.admitted - 1
+
+    def add_entry(self, cm, op, lhs, rhs):
+        cm = np.ascontiguousarray(cm, dtype=np.uint64)
+        s0, s1, _ = self._sums([cm])
+        idx = self._offer(cm, (s0[0], s1[0]), (op, lhs, rhs))
+        if idx == -3:
+            raise E.CoreOOM
+        return idx
+
+    def _eval(self, op, i, j):
+        return self.o.apply_unary(op, self.cms[i]) if j < 0 else self.o.apply_binary(op, self.cms[i], self.cms[j])
+
+    def run_level(self, segments):
+        segments = list(segments)
+        cands = [(k, c) for k, s in enumerate(segments) for c in seg_candidates(s)]
+        cms = [self._eval(op, i, j) for _, (op, i, j) in cands]
+        s0, s1, err = self._sums(cms) if cands else ([], [], [])
+        for n, (k, (op, i, j)) in enumerate(cands):
+            if err[n] <= self.err_max:
+                self.offered += 1  # the solving candidate is offered, never admitted (reference _speedups.pyx:347-350)
+                return 1, k, i, j
+            if self._offer(cms[n], (s0[n], s1[n]), (op, i, j)) == -3:
+                return 2, -1, -1, -1
+        return 0, -1, -1, -1
+
+    def get_record(self, idx):
+        return self.records[idx]
+
+    def get_cm(self, idx):
+        return self.cms[idx].copy()
+
+    def counters(self):
+        return [self.admitted, self.admitted * self.entry_bytes, self.offered, self.admitted, self.duplicates]
+
+    def transfer_stats(self):
+        return 0, 0

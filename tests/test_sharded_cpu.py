@@ -221,3 +221,68 @@ def test_row_sharded_wrapper_world2_gloo():
         assert p.exitcode == 0
     assert sorted(r for r, _, _ in results) == [0, 1]
     assert all((b, s) == _expected_sums(2) for _, b, s in results)
+
+
+# ------------------------------------------------------------------------------------------------ row shards (whole searches)
+
+ROW_CASES = [
+    dict(seed=41, n_props=2, n_pos=100, n_neg=70, lo=5, hi=40, kw=dict(max_cost=6)),                     # solved or ceiling
+    dict(seed=42, n_props=2, n_pos=30, n_neg=110, lo=70, hi=130, kw=dict(max_cost=5)),                   # 3 words per row
+    dict(seed=43, n_props=2, n_pos=90, n_neg=90, lo=10, hi=64, kw=dict(max_cost=6, budget_bytes=150 * (180 * 8 + 16) + 1)),
+    dict(seed=44, n_props=3, n_pos=64, n_neg=64, lo=3, hi=20, kw=dict(max_cost=6, noise=0.1)),           # errors summed
+    dict(seed=45, n_props=2, n_pos=80, n_neg=80, lo=6, hi=30, kw=dict(max_cost=8), planted="F(p0 & X p1)"),  # solved
+    dict(seed=46, n_props=2, n_pos=70, n_neg=90, lo=6, hi=30, kw=dict(max_cost=8, noise=0.3), planted="G(p0 | X p1)"),
+]
+
+
+def _row_case_spec(case):
+    if "planted" in case:
+        from paper_2402_12373_b200 import workloads as Wl
+
+        spec, alphabet, _ = Wl.planted_spec(case["n_props"], case["n_pos"], case["n_neg"], case["lo"], case["hi"],
+                                            case["planted"], case["seed"])
+        return spec, alphabet
+    return random_spec(np.random.default_rng(case["seed"]), case["n_props"], case["n_pos"], case["n_neg"], case["lo"],
+                       case["hi"])
+
+
+def _row_sharded(case, comm):
+    from paper_2402_12373_b200.sharded import row_sharded_core_factory
+    from stage_oracle import OracleRowShard
+
+    spec, alphabet = _row_case_spec(case)
+    factory = row_sharded_core_factory(comm, local_factory=OracleRowShard)
+    return _summary(L.learn(spec, None, alphabet, core_factory=factory, **case["kw"]))
+
+
+def _gloo_rows_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        comm = TorchComm()
+        out.put((rank, [_row_sharded(case, comm) for case in ROW_CASES]))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_sharded_learn_world2_gloo():
+    """Whole searches over two row shards (gloo processes, CPU stand-in shards): the exchange of per-candidate sums
+    and the replicated admission reproduce the single oracle core -- formula, counters, per-level rows."""
+    want = []
+    for case in ROW_CASES:
+        spec, alphabet = _row_case_spec(case)
+        want.append(_summary(L.learn(spec, None, alphabet, core_factory=oracle_factory(1), **case["kw"])))
+    ctx = mp.get_context("spawn")
+    out = ctx.Queue()
+    port = 33500 + os.getpid() % 2000
+    procs = [ctx.Process(target=_gloo_rows_worker, args=(r, 2, port, out)) for r in range(2)]
+    for p in procs:
+        p.start()
+    results = dict(out.get(timeout=900) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert any(w[0] == "oom" for w in want) and any(w[0] == "solved" for w in want)
+    for rank in (0, 1):
+        assert results[rank] == want, f"rank {rank}"
