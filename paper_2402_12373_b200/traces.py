@@ -99,6 +99,59 @@ def _first_occurrences(keys: np.ndarray) -> np.ndarray:
     return np.sort(first)
 
 
+def _row_hashes(chars: np.ndarray, lengths: np.ndarray, width: int) -> np.ndarray:
+    """64-bit hash of (length, padded characters) per trace, vectorised over the rows (a multilinear form over the
+    row's 64-bit words, one pass).  Equal traces have equal hashes; unequal hashes prove traces different, so the
+    exact (and slow: byte-string sort) comparison is only needed for the rare rows that share a hash."""
+    R = len(lengths)
+    if chars.shape[1] % 4 == 0 and chars.flags.c_contiguous and chars.dtype == np.uint16:
+        words = chars.view(np.uint64)  # (R, width / 4), no copy
+    else:
+        cols = -(-max(chars.shape[1], 1) // 4) * 4
+        key = np.zeros((R, cols), dtype=np.uint16)
+        key[:, : chars.shape[1]] = chars
+        words = key.view(np.uint64)
+    k = np.arange(1, words.shape[1] + 1, dtype=np.uint64)
+    consts = (k * np.uint64(0x9E3779B97F4A7C15) + np.uint64(0x632BE59BD9B4E019)) | np.uint64(1)
+    h = words @ consts + lengths.astype(np.uint64) * np.uint64(0xD6E8FEB86659FD93)  # wraps mod 2^64
+    h ^= h >> np.uint64(32)
+    h *= np.uint64(0xBF58476D1CE4E5B9)
+    h ^= h >> np.uint64(29)
+    return h
+
+
+def _member(a: np.ndarray, b: np.ndarray) -> np.ndarray:
+    """a[i] in b, for uint64 hashes (sorted needles into a sorted haystack: np.isin is 10x slower on 10^6 keys)."""
+    if len(b) == 0 or len(a) == 0:
+        return np.zeros(len(a), dtype=bool)
+    bs = np.sort(b)
+    if len(b) > 4096:  # big haystack: walk it in order, then spread the few common values back
+        a_s = np.sort(a)
+        idx = np.minimum(np.searchsorted(bs, a_s), len(bs) - 1)
+        common = np.unique(a_s[bs[idx] == a_s])
+        if len(common) == 0:
+            return np.zeros(len(a), dtype=bool)
+        bs = common
+    idx = np.minimum(np.searchsorted(bs, a), len(bs) - 1)
+    return bs[idx] == a
+
+
+def _dedup_first(chars: np.ndarray, lengths: np.ndarray, width: int):
+    """Indices of the first occurrence of every distinct trace, ascending, and the row hashes."""
+    h = _row_hashes(chars, lengths, width)
+    hs = np.sort(h)
+    dup_vals = hs[1:][hs[1:] == hs[:-1]]
+    if len(dup_vals) == 0:
+        return np.arange(len(lengths)), h
+    suspects = np.flatnonzero(_member(h, dup_vals))  # ascending row indices
+    keys = _row_keys(chars[suspects], lengths[suspects], width)
+    first = suspects[_first_occurrences(keys)]
+    drop = np.setdiff1d(suspects, first, assume_unique=True)
+    keep = np.ones(len(lengths), dtype=bool)
+    keep[drop] = False
+    return np.flatnonzero(keep), h
+
+
 class Specification:
     """Disjoint positive / negative trace sets in a fixed, meaningful order (it is the row order
     of every characteristic matrix: positives first)."""
@@ -124,31 +177,36 @@ class Specification:
             raise ValueError("traces longer than 65535 positions are not supported")
 
         def clean(chars, lengths):
+            if len(lengths) and chars.shape[1] == width and int(lengths.min()) >= width:
+                return np.ascontiguousarray(chars, dtype=np.uint16)  # every trace fills its row: nothing to pad
             full = np.zeros((len(lengths), width), dtype=np.uint16)
             if len(lengths):
                 full[:, : chars.shape[1]] = chars
-                full[np.arange(width)[None, :] >= lengths[:, None]] = 0  # canonical padding
+                full *= (np.arange(width)[None, :] < lengths[:, None]).astype(np.uint16)  # canonical zero padding
             return full
 
         pc, nc = clean(pc, pl), clean(nc, nl)
         sides = []
         for name, chars, lengths in (("positive", pc, pl), ("negative", nc, nl)):
             if len(lengths):
-                keys = _row_keys(chars, lengths, width)
-                keep = _first_occurrences(keys)
+                keep, hashes = _dedup_first(chars, lengths, width)
                 if len(keep) != len(lengths):
                     warnings.warn(f"{len(lengths) - len(keep)} duplicate {name} trace(s) dropped", stacklevel=4)
-                chars, lengths, keys = chars[keep], lengths[keep], keys[keep]
+                    chars, lengths, hashes = chars[keep], lengths[keep], hashes[keep]
             else:
-                keys = np.zeros(0, dtype=np.dtype((np.void, 2 * (width + 1))))
-            sides.append((chars, lengths, keys))
-        (pc, pl, pk), (nc, nl, nk) = sides
-        if len(pk) and len(nk):
-            clash = np.isin(pk, nk)
-            if clash.any():
-                i = int(np.argmax(clash))
-                j = int(np.argmax(nk == pk[i]))
-                raise ValueError(f"trace occurs on both sides (positive #{i}, negative #{j})")
+                hashes = np.zeros(0, dtype=np.uint64)
+            sides.append((chars, lengths, hashes))
+        (pc, pl, ph), (nc, nl, nh) = sides
+        if len(ph) and len(nh):
+            maybe = np.flatnonzero(_member(ph, nh))  # equal hashes: compare those few traces exactly
+            if len(maybe):
+                nsus = np.flatnonzero(_member(nh, ph[maybe]))
+                pk, nk = _row_keys(pc[maybe], pl[maybe], width), _row_keys(nc[nsus], nl[nsus], width)
+                clash = np.isin(pk, nk)
+                if clash.any():
+                    i = int(np.argmax(clash))
+                    j = int(nsus[int(np.argmax(nk == pk[i]))])
+                    raise ValueError(f"trace occurs on both sides (positive #{int(maybe[i])}, negative #{j})")
         self.n_pos = len(pl)
         self.n_neg = len(nl)
         self.chars = np.concatenate([pc, nc], axis=0) if (len(pl) + len(nl)) else np.zeros((0, width), np.uint16)

@@ -123,3 +123,38 @@ def test_cli_learn_report(tmp_path, monkeypatch, capsys):
     assert rep["status"] == "solved" and rep["formula"] == "F G p0 & (p0 U p1)" and rep["cost"] == 7
     assert rep["verified_errors"] == 0 and rep["stats"]["offered"] == 5762
     assert cli.main(["learn", str(tmp_path / "missing.trace")]) == 2
+
+
+def test_specification_dedup_matches_naive_on_many_traces():
+    """Hash-accelerated first-occurrence dedup and P/N clash detection (`traces.py`) against the obvious loops."""
+    import warnings
+
+    from paper_2402_12373_b200.traces import Specification
+
+    rng = np.random.default_rng(12)
+    R, L = 6000, 7
+    chars = rng.integers(0, 3, size=(2 * R, L)).astype(np.uint16)   # few distinct values: thousands of duplicates
+    lengths = rng.integers(0, L + 1, size=2 * R)
+    lengths[:R][lengths[:R] == 0] = 1
+    as_tuple = lambda k: tuple(int(c) for c in chars[k, : lengths[k]])  # noqa: E731
+    pos_seen, pos = set(), []
+    for k in range(R):
+        t = as_tuple(k)
+        if t not in pos_seen:
+            pos_seen.add(t)
+            pos.append(t)
+    neg_seen, neg = set(), []
+    for k in range(R, 2 * R):
+        t = as_tuple(k)
+        if t not in neg_seen and t not in pos_seen:  # keep the sides disjoint for the first check
+            neg_seen.add(t)
+            neg.append(t)
+    keep_neg = [k for k in range(R, 2 * R) if as_tuple(k) not in pos_seen]
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        spec = Specification.from_arrays(chars[:R], lengths[:R], chars[keep_neg], lengths[keep_neg])
+    assert spec.pos == tuple(pos) and spec.neg == tuple(neg)
+    with warnings.catch_warnings():
+        warnings.simplefilter("ignore")
+        with pytest.raises(ValueError, match="both sides"):
+            Specification.from_arrays(chars[:R], lengths[:R], chars[R:], lengths[R:])
