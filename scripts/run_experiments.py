@@ -36,11 +36,13 @@ for variant in ("mueller", "fkp"):
     rows = B.run_masking_sweep(spec, al, LearnerConfig(hash=HashScheme(variant)))
     sweeps[variant] = [{k: r.get(k) for k in ("k", "status", "cost", "wall_ms", "offered", "admitted")} for r in rows]
 t1 = time.perf_counter()
-ruc = B.run_ruc_experiment(a.seeds, ext_sizes=tuple(int(v) for v in a.ext.split(",")), base_seed=a.base_seed)
+ruc = B.run_ruc_experiment(a.seeds, ext_sizes=tuple(int(v) for v in a.ext.split(",")), base_seed=a.base_seed,
+                           skip_failed_generations=True)
 t2 = time.perf_counter()
 report = {"masking_sweep": {"formula": a.sweep_formula, "traces_per_side": a.sweep_traces, "lengths": [lo, hi],
                             "rows": sweeps, "wall_s": round(t1 - t0, 3)},
-          "ruc": {"seeds": a.seeds, "summary": ruc["summary"], "runs": len(ruc["rows"]), "wall_s": round(t2 - t1, 3)}}
+          "ruc": {"seeds": a.seeds, "summary": ruc["summary"], "runs": len(ruc["rows"]), "skipped": ruc["skipped"],
+                  "wall_s": round(t2 - t1, 3)}}
 text = json.dumps(report)
 if a.out:
     with open(a.out, "w") as fh:
