@@ -192,7 +192,8 @@ def main():
     if args.gpus > 1 or world > 1 or os.environ.get("LTL_FORCE_SHARDED"):  # the env switch: NCCL path on one GPU (tests)
         from paper_2402_12373_b200 import sharded
 
-        return sharded.bench_main(args, spec, alphabet, planted, cfg_desc)
+        return sharded.bench_main(args, spec, alphabet, planted, cfg_desc, sampler=ClockSampler(local_rank),
+                                  peaks=load_peaks())
 
     torch.cuda.set_device(local_rank)
     budget = int(args.budget_gb * (1 << 30))

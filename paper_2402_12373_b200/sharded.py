@@ -471,7 +471,7 @@ def sharded_core_factory(comm, local_factory: Callable | None = None, **options)
 # ------------------------------------------------------------------------------------------------ bench (N > 1)
 
 
-def bench_main(args, spec, alphabet, planted, cfg_desc):
+def bench_main(args, spec, alphabet, planted, cfg_desc, sampler=None, peaks=None):
     """`bench.py --gpus N` under torchrun: every rank runs the same search, sharded; device time of the K
     level loops, max over ranks; rank 0 prints the JSON line."""
     import json
@@ -518,6 +518,10 @@ def bench_main(args, spec, alphabet, planted, cfg_desc):
     offered = res.stats.offered
     dev_ms = 0.0
     launches = 0
+    kstats = []
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    if sampler is not None and comm.rank == 0:
+        sampler.start()
     for _ in range(args.steps):
         en = search()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -529,13 +533,16 @@ def bench_main(args, spec, alphabet, planted, cfg_desc):
         comm.barrier()
         torch.cuda.synchronize()
         dev_ms += ev0.elapsed_time(ev1)
-        launches += sum(v["launches"] for v in en.core.local.kernel_stats().values())
+        kstats.append(en.core.local.kernel_stats())
+        launches += sum(v["launches"] for v in kstats[-1].values())
+        flush.fill_(1)  # L2 flush between timed iterations
         if getattr(en.core, "stage_ms", None) is not None and comm.rank == 0:
             import sys
 
             print("stage ms:", {k: round(v, 2) for k, v in en.core.stage_ms.items()},
                   {k: round(v["ms"], 2) for k, v in en.core.local.kernel_stats().items() if v["launches"]}, file=sys.stderr)
         en.core.close()
+    clocks = sampler.stop() if sampler is not None and comm.rank == 0 else None
     # end to end: host trace arrays in (every rank packs and uploads its replica), formula text out
     from .traces import Specification
 
@@ -568,7 +575,20 @@ def bench_main(args, spec, alphabet, planted, cfg_desc):
             f"rows sharded over {comm.world} GPUs ({spec.size // comm.world} rows each), per-candidate partial fingerprints "
             f"all-reduced, entry store partitioned" if mode == "rows" else
             f"candidate ranges sharded over {comm.world} GPUs, hash-owner all-to-all, entry store replicated"))
+        # roofline of rank 0's phase-A kernel (its share of the rows / candidates), same definition as at N = 1
+        roofline = None
+        scr_ms = sum(ks["screen"]["ms"] for ks in kstats)
+        if scr_ms > 0:
+            peak, peak_src = peaks if peaks else (6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)")
+            scr_bytes = sum(ks["screen"]["alg_bytes"] for ks in kstats)
+            scr_launch = sum(ks["screen"]["launches"] for ks in kstats)
+            ach = scr_bytes / (scr_ms / 1e3) / 1e9
+            roofline = {"bound": "hbm", "kernel": "k_screen (rank 0)", "achieved": ach, "peak": peak, "unit": "GB/s",
+                        "frac": ach / peak, "traffic": None, "peak_source": peak_src,
+                        "alg_bytes_per_launch": scr_bytes / max(scr_launch, 1), "ms_per_launch": scr_ms / max(scr_launch, 1),
+                        "kernel_ms_by_class": {k: round(sum(ks[k]["ms"] for ks in kstats), 3) for k in kstats[0]}}
         print(json.dumps({
+            "clocks": clocks, "roofline": roofline, "cpu_baseline": None,
             "metric": "candidates_per_sec", "value": value, "unit": "candidates/s", "n_gpus": comm.world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",
