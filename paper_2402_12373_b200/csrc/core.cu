@@ -608,6 +608,7 @@ struct ltl_core : Arena {
     bool fuse_unary = true;
     // row shard (ltl_core_set_row_shard): this core holds rows of every matrix starting at word 64 * blk_base of the
     // whole matrix; partial sums are summed across the shards by `exchange` before candidates are completed
+    u64 pending_purge = ~0ull;  // global rank cut of a solve / OOM whose table sweep has not run yet
     u32 blk_base = 0;
     ltl_exchange_fn exchange = nullptr;
     void* exchange_ctx = nullptr;
@@ -953,10 +954,22 @@ static double screen_bytes(ltl_core* h, const std::vector<Piece>& pieces) {
 
 // fused_not >= 0: index of the piece (ext) whose candidates NOT(entry) are screened by phase B of the pending entries,
 // which this pass therefore issues itself, right before its own phase A launches
+static int apply_purge(ltl_core* h) {
+    if (h->pending_purge == ~0ull) return LTL_OK;
+    {
+        ScopedTimer t(h, LTL_K_PURGE, h->table_cap, (double)h->table_cap * sizeof(Slot));
+        k_purge<<<(unsigned)((h->table_cap + 255) / 256), 256, 0, h->stream>>>(h->table, h->table_cap, h->pending_purge);
+    }
+    CK(cudaGetLastError());
+    h->pending_purge = ~0ull;
+    return LTL_OK;
+}
+
 static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 tiles, int mode, bool check_solve,
                      bool materialize, ChunkOut* out, int fused_not = -1) {
     int rc;
     if (total <= 0) return LTL_OK;
+    if ((rc = apply_purge(h))) return rc;
     if (mode == MODE_INSERT) {
         bool tiled_pending = false;
         for (auto& pm : h->pending_mat) tiled_pending |= pm.tiled;
@@ -1154,9 +1167,9 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     h->admitted += count;
     h->n_entries += count;
     if (out->status != LTL_S_DONE) {
-        ScopedTimer t(h, LTL_K_PURGE, h->table_cap, (double)h->table_cap * sizeof(Slot));
-        k_purge<<<(unsigned)((h->table_cap + 255) / 256), 256, 0, h->stream>>>(h->table, h->table_cap, gbase + out->cut_c);
-        CK(cudaGetLastError());
+        // keys filed at or above the cut are not members.  A search normally ends here, so the sweep over the table
+        // is left to the next call that uses the table (apply_purge), if there is one.
+        h->pending_purge = gbase + out->cut_c;
         h->keys_upper += (u64)total;
     } else {
         h->keys_upper += count;
@@ -2044,6 +2057,7 @@ int ltl_core_stage_file(ltl_core* h, const uint64_t* d_tuples, int64_t count, un
     if (count == 0) return LTL_OK;
     if (!d_tuples || !d_win) return h->fail(LTL_ERR_ARG, "null argument");
     int rc;
+    if ((rc = apply_purge(h))) return rc;
     if ((rc = ensure_table(h, h->keys_upper + (u64)count))) return rc;
     if ((rc = ensure_scratch(h, count))) return rc;
     CK(cudaMemsetAsync(&h->d_ctl->total, 0, sizeof(u64), h->stream));
