@@ -88,3 +88,39 @@ def test_config4_full_size_row_split_properties():
     # operands are ever written, so 4 TB logical fits one GPU here
     planted_res = L.learn(spec, None, alphabet, max_cost=cfg["max_cost"], budget_bytes=4 << 40)
     assert planted_res.status == "solved" and Wl.error_count(planted_res.formula, spec, alphabet) == 0
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_config2_full_size_row_sharded(world):
+    """The bench workload over G row shards (virtual ranks on threads, each a real CudaCore holding 1024 / G rows of
+    every matrix on cuda:0; per-candidate partial sums added through the exchange callback; fused NOT in phase B on
+    every shard): level by level the fixture of the single-core run."""
+    import threading
+
+    from paper_2402_12373_b200.sharded import ThreadComm, row_sharded_core_factory
+
+    with open(os.path.join(ROOT, "tests", "golden", "c2_levels.json")) as fh:
+        want = json.load(fh)
+    spec, alphabet, planted, cfg = Wl.make_config("c2_planted")
+    comms = ThreadComm.group(world)
+    got, errs = [None] * world, []
+
+    def work(r):
+        try:
+            got[r] = L.learn(spec, None, alphabet, max_cost=cfg["max_cost"], budget_bytes=150 << 30,
+                             core_factory=row_sharded_core_factory(comms[r]))
+        except BaseException as exc:  # noqa: BLE001
+            errs.append(exc)
+            comms[r]._s.barrier.abort()
+
+    threads = [threading.Thread(target=work, args=(r,)) for r in range(world)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errs, errs
+    for res in got:
+        assert (res.status, res.text, res.cost) == (want["status"], want["formula"], want["cost"])
+        assert (res.stats.offered, res.stats.admitted, res.stats.duplicates) == (want["offered"], want["admitted"],
+                                                                               want["duplicates"])
+        assert _levels(res) == want["levels"]
