@@ -1023,6 +1023,8 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
         CK(cudaMemsetAsync(h->d_acc_s1, 0, (size_t)total * 8, h->stream));
         CK(cudaMemsetAsync(h->d_acc_err, 0, (size_t)total * 4, h->stream));
     }
+    u64 issued_units = 0;       // what the phase-A launches of this pass were booked with (statistics)
+    double issued_bytes = 0;
     const bool mueller = h->variant == VAR_MUELLER || h->variant == VAR_NH;  // hashed variants: two 64-bit sums
     const int screen_kind = h->variant == VAR_MUELLER ? KIND_MUELLER : h->variant == VAR_NH ? KIND_NH : KIND_BITS;
     if (fused_not >= 0) {
@@ -1037,6 +1039,8 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
         const bool whole = acc_path || mode == MODE_LOOKUP || (mode == MODE_FP_ONLY && !check_solve);
         const i64 per = whole ? tiles : std::max<i64>(h->sub_tiles, LTL_WARPS_PER_CTA);
         const double bytes_all = screen_bytes(h, pieces);
+        issued_units = 0;
+        issued_bytes = 0;
         u64 known_solver = ~0ull;
         int k = 0;
         for (i64 t0 = 0; t0 < tiles; t0 += per, k++) {
@@ -1058,6 +1062,8 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
             p.tile_offset = t0;
             const double frac = (double)(t1 - t0) / (double)tiles;
             ScopedTimer t(h, LTL_K_SCREEN, (u64)((double)total * frac), bytes_all * frac);
+            issued_units += (u64)((double)total * frac);
+            issued_bytes += bytes_all * frac;
             dim3 grid((unsigned)(((t1 - t0) * p.nsplit + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), 1);
             ScreenParams q = p;
             q.total_tiles = t1;
@@ -1160,6 +1166,19 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     } else {
         offered_c = (u64)total;
         h->duplicates += (u64)total - count;
+    }
+    if (out->status != LTL_S_DONE) {
+        // statistics: tiles above the cut returned at once (or were never launched), so phase A is booked with the
+        // candidates up to the cut only -- the algorithmic bytes of the roofline count work that was done
+        double done_bytes = 0;
+        const double B = 8.0 * (double)h->n;
+        for (auto& pc : pieces) {
+            if (pc.ext) continue;
+            const i64 upto = std::min<i64>(pc.count, std::max<i64>(0, (i64)offered_c - pc.cbase));
+            done_bytes += (double)upto * ((pc.kind == PIECE_UNARY ? 1.0 : 2.0) * B + 16.0);
+        }
+        h->stats[LTL_K_SCREEN].bytes += done_bytes - issued_bytes;
+        h->stats[LTL_K_SCREEN].units = h->stats[LTL_K_SCREEN].units - issued_units + std::min<u64>(issued_units, offered_c);
     }
     out->admitted = count;
     const u64 gbase = h->offered;
