@@ -932,10 +932,10 @@ struct ChunkOut {
 };
 
 static void choose_split(ltl_core* h, i64 tiles, int* nsplit, int* rows_per_split) {
-    int ns = 1;
+    int ns = 1;  // (tiles == 0: a pass whose only candidates are the NOTs that phase B screens -- found by scripts/soak.py)
     const i64 target = (i64)h->sm_count * 16 * 4;  // warps wanted: 4 waves, so uneven tiles still balance
     if (h->force_split > 0) ns = h->force_split;
-    else if (tiles < target && h->R >= 2 * LTL_SPLIT_ROWS) ns = (int)std::min<i64>((target + tiles - 1) / tiles, h->max_split);
+    else if (tiles > 0 && tiles < target && h->R >= 2 * LTL_SPLIT_ROWS) ns = (int)std::min<i64>((target + tiles - 1) / tiles, h->max_split);
     const int max_ns = (h->R + LTL_SPLIT_ROWS - 1) / LTL_SPLIT_ROWS;
     ns = std::max(1, std::min(ns, max_ns));
     int rps = (h->R + ns - 1) / ns;

@@ -438,7 +438,8 @@ def test_device_packing_matches_host_packing(R, L, n_props, W):
 @pytest.mark.parametrize("R,err_max,budget_entries,chunk", [(16, -1, None, None), (64, -1, None, None), (100, -1, None, None),
                                                             (200, -1, None, None), (1024, -1, None, None),
                                                             (100, 40, None, None), (64, 27, None, None),
-                                                            (100, -1, 700, None), (130, -1, None, 500), (256, 110, None, 3000)])
+                                                            (100, -1, 700, None), (130, -1, None, 500), (256, 110, None, 3000),
+                                                            (200, -1, None, 6), (256, -1, None, 7)])  # pass = the fused NOTs only
 @pytest.mark.parametrize("variant", [V_MUELLER, V_NH], ids=["mueller", "nh"])
 def test_fused_not_levels_match_unfused(R, err_max, budget_entries, chunk, variant):
     """Phase B of a level also screens NOT(new entry) for the next level (k_materialize_not): identical statuses,
