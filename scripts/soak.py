@@ -24,6 +24,7 @@ from paper_2402_12373_b200.sharded import ThreadComm, row_sharded_core_factory, 
 ap = argparse.ArgumentParser()
 ap.add_argument("--seconds", type=float, default=300)
 ap.add_argument("--seed", type=int, default=0)
+ap.add_argument("--big", action="store_true", help="up to 3000 traces per specification, shallower searches")
 a = ap.parse_args()
 warnings.simplefilter("ignore")
 if os.environ.get("SOAK_ONLY"):
@@ -66,7 +67,8 @@ t_end, n = time.time() + a.seconds, 0
 while time.time() < t_end:
     n += 1
     n_props = int(rng.integers(1, 4))
-    n_pos, n_neg = int(rng.integers(1, 200)), int(rng.integers(1, 200))
+    top = 1500 if a.big else 200
+    n_pos, n_neg = int(rng.integers(1, top)), int(rng.integers(1, top))
     hi = int(rng.choice([5, 20, 63, 64, 65, 130, 200]))
     lo = int(rng.integers(1, hi + 1))
     population = 1 << 40 if hi > 12 else sum((1 << n_props) ** length for length in range(lo, hi + 1))
@@ -80,7 +82,7 @@ while time.time() < t_end:
             spec, al = random_spec(rng, n_props, n_pos, n_neg, lo, hi)
     except (RuntimeError, ValueError):
         continue
-    kw = dict(max_cost=int(rng.integers(4, 8)))
+    kw = dict(max_cost=int(rng.integers(4, 7 if a.big else 8)))
     if rng.random() < 0.3:
         kw["noise"] = float(rng.choice([0.02, 0.1, 0.3]))
     if rng.random() < 0.2:
