@@ -514,7 +514,8 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
 
 // Resident CTAs per SM asked of ptxas.  One-word rows keep every hot loop spill-free below 85 registers (checked in
 // the SASS), and with 16 warps per SM ncu showed `wait` (fixed-latency dependencies) as the top stall, so W = 1 runs
-// 3 CTAs = 24 warps per SM (bench: k_screen 16.4 -> 14.8 ms per search; 4 CTAs: 15.5 ms); wider rows hold whole
+// 3 CTAs = 24 warps per SM (bench: k_screen 16.4 -> 14.8 ms per search; 4 CTAs: 15.5 ms; re-measured after the NOT pass
+// moved into phase B: 2 / 3 / 4 CTAs = 9.65 / 9.86 / 10.50 ms on the bench, 77.3 / 75.8 ms on the 8192-row deep run); wider rows hold whole
 // rows in registers and stay at 2.
 #ifndef LTL_MIN_CTAS_W1
 #define LTL_MIN_CTAS_W1 3
