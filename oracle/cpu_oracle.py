@@ -63,6 +63,9 @@ def lib():
         L.oracle_screen_unary.argtypes = [C.c_void_p, C.c_int, C.c_long, C.c_long, lp, lp]
         L.oracle_screen_binary.argtypes = [C.c_void_p, C.c_int, C.c_long, C.c_long, C.c_long, C.c_long, C.c_int, lp, lp]
         L.oracle_max_threads.restype = C.c_int
+        L.oracle_set_store_results.argtypes = [C.c_void_p, C.c_int]
+        L.oracle_unstored_from.argtypes = [C.c_void_p]
+        L.oracle_unstored_from.restype = C.c_long
         _lib = L
     return _lib
 
@@ -141,6 +144,7 @@ class OracleCore:
         return int(hi.value) << 64 | int(lo.value)
 
     def get_cm(self, idx):
+        self._check_stored(int(idx), 1)
         out = np.empty(self.n, dtype=np.uint64)
         lib().oracle_get_cm(self._h, int(idx), _u64(out))
         return out
@@ -154,6 +158,7 @@ class OracleCore:
         n = self.n_entries
         count = n - first if count is None else count
         out = np.empty((count, self.n), dtype=np.uint64)
+        self._check_stored(int(first), int(count))
         if count:
             lib().oracle_export_cms(self._h, int(first), int(count), _u64(out))
         return out
@@ -171,15 +176,30 @@ class OracleCore:
         return op, lhs, rhs
 
     def screen_unary(self, op, c0, c1):
+        self._check_stored(0, int(c1))
         li, ri = C.c_long(), C.c_long()
         st = lib().oracle_screen_unary(self._h, int(op), int(c0), int(c1), C.byref(li), C.byref(ri))
         return st, li.value, ri.value
 
     def screen_binary(self, op, a0, a1, b0, b1, tri):
+        self._check_stored(0, max(int(a1), int(b1)))
         li, ri = C.c_long(), C.c_long()
         st = lib().oracle_screen_binary(self._h, int(op), int(a0), int(a1), int(b0), int(b1), int(bool(tri)),
                                         C.byref(li), C.byref(ri))
         return st, li.value, ri.value
+
+    def set_option(self, name, value):
+        """Only ``store_results`` (same meaning as the device core's option): 0 = entries admitted from now on
+        keep record and fingerprint but no matrix."""
+        if name != "store_results":
+            raise ValueError(f"unknown option {name}")
+        if lib().oracle_set_store_results(self._h, int(value)):
+            raise ValueError("matrices were already skipped: storing cannot resume")
+
+    def _check_stored(self, first, count):
+        u = lib().oracle_unstored_from(self._h)
+        if u >= 0 and first + count > u:
+            raise ValueError("matrices of these entries were not stored")
 
     # -- pure operator access (op-level parity tests) ------------------------
     def apply_unary(self, op, x):

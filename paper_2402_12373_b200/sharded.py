@@ -218,6 +218,9 @@ class ShardedCore:
     def get_record(self, idx):
         return self.local.get_record(idx)
 
+    def export_records(self, first=0, count=None):
+        return self.local.export_records(first, count)
+
     def counters(self):
         return self.local.counters()
 
@@ -402,6 +405,9 @@ class RowShardedCore:
     # replicated state
     def get_record(self, idx):
         return self.local.get_record(idx)
+
+    def export_records(self, first=0, count=None):
+        return self.local.export_records(first, count)
 
     def counters(self):
         return self.local.counters()

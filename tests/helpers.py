@@ -92,3 +92,57 @@ def random_spec(rng, n_props, n_pos, n_neg, lo, hi):
             seen.add(tr)
             out.append(tr)
     return Specification(out[:n_pos], out[n_pos:]), Alphabet.default(n_props)
+
+
+def records_sha(core, first: int, count: int) -> str:
+    """SHA-256 of the (op int8, lhs int32, rhs int32) record arrays of entries [first, first + count): records
+    determine the characteristic matrices inductively, so equal hashes level by level mean the same set of
+    unique CS in the same order."""
+    if count <= 0:
+        return hashlib.sha256(b"").hexdigest()
+    if hasattr(core, "export_records"):
+        op, lhs, rhs = core.export_records(first, count)
+    else:
+        recs = np.array([core.get_record(first + k) for k in range(count)], dtype=np.int64).reshape(-1, 3)
+        op, lhs, rhs = recs[:, 0], recs[:, 1], recs[:, 2]
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(op, dtype=np.int8).tobytes())
+    h.update(np.ascontiguousarray(lhs, dtype="<i4").tobytes())
+    h.update(np.ascontiguousarray(rhs, dtype="<i4").tobytes())
+    return h.hexdigest()
+
+
+def search_with_record_hashes(spec, alphabet, *, max_cost, budget_bytes, core_factory=None, hash=None, device=0):
+    """One search through `learner.Enumeration`; returns the outcome as a JSON-able dict with, per cost level, the
+    counters and the SHA-256 of the level's records (fixtures: tests/golden/full_levels.json)."""
+    from paper_2402_12373_b200.formula import print_formula
+    from paper_2402_12373_b200.learner import Enumeration, OutOfMemory, Solved
+
+    cfg = LearnerConfig(ceiling=max_cost + 1, budget_bytes=int(budget_bytes), hash=hash or HashScheme(), device=device)
+    en = Enumeration(spec, alphabet, cfg, core_factory=core_factory)
+    en.keep_core = True
+    out = en.run()
+    status = "solved" if isinstance(out, Solved) else "oom" if isinstance(out, OutOfMemory) else "ceiling"
+    res = {"status": status, "formula": print_formula(out.formula, alphabet) if status == "solved" else None,
+           "cost": out.cost if status == "solved" else None, "offered": out.stats.offered,
+           "admitted": out.stats.admitted, "duplicates": out.stats.duplicates, "levels": []}
+    core, cache = en.core, en.cache
+    if core is not None:
+        n = core.counters()[0]
+        s, e = cache.bucket_range(1)
+        res["atoms_sha256"] = records_sha(core, s, e - s)
+        rows = {r["cost"]: r for r in out.stats.levels}
+        costs = sorted(c for c in cache._buckets if c > 1)
+        for c in costs:
+            s, e = cache._buckets[c]
+            e = max(e, s)
+            if c not in rows:  # the level a search ended in by OOM has no stats row; its bucket ends at n_entries
+                e = n
+            row = {k: v for k, v in rows.get(c, {"cost": c}).items() if k != "ms"}
+            row["entries"] = [int(s), int(e)]
+            row["records_sha256"] = records_sha(core, s, e - s)
+            res["levels"].append(row)
+        close = getattr(core, "close", None)
+        if close:
+            close()
+    return res
