@@ -49,6 +49,10 @@ extern "C" {
 /* not in the reference: this build's NH hash for matrices of more than 64 words, where the reference defines
  * nothing (it refuses such inputs, enumerator.py:70-73).  Definition: oracle/ltl_oracle.c fp_nh, DESIGN.md 3. */
 #define LTL_V_NH 3
+/* NH over row pairs, for specifications whose traces all have at most 32 positions (one word per row, W == 1):
+ * the core then stores two rows per 64-bit word (uint32 storage for L <= 32) and moves half the bytes per matrix.
+ * The ABI is unchanged -- matrices cross it as uint64[R].  Definition: oracle/ltl_oracle.c fp_nh32. */
+#define LTL_V_NH32 4
 
 /* error codes */
 #define LTL_OK 0

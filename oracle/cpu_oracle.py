@@ -18,7 +18,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 _LIB_PATH = os.path.join(_HERE, "liboracle.so")
 
 S_DONE, S_SOLVED, S_OOM = 0, 1, 2
-V_GATHER, V_MUELLER, V_FKP, V_NH = 0, 1, 2, 3
+V_GATHER, V_MUELLER, V_FKP, V_NH, V_NH32 = 0, 1, 2, 3, 4
 
 
 class CoreOOM(Exception):

@@ -60,6 +60,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     jobs = [(os.path.join(CSRC, "core.cu"), os.path.join(OBJ, "core.o"), [])]
     for w in range(1, MAX_W + 1):
         jobs.append((os.path.join(CSRC, "screen_inst.cu"), os.path.join(OBJ, f"screen_w{w}.o"), [f"-DLTL_W={w}"]))
+    jobs.append((os.path.join(CSRC, "screen_inst.cu"), os.path.join(OBJ, "screen_w1p.o"), ["-DLTL_W=1", "-DLTL_PAIR"]))
     with ThreadPoolExecutor(max_workers=min(len(jobs), os.cpu_count() or 4)) as pool:
         objs = list(pool.map(_compile, jobs))
     cmd = [nvcc(), *ARCH, "-shared", "-cudart", "static", "-o", LIB, *objs]

@@ -22,7 +22,7 @@ import numpy as np
 from .errors import BackendUnavailable, CoreError, CoreOOM
 
 S_DONE, S_SOLVED, S_OOM = 0, 1, 2
-V_GATHER, V_MUELLER, V_FKP, V_NH = 0, 1, 2, 3
+V_GATHER, V_MUELLER, V_FKP, V_NH, V_NH32 = 0, 1, 2, 3, 4
 MAX_WORDS_PER_ROW = 16
 
 ERR_ARG, ERR_CUDA, ERR_BUDGET, ERR_DEVICE_OOM = -1, -2, -3, -4

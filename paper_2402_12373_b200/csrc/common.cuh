@@ -21,7 +21,7 @@ typedef long long i64;
 
 // opcodes (reference formula.py:13-20); 0 doubles as "identity" for add_entry / fingerprint_of.
 enum { OP_IDENT = 0, OP_NOT = 1, OP_AND = 2, OP_OR = 3, OP_NEXT = 4, OP_FINALLY = 5, OP_GLOBALLY = 6, OP_UNTIL = 7 };
-enum { VAR_GATHER = 0, VAR_MUELLER = 1, VAR_FKP = 2, VAR_NH = 3 };  // NH: this build's hash beyond the reference's domain
+enum { VAR_GATHER = 0, VAR_MUELLER = 1, VAR_FKP = 2, VAR_NH = 3, VAR_NH32 = 4 };  // NH / NH32: this build's hashes beyond the reference's domain
 enum { PIECE_UNARY = 0, PIECE_RECT = 1, PIECE_TRI = 2 };
 enum { MODE_INSERT = 0, MODE_FP_ONLY = 1, MODE_LOOKUP = 2, MODE_REWRITE = 3 };
 enum { KIND_BITS = 0, KIND_MUELLER = 1, KIND_REWRITE = 2, KIND_NH = 3 };  // what a k_screen instantiation does with a row
@@ -108,7 +108,9 @@ struct ScreenParams {
     const u64* masks;  // n words
     const Piece* pieces;
     int n_pieces;
-    int R, W, n_pos, err_max;
+    int R, W, n_pos, err_max;  // half-width store: R = stored words per entry (row pairs), n_pos = positive HIGH-half rows
+    int n_pos_lo;              // half-width store: positive LOW-half rows (floor(n_pos / 2) of the real rows); else unused
+    int pair;                  // 1: half-width store (two 32-bit rows per word, see semantics.cuh apply_pair)
     i64 n;  // words per entry
     i64 total_tiles;
     i64 tile_offset;   // first warp tile of this launch (a level's phase A is issued in several launches)
@@ -150,6 +152,7 @@ struct MaterializeParams {
     // fused NOT (k_materialize<W, FK != 0>): while a new entry's rows are in registers, the candidate NOT(entry) of
     // the NEXT cost level is evaluated too -- its chunk-local rank is not_cbase + (entry - not_i0)
     int n_pos;
+    int n_pos_lo;  // as in ScreenParams (half-width store)
     i64 not_cbase, not_i0;
     u32 blk_base;  // as in ScreenParams
     u32 pad_;

@@ -34,6 +34,9 @@
 LTL_DECL_W(1) LTL_DECL_W(2) LTL_DECL_W(3) LTL_DECL_W(4) LTL_DECL_W(5) LTL_DECL_W(6) LTL_DECL_W(7) LTL_DECL_W(8)
 LTL_DECL_W(9) LTL_DECL_W(10) LTL_DECL_W(11) LTL_DECL_W(12) LTL_DECL_W(13) LTL_DECL_W(14) LTL_DECL_W(15) LTL_DECL_W(16)
 #undef LTL_DECL_W
+// half-width store (two 32-bit rows per word): screen_inst.cu compiled with -DLTL_W=1 -DLTL_PAIR
+extern "C" void ltl_launch_screen_w1p(const ScreenParams&, int, dim3, cudaStream_t);
+extern "C" void ltl_launch_materialize_w1p(const MaterializeParams&, const ScreenParams&, int, dim3, cudaStream_t);
 
 static const screen_launch_fn SCREEN_FN[LTL_MAX_W + 1] = {
     nullptr, ltl_launch_screen_w1, ltl_launch_screen_w2, ltl_launch_screen_w3, ltl_launch_screen_w4,
@@ -590,8 +593,13 @@ static size_t pool_trim() {  // give every pooled page back to the driver
 }
 
 struct ltl_core : Arena {
+    // Half-width store (`pair`, variant NH32: every trace has at most 32 positions): two rows share one stored word
+    // (row 2v high half, row 2v + 1 low half), so R / n / n_pos below count STORED words -- R = ceil(R_api / 2),
+    // n_pos = positive high-half rows, n_pos_lo = positive low-half rows -- while the C ABI keeps uint64[R_api].
     int R = 0, W = 0, n_pos = 0, err_max = 0, variant = 0, fkp_bits = 0, mask_k = 0;
-    i64 n = 0;
+    int R_api = 0, n_pos_lo = 0;
+    bool pair = false;
+    i64 n = 0, n_api = 0;
     u64 budget = 0, entry_bytes = 0;
     u64 cap_entries = 0;  // admissions allowed: min(logical budget, what the device can hold)
     int n_dep = 0;
@@ -995,6 +1003,8 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     p.R = h->R;
     p.W = h->W;
     p.n_pos = h->n_pos;
+    p.n_pos_lo = h->n_pos_lo;
+    p.pair = h->pair ? 1 : 0;
     p.err_max = h->err_max;
     p.n = h->n;
     p.total_tiles = tiles;
@@ -1067,7 +1077,7 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
             dim3 grid((unsigned)(((t1 - t0) * p.nsplit + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), 1);
             ScreenParams q = p;
             q.total_tiles = t1;
-            SCREEN_FN[h->W](q, screen_kind, grid, h->stream);
+            (h->pair ? ltl_launch_screen_w1p : SCREEN_FN[h->W])(q, screen_kind, grid, h->stream);
             if (per < tiles) {
                 CK(cudaMemcpyAsync(h->h_solver + (k & 1), &h->d_ctl->solver_c, sizeof(u64), cudaMemcpyDeviceToHost, h->stream));
                 CK(cudaEventRecord(h->sub_ev[k & 1], h->stream));
@@ -1222,6 +1232,8 @@ static int flush_materialize(ltl_core* h, const ScreenParams* sp, int fuse_kind,
             p.R = h->R;
             p.W = h->W;
             p.n_pos = h->n_pos;
+            p.n_pos_lo = h->n_pos_lo;
+            p.pair = h->pair ? 1 : 0;
             p.n = h->n;
             p.total_tiles = pm.tiles;
             choose_split(h, pm.tiles, &p.nsplit, &p.rows_per_split);
@@ -1231,7 +1243,7 @@ static int flush_materialize(ltl_core* h, const ScreenParams* sp, int fuse_kind,
             p.ctl = h->d_ctl;
             ScopedTimer t(h, LTL_K_MATERIALIZE, count, bytes);
             dim3 grid((unsigned)((pm.tiles * p.nsplit + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), 1);
-            SCREEN_FN[h->W](p, KIND_REWRITE, grid, h->stream);
+            (h->pair ? ltl_launch_screen_w1p : SCREEN_FN[h->W])(p, KIND_REWRITE, grid, h->stream);
             CK(cudaGetLastError());
             continue;
         }
@@ -1257,13 +1269,14 @@ static int flush_materialize(ltl_core* h, const ScreenParams* sp, int fuse_kind,
             m.nsplit = 1;
             m.rows_per_split = h->R;
             m.n_pos = h->n_pos;
+            m.n_pos_lo = h->n_pos_lo;
             m.not_cbase = not_cbase;
             m.not_i0 = not_i0;
             fk = fuse_kind;
         }
         ScopedTimer t(h, LTL_K_MATERIALIZE, count, bytes + (fk ? (double)count * 16.0 : 0.0));
         dim3 grid((unsigned)((groups + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), (unsigned)m.nsplit);
-        MATERIALIZE_FN[h->W](m, fk ? *sp : none, fk, grid, h->stream);
+        (h->pair ? ltl_launch_materialize_w1p : MATERIALIZE_FN[h->W])(m, fk ? *sp : none, fk, grid, h->stream);
         CK(cudaGetLastError());
     }
     h->pending_mat.clear();
@@ -1465,11 +1478,24 @@ static void plan_range(ltl_core* h, const std::vector<Unit>& units, i64 lo, i64 
 // ------------------------------------------------------------------------------------------------
 // single-matrix paths (add_entry / contains / fingerprint_of)
 
+// half-width store: uint64[R] rows (positions in the high half) <-> ceil(R / 2) words holding rows 2v | 2v + 1
+static void pack_pairs(const uint64_t* rows, int R, u64* out) {
+    for (int v = 0; 2 * v < R; v++)
+        out[v] = (rows[2 * v] & 0xFFFFFFFF00000000ull) | (2 * v + 1 < R ? rows[2 * v + 1] >> 32 : 0ull);
+}
+static void unpack_pairs(const u64* words, int R, uint64_t* out) {
+    for (int v = 0; 2 * v < R; v++) {
+        out[2 * v] = words[v] & 0xFFFFFFFF00000000ull;
+        if (2 * v + 1 < R) out[2 * v + 1] = words[v] << 32;
+    }
+}
+
 static int stage_matrix(ltl_core* h, const uint64_t* cm, i64 e) {
     int rc;
     if ((rc = ensure_entries(h, (u64)e + 1))) return rc;
     CK(cudaStreamSynchronize(h->stream));  // h_stage may still be in flight
-    memcpy(h->h_stage, cm, (size_t)h->n * 8);
+    if (h->pair) pack_pairs(cm, h->R_api, h->h_stage);
+    else memcpy(h->h_stage, cm, (size_t)h->n * 8);
     CK(cudaMemcpyAsync(h->d_stage, h->h_stage, (size_t)h->n * 8, cudaMemcpyHostToDevice, h->stream));
     h->h2d_bytes += (size_t)h->n * 8;
     ScopedTimer t(h, LTL_K_MISC, 1, 16.0 * (double)h->n);
@@ -1631,7 +1657,8 @@ int ltl_core_create(const uint64_t* masks, int R, int W, int n_pos, int err_max,
     if (!masks || R < 1) return bad("need at least one row");
     if (W < 1 || W > LTL_MAX_W) return bad("words per row must lie in [1, 16]");
     if (n_pos < 0 || n_pos > R) return bad("n_pos outside [0, R]");
-    if (variant < 0 || variant > VAR_NH) return bad("unknown fingerprint variant");
+    if (variant < 0 || variant > VAR_NH32) return bad("unknown fingerprint variant");
+    if (variant == VAR_NH32 && W != 1) return bad("the half-width variant (NH32) needs one word per row");
     if (n_proj < 0 || n_proj > 126) return bad("projection wider than the fingerprint");  // reference _speedups.pyx:92-93
     if (mask_k < 0 || mask_k > 126) return bad("mask_k outside [0, 126]");
     if ((int64_t)R * W > (int64_t)1 << 31) return bad("matrix too large");
@@ -1645,16 +1672,20 @@ int ltl_core_create(const uint64_t* masks, int R, int W, int n_pos, int err_max,
     if (device < 0 || device >= ndev) return bad("device index out of range");
     ltl_core* h = new ltl_core();
     h->device = device;
-    h->R = R;
+    h->R_api = R;
+    h->n_api = (i64)R * W;
+    h->pair = variant == VAR_NH32;
+    h->R = h->pair ? (R + 1) / 2 : R;
     h->W = W;
-    h->n = (i64)R * W;
-    h->n_pos = n_pos;
+    h->n = (i64)h->R * W;
+    h->n_pos = h->pair ? (n_pos + 1) / 2 : n_pos;
+    h->n_pos_lo = h->pair ? n_pos / 2 : n_pos;
     h->err_max = err_max;
-    h->variant = variant;
+    h->variant = h->pair ? VAR_NH : variant;
     h->fkp_bits = fkp_bits;
     h->mask_k = mask_k;
     h->budget = budget_bytes;
-    h->entry_bytes = (u64)h->n * 8 + 16;  // reference _speedups.pyx:100
+    h->entry_bytes = (u64)h->n_api * 8 + 16;  // reference _speedups.pyx:100 (logical: one 64-bit word per row)
     int rc = LTL_OK;
     auto boot = [&]() -> int {
         CK(cudaSetDevice(device));
@@ -1712,7 +1743,8 @@ int ltl_core_create(const uint64_t* masks, int R, int W, int n_pos, int err_max,
             CK(cudaMallocHost(&h->h_stage, (size_t)h->n * 8));
             h->stage_cap = h->n;
         }
-        memcpy(h->h_stage, masks, (size_t)h->n * 8);  // pinned staging: the copy below is truly asynchronous
+        if (h->pair) pack_pairs(masks, h->R_api, h->h_stage);
+        else memcpy(h->h_stage, masks, (size_t)h->n * 8);  // pinned staging: the copy below is truly asynchronous
         CK(cudaMemcpyAsync(h->d_masks, h->h_stage, (size_t)h->n * 8, cudaMemcpyHostToDevice, h->stream));
         h->h2d_bytes += (size_t)h->n * 8;
         std::vector<Deposit> deps;
@@ -1890,12 +1922,20 @@ int ltl_core_export_cms(ltl_core* h, int64_t first, int64_t count, uint64_t* cms
             ScopedTimer t(h, LTL_K_MISC, (u64)take, 16.0 * (double)h->n * (double)take);
             k_export<<<(unsigned)((threads + 255) / 256), 256, 0, h->stream>>>((const u64*)h->cms.base, f, take, h->n, d_out);
         }
-        cudaError_t e = cudaMemcpyAsync(cms_out + (size_t)done * h->n, d_out, (size_t)take * h->n * 8, cudaMemcpyDeviceToHost, h->stream);
+        void* host_dst = cms_out + (size_t)done * h->n_api;
+        std::vector<u64> packed;
+        if (h->pair) {
+            packed.resize((size_t)take * h->n);
+            host_dst = packed.data();
+        }
+        cudaError_t e = cudaMemcpyAsync(host_dst, d_out, (size_t)take * h->n * 8, cudaMemcpyDeviceToHost, h->stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(h->stream);
         if (e != cudaSuccess) {
             cudaFree(d_out);
             return h->cuda_fail(e, "export_cms");
         }
+        if (h->pair)
+            for (i64 k = 0; k < take; k++) unpack_pairs(packed.data() + (size_t)k * h->n, h->R_api, cms_out + (size_t)(done + k) * h->n_api);
         h->d2h_bytes += (size_t)take * h->n * 8;
         done += take;
     }
@@ -2019,13 +2059,16 @@ int ltl_core_level_size(ltl_core* h, const ltl_segment* segs, int n_segs, int64_
 int ltl_core_set_row_shard(ltl_core* h, int64_t word_base, int64_t total_words, ltl_exchange_fn fn, void* ctx) {
     ENTER(h);
     if (h->n_entries || h->offered) return h->fail(LTL_ERR_ARG, "set_row_shard: the core is already in use");
-    if (!fn || word_base < 0 || (word_base & 63) || total_words < word_base + h->n)
-        return h->fail(LTL_ERR_ARG, "set_row_shard: word_base must be a multiple of 64 and the shard must lie inside the matrix");
-    if (word_base + h->n < total_words && (h->n & 63))
-        return h->fail(LTL_ERR_ARG, "set_row_shard: only the last shard may end inside a 64-word fingerprint block");
+    // a fingerprint block is 64 STORED words: 64 API words, or 128 rows of the half-width store
+    const i64 blk_words = h->pair ? 128 : 64;
+    if (!fn || word_base < 0 || (word_base % blk_words) || total_words < word_base + h->n_api)
+        return h->fail(LTL_ERR_ARG, "set_row_shard: word_base must be a multiple of the fingerprint block (64 words; 128 rows for "
+                                    "the half-width store) and the shard must lie inside the matrix");
+    if (word_base + h->n_api < total_words && (h->n_api % blk_words))
+        return h->fail(LTL_ERR_ARG, "set_row_shard: only the last shard may end inside a fingerprint block");
     if (h->variant != VAR_MUELLER && h->variant != VAR_NH)
         return h->fail(LTL_ERR_ARG, "set_row_shard: needs a block-combinable fingerprint (mueller / nh)");
-    h->blk_base = (u32)(word_base >> 6);
+    h->blk_base = (u32)(word_base / blk_words);
     h->exchange = fn;
     h->exchange_ctx = ctx;
     // the budget counts whole matrices, like the reference's (reference _speedups.pyx:100, 252-253)
@@ -2186,7 +2229,7 @@ int ltl_core_info(ltl_core* h, uint64_t out[6]) {
     out[2] = h->table_cap;
     out[3] = (u64)h->chunk_cap;
     out[4] = (h->cms.vmm ? 1 : 0) | (h->device_oom ? 2 : 0);
-    out[5] = (u64)h->n;
+    out[5] = (u64)h->n_api;
     return LTL_OK;
 }
 

@@ -191,13 +191,13 @@ template <int OPS>
 __host__ __device__ constexpr int slot_op(int t) {
     return OPS < 16 ? OPS : ((OPS >> (4 * t)) & 15);
 }
-template <int OPS, int W>
+template <int OPS, int W, bool PAIR>
 __device__ __forceinline__ void apply_slot(const int t, u64 (&out)[W], const u64 (&x)[W], const u64 (&y)[W], const u64 (&m)[W]) {
     switch (t) {  // t is a constant after unrolling
-        case 0: apply_row<slot_op<OPS>(0), W>(out, x, y, m); break;
-        case 1: apply_row<slot_op<OPS>(1), W>(out, x, y, m); break;
-        case 2: apply_row<slot_op<OPS>(2), W>(out, x, y, m); break;
-        default: apply_row<slot_op<OPS>(3), W>(out, x, y, m); break;
+        case 0: apply_row<slot_op<OPS>(0), W, PAIR>(out, x, y, m); break;
+        case 1: apply_row<slot_op<OPS>(1), W, PAIR>(out, x, y, m); break;
+        case 2: apply_row<slot_op<OPS>(2), W, PAIR>(out, x, y, m); break;
+        default: apply_row<slot_op<OPS>(3), W, PAIR>(out, x, y, m); break;
     }
 }
 __host__ __device__ constexpr bool op_unary_c(int op) {
@@ -211,7 +211,7 @@ __host__ __device__ constexpr bool ops_need_mask() {
                        ((OPS >> 12) & 15) == OP_NOT || ((OPS >> 12) & 15) == OP_GLOBALLY);
 }
 
-template <int W, int KIND, int OP, int TI, bool XL>
+template <int W, int KIND, int OP, int TI, bool XL, bool PAIR>
 __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc, const i64 row0, const i64 lg,
                                           const int split, const int lane, u64* __restrict__ sbuf, u64* bars) {
     constexpr bool MUELLER = KIND == KIND_MUELLER;
@@ -269,13 +269,16 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
     // Verdict bits (MSB of word 0 of every row) are COUNTED with one multiply-add-high per row on the FMA pipe
     // (ones += hi32 * 2 >> 32); the count over the positive rows is snapshotted when the row index crosses n_pos:
     // errors = (#positives - ones_pos) + (ones - ones_pos)          (reference _speedups.pyx:327-333)
-    u32 ones[TI], ones_pos[TI];
+    // Half-width store (PAIR): a word holds rows 2v (high half, verdict bit 63) and 2v + 1 (low half, verdict bit 31);
+    // the low rows are counted in ones2 and snapshotted where THEIR positives end (p.n_pos_lo <= p.n_pos <= p.n_pos_lo + 1).
+    u32 ones[TI], ones_pos[TI], ones2[TI], ones2_pos[TI];
 #pragma unroll
     for (int t = 0; t < TI; t++) {
         s0[t] = s1[t] = 0;
         h0[t] = NH ? 0ull : K_SEED0;  // NH: the block's two accumulators d_0, d_1
         h1[t] = NH ? 0ull : K_SEED1;
         ones[t] = ones_pos[t] = 0;
+        ones2[t] = ones2_pos[t] = 0;
     }
     u64 tw = ((u64)p.blk_base * 64ull + (u64)r0 * W + 1ull) * K_STEP;  // (k + 1) * STEP for the next (global) word k
     int d = 0;                               // next deposit (bits fingerprints)
@@ -318,6 +321,11 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
 #pragma unroll
         for (int t = 0; t < TI; t++) ones_pos[t] = ones[t];
     };
+    auto snapshot_lo = [&]() {
+#pragma unroll
+        for (int t = 0; t < TI; t++) ones2_pos[t] = ones2[t];
+    };
+    const int n_pos_lo = PAIR ? p.n_pos_lo : p.n_pos;
 
     // src: this lane's column of the staged row (word w at src[w * 32]); xs: the row operands' words of that row
     // (entry t at xs[t * RG_ROWSTRIDE + w])
@@ -345,9 +353,9 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
             u64 b[W], out[W];
 #pragma unroll
             for (int w = 0; w < W; w++) b[w] = BIN ? xs[t * RG_ROWSTRIDE + w] : 0ull;
-            if (!BIN) apply_slot<OP, W>(t, out, a, a, m);
-            else if (XL) apply_slot<OP, W>(t, out, a, b, m);
-            else apply_slot<OP, W>(t, out, b, a, m);
+            if (!BIN) apply_slot<OP, W, PAIR>(t, out, a, a, m);
+            else if (XL) apply_slot<OP, W, PAIR>(t, out, a, b, m);
+            else apply_slot<OP, W, PAIR>(t, out, b, a, m);
             if (REWRITE) {
                 if (pd[t]) {
 #pragma unroll
@@ -356,6 +364,7 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
                 continue;
             }
             asm("mad.hi.u32 %0, %1, 2, %0;" : "+r"(ones[t]) : "r"((u32)(out[0] >> 32)));
+            if (PAIR) asm("mad.hi.u32 %0, %1, 2, %0;" : "+r"(ones2[t]) : "r"((u32)out[0]));
             if (NH) {
 #pragma unroll
                 for (int w = 0; w < W; w++) {  // oracle fp_nh
@@ -456,8 +465,10 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
         const u64* __restrict__ xsrc = sbuf + stage * RG::STAGE_U64 + RG::LANE_U64;
         const int rbase = r0 + c * RG::RPC;
         const int rows_c = min(RG::RPC, r1 - rbase);
-        const bool straddle = p.n_pos > rbase && p.n_pos < rbase + rows_c;
+        const bool straddle = (p.n_pos > rbase && p.n_pos < rbase + rows_c) ||
+                              (PAIR && n_pos_lo > rbase && n_pos_lo < rbase + rows_c);
         if (rbase == p.n_pos) snapshot();
+        if (PAIR && rbase == n_pos_lo) snapshot_lo();
         if (rows_c == RG::RPC && !straddle) {
             // partial unroll: a fully unrolled stage of a 4-slot tile is ~24 KB of code, and a level with many
             // small pieces runs a dozen tile variants per SM -- ncu showed `no_instructions` as the top stall
@@ -466,6 +477,7 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
         } else {
             for (int rr = 0; rr < rows_c; rr++) {
                 if (rr && rbase + rr == p.n_pos) snapshot();
+                if (PAIR && rr && rbase + rr == n_pos_lo) snapshot_lo();
                 do_row(rbase + rr, src + rr * W * 32, xsrc + rr * W);
             }
         }
@@ -493,6 +505,11 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
         for (int t = 0; t < TI; t++) {
             if (p.n_pos >= r1) ones_pos[t] = ones[t];  // every row of the split is positive
             err[t] = ((u32)npos_here - ones_pos[t]) + (ones[t] - ones_pos[t]);
+            if (PAIR) {
+                const int npos_lo_here = max(0, min(r1, n_pos_lo) - r0);
+                if (n_pos_lo >= r1) ones2_pos[t] = ones2[t];
+                err[t] += ((u32)npos_lo_here - ones2_pos[t]) + (ones2[t] - ones2_pos[t]);
+            }
         }
     }
 #pragma unroll
@@ -520,8 +537,9 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
 #ifndef LTL_MIN_CTAS_W1
 #define LTL_MIN_CTAS_W1 3
 #endif
-template <int W, int KIND>
+template <int W, int KIND, bool PAIR = false>
 __global__ void __launch_bounds__(LTL_CTA, (W == 1 ? LTL_MIN_CTAS_W1 : 2)) k_screen(const __grid_constant__ ScreenParams p) {
+    static_assert(!PAIR || (W == 1 && (KIND == KIND_NH || KIND == KIND_REWRITE)), "half-width rows: one word, NH fingerprint");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
@@ -602,7 +620,7 @@ __global__ void __launch_bounds__(LTL_CTA, (W == 1 ? LTL_MIN_CTAS_W1 : 2)) k_scr
     }
     const bool xl = pc.swap != 0;
 
-#define LTL_TILE(OP_, TI_, XL_) tile_eval<W, KIND, OP_, TI_, XL_>(p, pc, row0, lg, split, lane, sbuf, bars)
+#define LTL_TILE(OP_, TI_, XL_) tile_eval<W, KIND, OP_, TI_, XL_, PAIR>(p, pc, row0, lg, split, lane, sbuf, bars)
 #define LTL_TILE_TI(OP_, XL_)                       \
     do {                                            \
         if (W == 1 && KIND != KIND_BITS) {          \
@@ -664,7 +682,7 @@ __global__ void __launch_bounds__(LTL_CTA, (W == 1 ? LTL_MIN_CTAS_W1 : 2)) k_scr
 // ------------------------------------------------------------------------------------------------
 // phase B kernel
 
-template <int W, int OP>
+template <int W, int OP, bool PAIR>
 __device__ __forceinline__ void mat_rows(const MaterializeParams& p, const bool mine, const i64 dst, const int lhs,
                                          const int rhs, const int r0, const int r1) {
     constexpr bool BIN = !(OP == OP_IDENT || OP == OP_NOT || OP == OP_NEXT || OP == OP_FINALLY || OP == OP_GLOBALLY);
@@ -684,13 +702,13 @@ __device__ __forceinline__ void mat_rows(const MaterializeParams& p, const bool 
             y[w] = BIN ? ld_nc(py + (kb + w) * 32) : 0ull;
             m[w] = NEEDM ? ld_nc(p.masks + kb + w) : 0ull;
         }
-        apply_row<OP, W>(out, x, y, m);
+        apply_row<OP, W, PAIR>(out, x, y, m);
 #pragma unroll
         for (int w = 0; w < W; w++) po[(kb + w) * 32] = out[w];
     }
 }
 
-template <int W>
+template <int W, bool PAIR = false>
 __global__ void __launch_bounds__(LTL_CTA) k_materialize(const __grid_constant__ MaterializeParams p) {
     const int lane = threadIdx.x & 31;
     const i64 g = (p.n_base >> 5) + (i64)blockIdx.x * LTL_WARPS_PER_CTA + (threadIdx.x >> 5);
@@ -709,14 +727,14 @@ __global__ void __launch_bounds__(LTL_CTA) k_materialize(const __grid_constant__
         const bool mine = valid && op == cur;
         remaining &= ~__ballot_sync(0xFFFFFFFFu, mine);
         switch (cur) {
-            case OP_NOT: mat_rows<W, OP_NOT>(p, mine, dst, lhs, rhs, r0, r1); break;
-            case OP_AND: mat_rows<W, OP_AND>(p, mine, dst, lhs, rhs, r0, r1); break;
-            case OP_OR: mat_rows<W, OP_OR>(p, mine, dst, lhs, rhs, r0, r1); break;
-            case OP_NEXT: mat_rows<W, OP_NEXT>(p, mine, dst, lhs, rhs, r0, r1); break;
-            case OP_FINALLY: mat_rows<W, OP_FINALLY>(p, mine, dst, lhs, rhs, r0, r1); break;
-            case OP_GLOBALLY: mat_rows<W, OP_GLOBALLY>(p, mine, dst, lhs, rhs, r0, r1); break;
-            case OP_UNTIL: mat_rows<W, OP_UNTIL>(p, mine, dst, lhs, rhs, r0, r1); break;
-            default: mat_rows<W, OP_IDENT>(p, mine, dst, lhs, rhs, r0, r1); break;
+            case OP_NOT: mat_rows<W, OP_NOT, PAIR>(p, mine, dst, lhs, rhs, r0, r1); break;
+            case OP_AND: mat_rows<W, OP_AND, PAIR>(p, mine, dst, lhs, rhs, r0, r1); break;
+            case OP_OR: mat_rows<W, OP_OR, PAIR>(p, mine, dst, lhs, rhs, r0, r1); break;
+            case OP_NEXT: mat_rows<W, OP_NEXT, PAIR>(p, mine, dst, lhs, rhs, r0, r1); break;
+            case OP_FINALLY: mat_rows<W, OP_FINALLY, PAIR>(p, mine, dst, lhs, rhs, r0, r1); break;
+            case OP_GLOBALLY: mat_rows<W, OP_GLOBALLY, PAIR>(p, mine, dst, lhs, rhs, r0, r1); break;
+            case OP_UNTIL: mat_rows<W, OP_UNTIL, PAIR>(p, mine, dst, lhs, rhs, r0, r1); break;
+            default: mat_rows<W, OP_IDENT, PAIR>(p, mine, dst, lhs, rhs, r0, r1); break;
         }
         __syncwarp();
     }
@@ -748,9 +766,15 @@ struct NotFold {
         h1 = FK == KIND_NH ? 0ull : K_SEED1;
     }
     // v = word k (= row k, W = 1) of NOT(entry); pk = k mod 64
-    __device__ __forceinline__ void word(const u64 v, const u32 k, const u32 pk, const bool positive) {
+    // (half-width store: v holds two rows; positive_lo says whether the low-half row is a positive trace)
+    template <bool PAIR>
+    __device__ __forceinline__ void word(const u64 v, const u32 k, const u32 pk, const bool positive, const bool positive_lo) {
         const u32 bit = (u32)(v >> 63);
         err += positive ? 1u - bit : bit;
+        if (PAIR) {
+            const u32 bit2 = ((u32)v) >> 31;
+            err += positive_lo ? 1u - bit2 : bit2;
+        }
         if (FK == KIND_NH) {
             const u64 key0 = c_nh.k[pk], key1 = c_nh.k[pk + 1];
             const u32 xl = (u32)v, xh = (u32)(v >> 32);
@@ -774,7 +798,7 @@ struct NotFold {
     }
 };
 
-template <int OP, int FK>
+template <int OP, int FK, bool PAIR>
 __device__ __forceinline__ void mat_rows_not(const MaterializeParams& p, const bool mine, const i64 dst, const int lhs,
                                              const int rhs, NotFold<FK>& f) {
     constexpr bool BIN = !(OP == OP_IDENT || OP == OP_NOT || OP == OP_NEXT || OP == OP_FINALLY || OP == OP_GLOBALLY);
@@ -784,16 +808,16 @@ __device__ __forceinline__ void mat_rows_not(const MaterializeParams& p, const b
     const u64* __restrict__ py = p.cms + cm_index(BIN ? rhs : lhs, n, 0);
     u64* __restrict__ po = p.cms + cm_index(dst, n, 0);
     const u64* __restrict__ pm = p.masks;
-    const int R = p.R, n_pos = p.n_pos;
+    const int R = p.R, n_pos = p.n_pos, n_pos_lo = p.n_pos_lo;
     const u32 kbase = p.blk_base * 64u;
     auto row = [&](const int r, const u32 pk) {
         u64 x[1], y[1], m[1], out[1];
         x[0] = ld_nc(px + (size_t)r * 32);
         y[0] = BIN ? ld_nc(py + (size_t)r * 32) : 0ull;
         m[0] = ld_nc(pm + r);
-        apply_row<OP, 1>(out, x, y, m);
+        apply_row<OP, 1, PAIR>(out, x, y, m);
         po[(size_t)r * 32] = out[0];
-        f.word(~out[0] & m[0], kbase + (u32)r, pk, r < n_pos);
+        f.template word<PAIR>(~out[0] & m[0], kbase + (u32)r, pk, r < n_pos, r < n_pos_lo);
     };
     constexpr int UNROLL = LTL_MATF_UNROLL;
     for (int rb = 0; rb < R; rb += 64) {
@@ -808,7 +832,7 @@ __device__ __forceinline__ void mat_rows_not(const MaterializeParams& p, const b
     }
 }
 
-template <int FK>
+template <int FK, bool PAIR = false>
 __global__ void __launch_bounds__(LTL_CTA, LTL_MATF_MINB) k_materialize_not(const __grid_constant__ MaterializeParams p,
                                                                             const __grid_constant__ ScreenParams sp) {
     const int lane = threadIdx.x & 31;
@@ -829,14 +853,14 @@ __global__ void __launch_bounds__(LTL_CTA, LTL_MATF_MINB) k_materialize_not(cons
         const bool mine = valid && op == cur;
         remaining &= ~__ballot_sync(0xFFFFFFFFu, mine);
         switch (cur) {
-            case OP_NOT: mat_rows_not<OP_NOT, FK>(p, mine, dst, lhs, rhs, f); break;
-            case OP_AND: mat_rows_not<OP_AND, FK>(p, mine, dst, lhs, rhs, f); break;
-            case OP_OR: mat_rows_not<OP_OR, FK>(p, mine, dst, lhs, rhs, f); break;
-            case OP_NEXT: mat_rows_not<OP_NEXT, FK>(p, mine, dst, lhs, rhs, f); break;
-            case OP_FINALLY: mat_rows_not<OP_FINALLY, FK>(p, mine, dst, lhs, rhs, f); break;
-            case OP_GLOBALLY: mat_rows_not<OP_GLOBALLY, FK>(p, mine, dst, lhs, rhs, f); break;
-            case OP_UNTIL: mat_rows_not<OP_UNTIL, FK>(p, mine, dst, lhs, rhs, f); break;
-            default: mat_rows_not<OP_IDENT, FK>(p, mine, dst, lhs, rhs, f); break;
+            case OP_NOT: mat_rows_not<OP_NOT, FK, PAIR>(p, mine, dst, lhs, rhs, f); break;
+            case OP_AND: mat_rows_not<OP_AND, FK, PAIR>(p, mine, dst, lhs, rhs, f); break;
+            case OP_OR: mat_rows_not<OP_OR, FK, PAIR>(p, mine, dst, lhs, rhs, f); break;
+            case OP_NEXT: mat_rows_not<OP_NEXT, FK, PAIR>(p, mine, dst, lhs, rhs, f); break;
+            case OP_FINALLY: mat_rows_not<OP_FINALLY, FK, PAIR>(p, mine, dst, lhs, rhs, f); break;
+            case OP_GLOBALLY: mat_rows_not<OP_GLOBALLY, FK, PAIR>(p, mine, dst, lhs, rhs, f); break;
+            case OP_UNTIL: mat_rows_not<OP_UNTIL, FK, PAIR>(p, mine, dst, lhs, rhs, f); break;
+            default: mat_rows_not<OP_IDENT, FK, PAIR>(p, mine, dst, lhs, rhs, f); break;
         }
         __syncwarp();
     }
@@ -855,5 +879,6 @@ __global__ void __launch_bounds__(LTL_CTA, LTL_MATF_MINB) k_materialize_not(cons
 #endif  // __CUDACC__
 
 // launchers, one translation unit per W (screen_inst.cu compiled with -DLTL_W=<W>)
+// (W == 1 has a second pair of launchers for the half-width store: ltl_launch_screen_w1p / ltl_launch_materialize_w1p)
 typedef void (*screen_launch_fn)(const ScreenParams&, int kind, dim3 grid, cudaStream_t stream);
 typedef void (*materialize_launch_fn)(const MaterializeParams&, const ScreenParams&, int fuse_kind, dim3 grid, cudaStream_t stream);

@@ -8,6 +8,28 @@
 #define LTL_CAT2(a, b) a##b
 #define LTL_CAT(a, b) LTL_CAT2(a, b)
 
+#ifdef LTL_PAIR
+// the half-width store (two 32-bit rows per word; one-word rows, NH fingerprint only): -DLTL_W=1 -DLTL_PAIR
+#if LTL_W != 1
+#error "LTL_PAIR needs LTL_W == 1"
+#endif
+extern "C" void ltl_launch_screen_w1p(const ScreenParams& p, int kind, dim3 grid, cudaStream_t stream) {
+    static bool configured = false;
+    if (!configured) {
+        cudaFuncSetAttribute(k_screen<1, KIND_NH, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Ring<1>::CTA_BYTES);
+        cudaFuncSetAttribute(k_screen<1, KIND_REWRITE, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, Ring<1>::CTA_BYTES);
+        configured = true;
+    }
+    if (kind == KIND_NH) k_screen<1, KIND_NH, true><<<grid, LTL_CTA, Ring<1>::CTA_BYTES, stream>>>(p);
+    else k_screen<1, KIND_REWRITE, true><<<grid, LTL_CTA, Ring<1>::CTA_BYTES, stream>>>(p);
+}
+extern "C" void ltl_launch_materialize_w1p(const MaterializeParams& p, const ScreenParams& sp, int fuse_kind, dim3 grid,
+                                           cudaStream_t stream) {
+    if (fuse_kind == KIND_NH) k_materialize_not<KIND_NH, true><<<grid, LTL_CTA, 0, stream>>>(p, sp);
+    else k_materialize<1, true><<<grid, LTL_CTA, 0, stream>>>(p);
+}
+#else
+
 extern "C" void LTL_CAT(ltl_launch_screen_w, LTL_W)(const ScreenParams& p, int kind, dim3 grid, cudaStream_t stream) {
     static bool configured = false;
     if (!configured) {  // > 48 KiB of dynamic shared memory needs an opt-in, once per process
@@ -40,3 +62,4 @@ extern "C" void LTL_CAT(ltl_launch_materialize_w, LTL_W)(const MaterializeParams
     (void)fuse_kind;
     k_materialize<LTL_W><<<grid, LTL_CTA, 0, stream>>>(p);
 }
+#endif  // LTL_PAIR

@@ -96,10 +96,44 @@ __device__ __forceinline__ void row_smear_up(u64 (&out)[W], const u64 (&x)[W]) {
     }
 }
 
+// ---- half-width rows (PAIR): traces of at most 32 positions are stored TWO ROWS PER 64-BIT WORD -- row 2i in the
+// high half, row 2i+1 in the low half (uint32 storage for L <= 32; fingerprint = NH over these words, oracle fp_nh32).
+// The connectives act on both halves at once; nothing may cross from the low half into the high one:
+//     X   : (x << 1) with bit 32 cleared            F   : x | -x per half (two 32-bit negations)
+//     U   : the carry-chain form with two 32-bit adds
+__device__ __forceinline__ u64 pack_halves(u32 hi, u32 lo) { return ((u64)hi << 32) | lo; }
+#define LTL_PAIR_SHL1_MASK 0xFFFFFFFEFFFFFFFEull
+
+template <int OP>
+__device__ __forceinline__ u64 apply_pair(const u64 x, const u64 y, const u64 m) {
+    if (OP == OP_IDENT) return x;
+    if (OP == OP_NOT) return ~x & m;
+    if (OP == OP_AND) return x & y;
+    if (OP == OP_OR) return x | y;
+    if (OP == OP_NEXT) return (x << 1) & LTL_PAIR_SHL1_MASK;
+    if (OP == OP_FINALLY) {
+        const u32 h = (u32)(x >> 32), l = (u32)x;
+        return pack_halves(h | (0u - h), l | (0u - l));
+    }
+    if (OP == OP_GLOBALLY) {  // dual of F inside the mask (reference bitsem.py:133-138)
+        const u64 t = ~x & m;
+        const u32 h = (u32)(t >> 32), l = (u32)t;
+        return ~pack_halves(h | (0u - h), l | (0u - l)) & m;
+    }
+    // OP_UNTIL: y | s | (((x + s) ^ x) & x), s = x & (y << 1), per half
+    const u64 sd = x & ((y << 1) & LTL_PAIR_SHL1_MASK);
+    const u64 t = pack_halves((u32)(x >> 32) + (u32)(sd >> 32), (u32)x + (u32)sd);
+    return y | sd | ((t ^ x) & x);
+}
+
 // out = OP(x [, y]) on one row; m = the row's length mask (used by NOT / GLOBALLY only).
-// x is the left (or only) operand, y the right operand.
-template <int OP, int W>
+// x is the left (or only) operand, y the right operand.  PAIR (W == 1 only): the word holds two 32-bit rows.
+template <int OP, int W, bool PAIR = false>
 __device__ __forceinline__ void apply_row(u64 (&out)[W], const u64 (&x)[W], const u64 (&y)[W], const u64 (&m)[W]) {
+    if (PAIR) {
+        out[0] = apply_pair<OP>(x[0], y[0], m[0]);
+        return;
+    }
     if (OP == OP_IDENT) {
 #pragma unroll
         for (int w = 0; w < W; w++) out[w] = x[w];

@@ -10,13 +10,18 @@ NH fingerprint (`V_NH`; definition `oracle/ltl_oracle.c` fp_nh): two multiply-ad
 MuellerHash's four 64-bit multiplies, which is what bounds the screening kernel.  ``"mueller_blocked"``
 keeps the blocked MuellerHash extension at every size, ``"nh"`` forces NH at every size (tests, A/B runs).
 Inside the reference's domain ``"mueller"`` is the reference's MuellerHash bit for bit.
+
+Whenever NH is selected and no trace has more than 32 positions, the variant is `V_NH32`: NH over row PAIRS
+(definition `oracle/ltl_oracle.c` fp_nh32).  It goes with the device core's half-width store -- two rows per 64-bit
+word, i.e. uint32 storage for L <= 32 (north-star subsystem 1): BASELINE config 4 moves 8 MiB instead of 16 MiB per matrix.
 """
 from __future__ import annotations
 
 from dataclasses import dataclass
 
 FP_BITS = 126
-V_GATHER, V_MUELLER, V_FKP, V_NH = 0, 1, 2, 3
+V_GATHER, V_MUELLER, V_FKP, V_NH, V_NH32 = 0, 1, 2, 3, 4
+HALF_WORD = 32  # rows of at most this many positions are stored two per 64-bit word
 REFERENCE_WORDS = 64  # the reference's largest matrix: 64 rows x one word
 
 
@@ -64,5 +69,7 @@ def resolve_scheme(scheme: HashScheme, lengths, suffix_table=None, words_per_row
     if scheme.variant in ("mueller", "mueller_blocked", "nh"):
         big = len(lengths) * int(words_per_row) > REFERENCE_WORDS
         nh = scheme.variant == "nh" or (scheme.variant == "mueller" and big)
+        if nh and int(words_per_row) == 1 and max((int(n) for n in lengths), default=0) <= HALF_WORD:
+            return ResolvedScheme(V_NH32, mask_k=scheme.mask_bits)
         return ResolvedScheme(V_NH if nh else V_MUELLER, mask_k=scheme.mask_bits)
     return ResolvedScheme(V_FKP, fkp_bits=fkp_bits_per_row(len(lengths)), mask_k=scheme.mask_bits)

@@ -337,12 +337,13 @@ class ShardedCore:
 # ------------------------------------------------------------------------------------------------ row shards
 
 
-def row_slices(n_rows: int, words_per_row: int, world: int):
+def row_slices(n_rows: int, words_per_row: int, world: int, half_width: bool = False):
     """Row range of every shard: equal slices whose word offsets are multiples of 64 (fingerprint blocks must not
-    straddle shards); trailing shards may be short or -- if there are too few rows -- empty (then: ValueError)."""
+    straddle shards); trailing shards may be short or -- if there are too few rows -- empty (then: ValueError).
+    ``half_width``: the core stores two rows per word (variant NH32), so a fingerprint block is 128 rows."""
     import math
 
-    unit = 64 // math.gcd(64, words_per_row)  # rows per whole number of 64-word blocks
+    unit = 128 if half_width else 64 // math.gcd(64, words_per_row)  # rows per whole number of 64-word blocks
     per = -(-n_rows // world)
     per = -(-per // unit) * unit
     out = [(min(n_rows, g * per), min(n_rows, (g + 1) * per)) for g in range(world)]
@@ -439,7 +440,7 @@ def row_sharded_core_factory(comm, local_factory: Callable | None = None, **opti
         W = int(words_per_row)
         m = np.ascontiguousarray(masks, dtype=np.uint64).reshape(-1)
         n_rows = len(m) // W
-        r0, r1 = row_slices(n_rows, W, comm.world)[comm.rank]
+        r0, r1 = row_slices(n_rows, W, comm.world, half_width=int(variant) == 4)[comm.rank]
         if local_factory is None:
             from .core import make_core as factory
         else:
@@ -477,7 +478,7 @@ def sharded_core_factory(comm, local_factory: Callable | None = None, **options)
 # ------------------------------------------------------------------------------------------------ bench (N > 1)
 
 
-def bench_main(args, spec, alphabet, planted, cfg_desc, sampler=None, peaks=None):
+def bench_main(args, spec, alphabet, planted, cfg_desc, sampler=None, peaks=None, cpu_baseline_fn=None):
     """`bench.py --gpus N` under torchrun: every rank runs the same search, sharded; device time of the K
     level loops, max over ranks; rank 0 prints the JSON line."""
     import json
@@ -496,12 +497,14 @@ def bench_main(args, spec, alphabet, planted, cfg_desc, sampler=None, peaks=None
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     comm = TorchComm()
     max_cost = cfg_desc["max_cost"]
+    from .scheme import HashScheme
+
     lcfg = LearnerConfig(ceiling=max_cost + 1, budget_bytes=int(args.budget_gb * (1 << 30)), device=local_rank,
-                         pack_on_device=True)
+                         pack_on_device=True, hash=HashScheme(getattr(args, "hash", "mueller")))
     mode = getattr(args, "sharding", "auto")
     if mode == "auto":
         try:
-            row_slices(spec.size, -(-spec.max_len // 64), comm.world)
+            row_slices(spec.size, -(-spec.max_len // 64), comm.world, half_width=spec.max_len <= 32)
             mode = "rows"
         except ValueError:
             mode = "candidates"
@@ -593,8 +596,9 @@ def bench_main(args, spec, alphabet, planted, cfg_desc, sampler=None, peaks=None
                         "frac": ach / peak, "traffic": None, "peak_source": peak_src,
                         "alg_bytes_per_launch": scr_bytes / max(scr_launch, 1), "ms_per_launch": scr_ms / max(scr_launch, 1),
                         "kernel_ms_by_class": {k: round(sum(ks[k]["ms"] for ks in kstats), 3) for k in kstats[0]}}
+        cpu = cpu_baseline_fn() if cpu_baseline_fn is not None else None  # rank 0's host cores, after the timed regions
         print(json.dumps({
-            "clocks": clocks, "roofline": roofline, "cpu_baseline": None,
+            "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu,
             "metric": "candidates_per_sec", "value": value, "unit": "candidates/s", "n_gpus": comm.world,
             "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u64", "data": "synthetic",

@@ -20,8 +20,14 @@ for c in $cfgs; do
   n=$(grep -c k_screen gpurun_out/${tag}_launches_$c.csv)
   n=$((n / 6))
   skip=$((n > 3 ? n - 3 : 0))
-  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_screen -s $skip -c 3 -f -o gpurun_out/${tag}_full_$c \
+  # reports stay in /tmp on the box (gpurun_out is capped at 64 MiB): the raw and source pages come back as CSV
+  timeout 1500 ncu --set full --clock-control none --import-source on -k regex:k_screen -s $skip -c 3 -f -o /tmp/${tag}_full_$c \
       python scripts/profile_target.py --config $c $extra > gpurun_out/${tag}_full_$c.log 2>&1
   tail -2 gpurun_out/${tag}_full_$c.log
+  ncu -i /tmp/${tag}_full_$c.ncu-rep --page raw --csv > gpurun_out/${tag}_full_${c}_raw.csv 2>/dev/null
+  ncu -i /tmp/${tag}_full_$c.ncu-rep --page source --csv 2>/dev/null | gzip > gpurun_out/${tag}_full_${c}_source.csv.gz
+  sz=$(stat -c %s /tmp/${tag}_full_$c.ncu-rep 2>/dev/null || echo 0)
+  [ "$sz" -gt 0 ] && [ "$sz" -lt 12000000 ] && cp /tmp/${tag}_full_$c.ncu-rep gpurun_out/
+  du -sh gpurun_out
 done
 date

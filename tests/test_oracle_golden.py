@@ -179,3 +179,25 @@ def test_scheme_selects_nh_only_beyond_the_reference_domain():
     assert S.resolve_scheme(S.HashScheme("nh"), long_rows).variant == S.V_NH
     assert S.resolve_scheme(S.HashScheme("fkp"), [63] * 65).variant == S.V_FKP
     assert S.resolve_scheme(S.HashScheme(), [5] * 8).variant == S.V_GATHER              # precise mode is unaffected
+
+
+def test_nh32_is_nh_over_row_pairs():
+    """V_NH32 (traces of at most 32 positions): NH over virtual words holding two rows each -- the value the device's
+    half-width store hashes.  Independent restatement: pack the pairs in numpy, hash with the Python NH above."""
+    from paper_2402_12373_b200 import scheme as S
+
+    rng = np.random.default_rng(5)
+    for R in (1, 2, 3, 64, 65, 127, 128, 129, 1000, 1025):
+        core = cpu_oracle.OracleCore(np.full(R, 0xFFFFFFFF00000000, dtype=np.uint64), 1, 0, cpu_oracle.V_NH32)
+        for _ in range(3):
+            cm = rng.integers(0, 1 << 32, size=R, dtype=np.uint64) << np.uint64(32)
+            padded = np.concatenate([cm, np.zeros(R % 2, dtype=np.uint64)])
+            virtual = padded[0::2] | (padded[1::2] >> np.uint64(32))
+            assert core.fingerprint_of(cm) == _nh_python(virtual)
+    assert S.resolve_scheme(S.HashScheme(), [32] * 65).variant == S.V_NH32
+    assert S.resolve_scheme(S.HashScheme(), [33] * 65).variant == S.V_NH
+    assert S.resolve_scheme(S.HashScheme(), [32] * 64).variant == S.V_MUELLER      # inside the reference's domain
+    assert S.resolve_scheme(S.HashScheme("nh"), [20] * 40).variant == S.V_NH32
+    assert S.resolve_scheme(S.HashScheme("mueller_blocked"), [32] * 65).variant == S.V_MUELLER
+    with pytest.raises(ValueError):
+        cpu_oracle.OracleCore(np.zeros(4, dtype=np.uint64), 1, 0, cpu_oracle.V_NH32, words_per_row=2)
