@@ -99,6 +99,40 @@ LTL_API int ltl_device_count(void);
 LTL_API int ltl_pack_traces(const uint16_t* chars, const int64_t* lengths, int64_t R, int L, int n_props, int W, int device,
                             uint64_t* masks_out, uint64_t* atoms_out);
 
+/* ---- Device-resident specification (for specifications of many traces; no reference counterpart as an object) -------
+ * What the reference does on the host before a search, done on the device so that a 2^21-trace specification is
+ * uploaded once and nothing comes back but counters:
+ *   ltl_traces_create  uploads the character matrices (positives, then negatives: the row order of every matrix,
+ *                      reference traces.py:81-83; both uint16[rows][L], entries at positions >= length ignored), hashes
+ *                      every trace to 128 bits and files the hashes with atomicMin(row): rows that are not the first
+ *                      holder of their hash are SUSPECTS of being duplicates (reference traces.py:64-106 de-duplicates
+ *                      per side and refuses P and N sharing a trace) -- the host compares exactly those few rows;
+ *                      also the census of the closed-form overfit cost (reference formula.py:230-250)
+ *   ltl_traces_pack    trace packing (reference bitsem.py:73-88) into device-resident masks / atoms, plus the error
+ *                      counts of every bare proposition and its negation (atom fast path, enumerator.py:182-192)
+ *   ltl_traces_info    out[48]: 0 rows, 1 positives, 2 words per row, 3 max length, 4 min length, 5 non-empty traces,
+ *                      6 OR of all characters, 7 positions of the positive traces, 8 set proposition bits of the positive
+ *                      traces, 9 suspects, 10 empty positive traces, 11 propositions packed, 12 / 13 bytes copied
+ *                      host->device / device->host, 16 + p errors of proposition p, 32 + p errors of its negation
+ *   ltl_traces_suspects  (row, first row with the same hash) pairs, returns how many were written
+ *   ltl_traces_export  host copies of the packed masks[R*W] and atoms[n_props][R*W] (tools, tests)
+ *   ltl_core_create_on_traces / ltl_core_add_atom  a core over the packed traces (masks stay in HBM) and the
+ *                      admission of a proposition's matrix (negated != 0: its negation inside the mask, for the NNF
+ *                      fragment, reference enumerator.py:223-230) -- add_entry without the host round trip */
+typedef struct ltl_traces ltl_traces;
+LTL_API int ltl_traces_create(const uint16_t* pos_chars, const int64_t* pos_lengths, int64_t n_pos, const uint16_t* neg_chars,
+                              const int64_t* neg_lengths, int64_t n_neg, int L, int device, ltl_traces** out);
+LTL_API void ltl_traces_destroy(ltl_traces* t);
+LTL_API const char* ltl_traces_last_error(const ltl_traces* t); /* t may be NULL: last create() failure */
+LTL_API int ltl_traces_pack(ltl_traces* t, int n_props);
+LTL_API int ltl_traces_info(ltl_traces* t, uint64_t out[48]);
+LTL_API int ltl_traces_suspects(ltl_traces* t, int64_t* pairs, int64_t cap_pairs);
+LTL_API int ltl_traces_export(ltl_traces* t, uint64_t* masks_out, uint64_t* atoms_out);
+LTL_API int ltl_core_create_on_traces(ltl_traces* t, int err_max, int variant, const int32_t* proj_rows,
+                                      const int32_t* proj_offs, int n_proj, int fkp_bits, int mask_k, uint64_t budget_bytes,
+                                      ltl_core** out);
+LTL_API int ltl_core_add_atom(ltl_core* h, ltl_traces* t, int prop, int negated, int op, int lhs, int rhs, int64_t* index_out);
+
 /* Constructor: reference _speedups.pyx:79-111 (Core.__cinit__) / kernels.py:140-172 (make_core).
  * masks: uint64[R*W] length masks.  proj_rows/proj_offs (n_proj <= 126 pairs): gather projection
  * (row, position).  fkp_bits: per-row prefix width of the fkp variant.  mask_k: low fingerprint bits

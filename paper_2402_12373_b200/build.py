@@ -57,7 +57,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and os.path.exists(LIB) and os.path.exists(stamp) and open(stamp).read() == digest:
         return LIB
     os.makedirs(OBJ, exist_ok=True)
-    jobs = [(os.path.join(CSRC, "core.cu"), os.path.join(OBJ, "core.o"), [])]
+    jobs = [(os.path.join(CSRC, "core.cu"), os.path.join(OBJ, "core.o"), []),
+            (os.path.join(CSRC, "traces.cu"), os.path.join(OBJ, "traces.o"), [])]
     for w in range(1, MAX_W + 1):
         jobs.append((os.path.join(CSRC, "screen_inst.cu"), os.path.join(OBJ, f"screen_w{w}.o"), [f"-DLTL_W={w}"]))
     jobs.append((os.path.join(CSRC, "screen_inst.cu"), os.path.join(OBJ, "screen_w1p.o"), ["-DLTL_W=1", "-DLTL_PAIR"]))

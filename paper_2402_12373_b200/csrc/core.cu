@@ -22,6 +22,7 @@
 
 #include "../../include/ltl_core.h"
 #include "screen.cuh"
+#include "traces.cuh"
 
 // ------------------------------------------------------------------------------------------------
 // per-W launchers (screen_inst.cu)
@@ -199,6 +200,26 @@ __global__ void __launch_bounds__(RES_CTA) k_emit(const u32* __restrict__ flagw,
     rec_op[e] = (unsigned char)pc.op;
     rec_lhs[e] = (int)i;
     rec_rhs[e] = (int)j;
+}
+
+// entry e <- proposition words resident on the device (ltl_traces): optionally negated inside the mask, optionally
+// packed two rows per word (half-width store).  n = stored words per entry, R = rows (one word each when pair).
+__global__ void k_import_dev(const u64* __restrict__ src, const u64* __restrict__ masks, int negated, int pair, i64 R,
+                             u64* __restrict__ cms, i64 e, i64 n) {
+    const i64 k = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    auto val = [&](i64 i) -> u64 { return negated ? ~src[i] & masks[i] : src[i]; };
+    u64 word;
+    if (pair) word = (val(2 * k) & 0xFFFFFFFF00000000ull) | (2 * k + 1 < R ? val(2 * k + 1) >> 32 : 0ull);
+    else word = val(k);
+    cms[cm_index(e, n, k)] = word;
+}
+
+// masks of the half-width store from one-word row masks
+__global__ void k_pack_pairs(const u64* __restrict__ rows, i64 R, u64* __restrict__ out, i64 n) {
+    const i64 k = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (k >= n) return;
+    out[k] = (rows[2 * k] & 0xFFFFFFFF00000000ull) | (2 * k + 1 < R ? rows[2 * k + 1] >> 32 : 0ull);
 }
 
 __global__ void k_import(const u64* __restrict__ stage, u64* __restrict__ cms, i64 e, i64 n) {
@@ -1645,16 +1666,19 @@ void ltl_core_destroy(ltl_core* h) {
     delete h;
 }
 
-int ltl_core_create(const uint64_t* masks, int R, int W, int n_pos, int err_max, int variant, const int32_t* proj_rows,
-                    const int32_t* proj_offs, int n_proj, int fkp_bits, int mask_k, uint64_t budget_bytes, int device,
-                    ltl_core** out) {
+}  // extern "C"
+
+// masks: host length masks, or null with `tr`: the masks packed on the device by ltl_traces_pack
+static int core_create_impl(const uint64_t* masks, const ltl_traces* tr, int R, int W, int n_pos, int err_max, int variant,
+                            const int32_t* proj_rows, const int32_t* proj_offs, int n_proj, int fkp_bits, int mask_k,
+                            uint64_t budget_bytes, int device, ltl_core** out) {
     if (!out) return LTL_ERR_ARG;
     *out = nullptr;
     auto bad = [&](const char* m) {
         g_create_error = m;
         return LTL_ERR_ARG;
     };
-    if (!masks || R < 1) return bad("need at least one row");
+    if ((!masks && !tr) || R < 1) return bad("need at least one row");
     if (W < 1 || W > LTL_MAX_W) return bad("words per row must lie in [1, 16]");
     if (n_pos < 0 || n_pos > R) return bad("n_pos outside [0, R]");
     if (variant < 0 || variant > VAR_NH32) return bad("unknown fingerprint variant");
@@ -1743,10 +1767,16 @@ int ltl_core_create(const uint64_t* masks, int R, int W, int n_pos, int err_max,
             CK(cudaMallocHost(&h->h_stage, (size_t)h->n * 8));
             h->stage_cap = h->n;
         }
-        if (h->pair) pack_pairs(masks, h->R_api, h->h_stage);
-        else memcpy(h->h_stage, masks, (size_t)h->n * 8);  // pinned staging: the copy below is truly asynchronous
-        CK(cudaMemcpyAsync(h->d_masks, h->h_stage, (size_t)h->n * 8, cudaMemcpyHostToDevice, h->stream));
-        h->h2d_bytes += (size_t)h->n * 8;
+        if (tr) {  // the masks are in HBM already (the traces' stream is idle: ltl_traces_pack waits for its kernel)
+            if (h->pair) k_pack_pairs<<<(unsigned)((h->n + 255) / 256), 256, 0, h->stream>>>(tr->d_masks, h->R_api, h->d_masks, h->n);
+            else CK(cudaMemcpyAsync(h->d_masks, tr->d_masks, (size_t)h->n * 8, cudaMemcpyDeviceToDevice, h->stream));
+            CK(cudaGetLastError());
+        } else {
+            if (h->pair) pack_pairs(masks, h->R_api, h->h_stage);
+            else memcpy(h->h_stage, masks, (size_t)h->n * 8);  // pinned staging: the copy below is truly asynchronous
+            CK(cudaMemcpyAsync(h->d_masks, h->h_stage, (size_t)h->n * 8, cudaMemcpyHostToDevice, h->stream));
+            h->h2d_bytes += (size_t)h->n * 8;
+        }
         std::vector<Deposit> deps;
         int r2 = build_deposits(h, proj_rows, proj_offs, n_proj, deps);
         if (r2) return r2;
@@ -1785,6 +1815,34 @@ int ltl_core_create(const uint64_t* masks, int R, int W, int n_pos, int err_max,
     return LTL_OK;
 }
 
+extern "C" {
+
+int ltl_core_create(const uint64_t* masks, int R, int W, int n_pos, int err_max, int variant, const int32_t* proj_rows,
+                    const int32_t* proj_offs, int n_proj, int fkp_bits, int mask_k, uint64_t budget_bytes, int device,
+                    ltl_core** out) {
+    if (!masks) {
+        g_create_error = "need at least one row";
+        return LTL_ERR_ARG;
+    }
+    return core_create_impl(masks, nullptr, R, W, n_pos, err_max, variant, proj_rows, proj_offs, n_proj, fkp_bits, mask_k,
+                            budget_bytes, device, out);
+}
+
+int ltl_core_create_on_traces(ltl_traces* t, int err_max, int variant, const int32_t* proj_rows, const int32_t* proj_offs,
+                              int n_proj, int fkp_bits, int mask_k, uint64_t budget_bytes, ltl_core** out) {
+    if (!t || !t->n_props) {
+        g_create_error = "create_on_traces: the traces are not packed (ltl_traces_pack)";
+        return LTL_ERR_ARG;
+    }
+    if (t->R > 0x7FFFFFFF) {
+        g_create_error = "create_on_traces: too many rows";
+        return LTL_ERR_ARG;
+    }
+    int rc = core_create_impl(nullptr, t, (int)t->R, t->W, (int)t->n_pos, err_max, variant, proj_rows, proj_offs, n_proj, fkp_bits,
+                              mask_k, budget_bytes, t->device, out);
+    return rc;
+}
+
 #define ENTER(h)                              \
     if (!(h)) return LTL_ERR_ARG;             \
     {                                         \
@@ -1804,6 +1862,35 @@ int ltl_core_add_entry(ltl_core* h, const uint64_t* cm, int op, int lhs, int rhs
     if (co.status == LTL_S_OOM) return h->fail(LTL_ERR_BUDGET, "memory budget exhausted");
     if (co.admitted == 1) {
         ScopedTimer t(h, LTL_K_MISC, 1, 9.0);
+        k_set_record<<<1, 1, 0, h->stream>>>((unsigned char*)h->rec_op.base, (int*)h->rec_lhs.base, (int*)h->rec_rhs.base, e, op,
+                                             lhs, rhs);
+        CK(cudaGetLastError());
+        *index_out = e;
+    }
+    return LTL_OK;
+}
+
+int ltl_core_add_atom(ltl_core* h, ltl_traces* t, int prop, int negated, int op, int lhs, int rhs, int64_t* index_out) {
+    ENTER(h);
+    if (!t || !index_out) return h->fail(LTL_ERR_ARG, "null argument");
+    *index_out = -1;
+    if (t->device != h->device || t->R * t->W != h->n_api || prop < 0 || prop >= t->n_props)
+        return h->fail(LTL_ERR_ARG, "add_atom: the traces do not belong to this core (device, shape or proposition)");
+    const i64 e = (i64)h->n_entries;
+    int rc;
+    if ((rc = ensure_entries(h, (u64)e + 1))) return rc;
+    {
+        ScopedTimer tm(h, LTL_K_MISC, 1, 16.0 * (double)h->n);
+        k_import_dev<<<(unsigned)((h->n + 255) / 256), 256, 0, h->stream>>>(t->d_atoms + (size_t)prop * (size_t)h->n_api, t->d_masks,
+                                                                              negated ? 1 : 0, h->pair ? 1 : 0, h->R_api,
+                                                                              (u64*)h->cms.base, e, h->n);
+    }
+    CK(cudaGetLastError());
+    ChunkOut co;
+    if ((rc = single_chunk(h, e, MODE_INSERT, &co))) return rc;
+    if (co.status == LTL_S_OOM) return h->fail(LTL_ERR_BUDGET, "memory budget exhausted");
+    if (co.admitted == 1) {
+        ScopedTimer tm(h, LTL_K_MISC, 1, 9.0);
         k_set_record<<<1, 1, 0, h->stream>>>((unsigned char*)h->rec_op.base, (int*)h->rec_lhs.base, (int*)h->rec_rhs.base, e, op,
                                              lhs, rhs);
         CK(cudaGetLastError());
