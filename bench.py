@@ -339,10 +339,8 @@ def measure_config(config: str, args, *, steps: int, warmup: int, cpu_cost: int 
     from paper_2402_12373_b200 import workloads as Wl
     from paper_2402_12373_b200.core import make_core
     from paper_2402_12373_b200.formula import print_formula
-    from paper_2402_12373_b200.learner import Enumeration, LearnerConfig, Solved, learn
+    from paper_2402_12373_b200.learner import Enumeration, LearnerConfig, Solved, as_specification, learn
     from paper_2402_12373_b200.scheme import HashScheme
-    from paper_2402_12373_b200.traces import Specification
-
     spec, alphabet, planted, wl = Wl.make_config(config)
     max_cost = (args.max_cost if config == args.config and args.max_cost else None) or wl["max_cost"]
     cfg_desc = workload_desc(config, spec, wl, planted, alphabet, max_cost, args.hash)
@@ -415,7 +413,8 @@ def measure_config(config: str, args, *, steps: int, warmup: int, cpu_cost: int 
 
     def e2e_once():
         ta = time.perf_counter()
-        s = Specification.from_arrays(pos_c, pos_l, neg_c, neg_l)
+        # host arrays in: uploaded, screened for duplicates, censused and packed on the device (core.DeviceTraces)
+        s = as_specification((pos_c, pos_l), (neg_c, neg_l), device=local_rank)
         tb = time.perf_counter()
         out = learn(s, None, alphabet, max_cost=max_cost, budget_bytes=budget, device=local_rank,
                     hash=HashScheme(args.hash))

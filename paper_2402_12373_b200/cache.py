@@ -26,7 +26,17 @@ class LanguageCache:
         op, lhs, rhs = record
         if cost < self._frontier:
             raise ValueError(f"bucket for cost {cost} is frozen")
-        idx = self.core.add_entry(np.asarray(cm, dtype=np.uint64), op, lhs, rhs)
+        return self._book(self.core.add_entry(np.asarray(cm, dtype=np.uint64), op, lhs, rhs), cost)
+
+    def try_admit_atom(self, traces, prop: int, negated: bool, record, cost: int) -> bool:
+        """`try_admit` of a proposition's matrix (or its negation) taken from device-resident packed traces
+        (`CudaCore.add_atom`): no matrix crosses the host."""
+        op, lhs, rhs = record
+        if cost < self._frontier:
+            raise ValueError(f"bucket for cost {cost} is frozen")
+        return self._book(self.core.add_atom(traces, prop, negated, op, lhs, rhs), cost)
+
+    def _book(self, idx: int, cost: int) -> bool:
         if idx < 0:
             return False
         rng = self._buckets.setdefault(cost, [idx, idx])

@@ -90,6 +90,22 @@ def load_library():
     L.ltl_pool_trim.restype = C.c_uint64
     L.ltl_pack_traces.argtypes = [C.POINTER(C.c_uint16), i64p, C.c_int64, C.c_int, C.c_int, C.c_int, C.c_int, u64p, u64p]
     L.ltl_pack_traces.restype = C.c_int
+    u16p = C.POINTER(C.c_uint16)
+    L.ltl_traces_create.argtypes = [u16p, i64p, C.c_int64, u16p, i64p, C.c_int64, C.c_int, C.c_int, C.POINTER(vp)]
+    L.ltl_traces_destroy.argtypes = [vp]
+    L.ltl_traces_destroy.restype = None
+    L.ltl_traces_last_error.argtypes = [vp]
+    L.ltl_traces_last_error.restype = C.c_char_p
+    L.ltl_traces_pack.argtypes = [vp, C.c_int]
+    L.ltl_traces_info.argtypes = [vp, u64p]
+    L.ltl_traces_suspects.argtypes = [vp, i64p, C.c_int64]
+    L.ltl_traces_export.argtypes = [vp, u64p, u64p]
+    L.ltl_core_create_on_traces.argtypes = [vp, C.c_int, C.c_int, i32p, i32p, C.c_int, C.c_int, C.c_int, C.c_uint64,
+                                            C.POINTER(vp)]
+    L.ltl_core_add_atom.argtypes = [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, i64p]
+    for name in ("ltl_traces_create", "ltl_traces_pack", "ltl_traces_info", "ltl_traces_suspects", "ltl_traces_export",
+                 "ltl_core_create_on_traces", "ltl_core_add_atom"):
+        getattr(L, name).restype = C.c_int
     L.ltl_core_level_size.argtypes = [vp, C.POINTER(Segment), C.c_int, i64p]
     L.ltl_core_stage_eval.argtypes = [vp, C.POINTER(Segment), C.c_int, C.c_int64, C.c_int64, vp, i64p]
     L.ltl_core_stage_file.argtypes = [vp, vp, C.c_int64, vp, i64p]
@@ -148,18 +164,107 @@ def pack_traces(chars: np.ndarray, lengths: np.ndarray, n_props: int, words_per_
     return masks, atoms
 
 
+class DeviceTraces:
+    """A specification resident in HBM (`include/ltl_core.h: ltl_traces_*`): the padded character matrices are uploaded
+    once; duplicate screening (reference `traces.py:64-106`), the census of the overfit cost (`formula.py:230-250`),
+    trace packing (`bitsem.py:73-88`) and the atom fast path's error counts (`enumerator.py:182-192`) run on the device
+    and only counters come back.  `CudaCore.on_traces` / `CudaCore.add_atom` consume the packed masks / atoms in place."""
+
+    INFO_WORDS = 48
+
+    def __init__(self, pos_chars, pos_lengths, neg_chars, neg_lengths, device: int = 0):
+        L = load_library()
+        if device_count() <= 0:
+            raise BackendUnavailable("no CUDA device visible (there is no CPU fallback)")
+        pl = np.ascontiguousarray(pos_lengths, dtype=np.int64).reshape(-1)
+        nl = np.ascontiguousarray(neg_lengths, dtype=np.int64).reshape(-1)
+        pc = np.ascontiguousarray(pos_chars, dtype=np.uint16).reshape(len(pl), -1)
+        nc = np.ascontiguousarray(neg_chars, dtype=np.uint16).reshape(len(nl), -1)
+        width = max(pc.shape[1] if len(pl) else 0, nc.shape[1] if len(nl) else 0)
+        if len(pl) and pc.shape[1] != width:
+            pc = np.ascontiguousarray(np.pad(pc, ((0, 0), (0, width - pc.shape[1]))))
+        if len(nl) and nc.shape[1] != width:
+            nc = np.ascontiguousarray(np.pad(nc, ((0, 0), (0, width - nc.shape[1]))))
+        if (len(pl) and (int(pl.min()) < 0 or int(pl.max()) > width)) or (len(nl) and (int(nl.min()) < 0 or int(nl.max()) > width)):
+            raise ValueError("trace lengths must lie in [0, row width]")
+        self._L, self._h = L, C.c_void_p()
+        self.device_index = int(device)
+        u16p, i64p = C.POINTER(C.c_uint16), C.POINTER(C.c_int64)
+        rc = L.ltl_traces_create(pc.ctypes.data_as(u16p), pl.ctypes.data_as(i64p), len(pl), nc.ctypes.data_as(u16p),
+                                 nl.ctypes.data_as(i64p), len(nl), int(width), int(device), C.byref(self._h))
+        if rc:
+            msg = (L.ltl_traces_last_error(None) or b"").decode()
+            self._h = None
+            if rc == ERR_ARG:
+                raise ValueError(msg)
+            if rc == ERR_CUDA:
+                raise BackendUnavailable(f"CUDA core unavailable: {msg} (there is no CPU fallback)")
+            raise CoreError(msg)
+
+    def close(self):
+        h, self._h = getattr(self, "_h", None), None
+        if h:
+            self._L.ltl_traces_destroy(h)
+
+    __del__ = close
+
+    def _check(self, rc):
+        if rc == 0:
+            return
+        msg = (self._L.ltl_traces_last_error(self._h) or b"").decode()
+        if rc == ERR_ARG:
+            raise ValueError(msg)
+        raise CoreError(f"[{rc}] {msg}")
+
+    def info(self) -> dict:
+        out = np.zeros(self.INFO_WORDS, dtype=np.uint64)
+        self._check(self._L.ltl_traces_info(self._h, _u64(out)))
+        keys = ("rows", "n_pos", "words", "max_len", "min_len", "non_empty", "char_or", "pos_positions", "pos_bits",
+                "suspects", "empty_pos", "n_props", "h2d_bytes", "d2h_bytes")
+        d = {k: int(v) for k, v in zip(keys, out)}
+        d["atom_errors"] = [int(v) for v in out[16:32]]
+        d["neg_atom_errors"] = [int(v) for v in out[32:48]]
+        return d
+
+    def suspects(self) -> np.ndarray:
+        """int64[k, 2]: (row, first row with the same 128-bit hash) -- candidates for being duplicate traces."""
+        n = self.info()["suspects"]
+        pairs = np.zeros((max(n, 1), 2), dtype=np.int64)
+        got = self._L.ltl_traces_suspects(self._h, pairs.ctypes.data_as(C.POINTER(C.c_int64)), n)
+        if got < 0:
+            self._check(got)
+        return pairs[:got]
+
+    def pack(self, n_props: int):
+        self._check(self._L.ltl_traces_pack(self._h, int(n_props)))
+
+    def export(self):
+        """Host copies of the packed masks ``uint64[R, W]`` and atoms ``uint64[n_props, R, W]`` (tools, tests)."""
+        i = self.info()
+        R, W, n_props = i["rows"], i["words"], i["n_props"]
+        masks = np.empty((R, W), dtype=np.uint64)
+        atoms = np.empty((max(n_props, 1), R, W), dtype=np.uint64)
+        self._check(self._L.ltl_traces_export(self._h, _u64(masks), _u64(atoms)))
+        return masks, atoms[:n_props]
+
+
 class CudaCore:
     """Device-resident screening core (matrices, records, uniqueness table live in HBM)."""
 
     def __init__(self, masks, n_pos, err_max, variant, proj_rows: Sequence[int] = (), proj_offs: Sequence[int] = (),
                  fkp_bits=0, mask_k=0, budget_bytes=2 << 30, *, words_per_row=1, device=0, chunk_candidates=None,
-                 profile=False):
+                 profile=False, traces: "DeviceTraces | None" = None):
         L = load_library()
-        m = np.ascontiguousarray(masks, dtype=np.uint64).reshape(-1)
-        W = int(words_per_row)
+        if traces is not None:  # masks are in HBM already (DeviceTraces.pack): `masks` is ignored
+            ti = traces.info()
+            W, n_words = ti["words"], ti["rows"] * ti["words"]
+            n_pos, device = ti["n_pos"], traces.device_index
+        else:
+            m = np.ascontiguousarray(masks, dtype=np.uint64).reshape(-1)
+            W, n_words = int(words_per_row), len(m)
         if W < 1 or W > MAX_WORDS_PER_ROW:
             raise ValueError(f"words_per_row must lie in [1, {MAX_WORDS_PER_ROW}]")
-        if len(m) == 0 or len(m) % W:
+        if n_words == 0 or n_words % W:
             raise ValueError("masks length must be a positive multiple of words_per_row")
         pr = np.ascontiguousarray(list(proj_rows), dtype=np.int32)
         po = np.ascontiguousarray(list(proj_offs), dtype=np.int32)
@@ -167,14 +272,19 @@ class CudaCore:
             raise ValueError("proj_rows and proj_offs differ in length")
         if len(pr) > 126:
             raise ValueError("projection wider than the fingerprint")  # reference `_speedups.pyx:92-93`
-        self.R, self.W, self.n = len(m) // W, W, len(m)
+        self.R, self.W, self.n = n_words // W, W, n_words
         self.device_index = int(device)
         self._L = L
         self._h = C.c_void_p()
         i32p = C.POINTER(C.c_int32)
-        rc = L.ltl_core_create(_u64(m), self.R, W, int(n_pos), int(err_max), int(variant), pr.ctypes.data_as(i32p),
-                               po.ctypes.data_as(i32p), len(pr), int(fkp_bits), int(mask_k), int(budget_bytes),
-                               int(device), C.byref(self._h))
+        if traces is not None:
+            rc = L.ltl_core_create_on_traces(traces._h, int(err_max), int(variant), pr.ctypes.data_as(i32p),
+                                             po.ctypes.data_as(i32p), len(pr), int(fkp_bits), int(mask_k),
+                                             int(budget_bytes), C.byref(self._h))
+        else:
+            rc = L.ltl_core_create(_u64(m), self.R, W, int(n_pos), int(err_max), int(variant), pr.ctypes.data_as(i32p),
+                                   po.ctypes.data_as(i32p), len(pr), int(fkp_bits), int(mask_k), int(budget_bytes),
+                                   int(device), C.byref(self._h))
         if rc:
             msg = (L.ltl_core_last_error(None) or b"").decode()
             self._h = None
@@ -235,6 +345,14 @@ class CudaCore:
     def add_entry(self, cm, op, lhs, rhs) -> int:
         idx = C.c_int64()
         self._check(self._L.ltl_core_add_entry(self._h, _u64(self._cm(cm)), int(op), int(lhs), int(rhs), C.byref(idx)))
+        return int(idx.value)
+
+    def add_atom(self, traces: DeviceTraces, prop: int, negated: bool, op, lhs, rhs) -> int:
+        """`add_entry` of a proposition's characteristic matrix (``negated``: its negation inside the length mask) taken
+        from the device-resident packed traces -- no host round trip."""
+        idx = C.c_int64()
+        self._check(self._L.ltl_core_add_atom(self._h, traces._h, int(prop), int(bool(negated)), int(op), int(lhs),
+                                              int(rhs), C.byref(idx)))
         return int(idx.value)
 
     def contains(self, cm) -> bool:
@@ -469,6 +587,7 @@ class CudaCore:
 
 def make_core(masks, n_pos, err_max, variant, proj_rows=(), proj_offs=(), fkp_bits=0, mask_k=0,
               budget_bytes=2 << 30, *, words_per_row=1, device=0, **options) -> CudaCore:
-    """The drop-in for reference `kernels.make_core` (`kernels.py:140-172`): always the CUDA core."""
+    """The drop-in for reference `kernels.make_core` (`kernels.py:140-172`): always the CUDA core.
+    ``traces=DeviceTraces`` (keyword): a core over a specification already packed in HBM (``masks`` may be None)."""
     return CudaCore(masks, n_pos, err_max, variant, proj_rows, proj_offs, fkp_bits, mask_k, budget_bytes,
                     words_per_row=words_per_row, device=device, **options)

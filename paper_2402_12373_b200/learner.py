@@ -151,7 +151,7 @@ def _validate(spec: Specification, alphabet: Alphabet, cfg: LearnerConfig):
         raise ValueError(f"{spec.size} traces exceed the limit of {cfg.max_traces}")
     if spec.max_len > cfg.max_trace_len:
         raise ValueError(f"trace of length {spec.max_len} exceeds {cfg.max_trace_len}")
-    if (spec.lengths[: spec.n_pos] == 0).any():
+    if spec.n_empty_positive:
         raise ValueError("an empty positive trace can never be satisfied")
     if spec.char_width() > alphabet.size:
         raise ValueError("traces use propositions outside the alphabet")
@@ -237,16 +237,21 @@ class Enumeration:
         # product path (no injected core): packing runs on the device too; an injected core factory (tests with
         # the CPU oracle, the sharded wrapper) gets host-packed inputs
         on_device = cfg.pack_on_device if cfg.pack_on_device is not None else core_factory is None
-        t_pack = time.perf_counter()
-        self.ctx = ctx = TraceContext.from_spec(spec, alphabet, device=cfg.device if on_device else None)
-        n_pos, err_max, h = spec.n_pos, cfg.err_max(spec), cfg.cost
         self.stats = stats = EnumStats()
-        stats.phase_ms["pack"] = 1e3 * (time.perf_counter() - t_pack)
-        stats.ceiling = overfit_cost(spec, alphabet, h)
-        self.ceiling = stats.ceiling if cfg.ceiling is None else min(cfg.ceiling, stats.ceiling)
         self.outcome: EnumOutcome | None = None
         self.core = None
         self.cache = None
+        self._traces = None
+        dev = spec.device_traces
+        if dev is not None and core_factory is None and dev.device_index == cfg.device:
+            self._init_resident(dev)  # the specification is in HBM already: nothing but counters crosses the host
+            return
+        t_pack = time.perf_counter()
+        self.ctx = ctx = TraceContext.from_spec(spec, alphabet, device=cfg.device if on_device else None)
+        n_pos, err_max, h = spec.n_pos, cfg.err_max(spec), cfg.cost
+        stats.phase_ms["pack"] = 1e3 * (time.perf_counter() - t_pack)
+        stats.ceiling = overfit_cost(spec, alphabet, h)
+        self.ceiling = stats.ceiling if cfg.ceiling is None else min(cfg.ceiling, stats.ceiling)
 
         atom_c = h.of(OP_ATOM)
         for p in range(alphabet.size):
@@ -283,6 +288,55 @@ class Enumeration:
         except CoreOOM:
             self.outcome = self._finish(OutOfMemory(stats))
 
+    def _init_resident(self, dev):
+        """`__init__` for a device-resident specification (`Specification.from_arrays(..., device=d)`): packing
+        (`bitsem.py:73-88`), the atom fast path (`enumerator.py:182-192`) and the admission of the atoms (`218-232`) run on
+        the device over the uploaded character matrix; masks and atoms never visit the host."""
+        spec, alphabet, cfg, stats = self.spec, self.alphabet, self.cfg, self.stats
+        err_max, h = cfg.err_max(spec), cfg.cost
+        t_pack = time.perf_counter()
+        dev.pack(alphabet.size)
+        info = dev.info()
+        self.ctx = None
+        self._traces = dev
+        stats.phase_ms["pack"] = 1e3 * (time.perf_counter() - t_pack)
+        stats.ceiling = overfit_cost(spec, alphabet, h)
+        self.ceiling = stats.ceiling if cfg.ceiling is None else min(cfg.ceiling, stats.ceiling)
+        atom_c = h.of(OP_ATOM)
+        for p in range(alphabet.size):
+            if info["atom_errors"][p] <= err_max:
+                stats.atom_fast_path = True
+                self.outcome = Solved(Atom(p), atom_c, stats)
+                return
+        if cfg.require_nnf:
+            for p in range(alphabet.size):
+                if info["neg_atom_errors"][p] <= err_max:
+                    stats.atom_fast_path = True
+                    self.outcome = Solved(Not(Atom(p)), atom_c + h.of(OP_NOT), stats)
+                    return
+        t_scheme = time.perf_counter()
+        words = info["words"]
+        rs = resolve_scheme(cfg.hash, spec.lengths, SuffixTable.from_spec(spec, limit=126), words_per_row=words)
+        stats.precise = rs.precise
+        t_create = time.perf_counter()
+        stats.phase_ms["scheme"] = 1e3 * (t_create - t_scheme)
+        from .core import make_core
+
+        self.core = make_core(None, spec.n_pos, err_max, rs.variant, rs.proj_rows, rs.proj_offs, rs.fkp_bits, rs.mask_k,
+                              cfg.budget_bytes, words_per_row=words, device=cfg.device, traces=dev)
+        self.cache = cache = LanguageCache(self.core)
+        self._t_search = time.perf_counter()
+        stats.phase_ms["create"] = 1e3 * (self._t_search - t_create)
+        try:
+            admitted_atoms = [p for p in range(alphabet.size)
+                              if cache.try_admit_atom(dev, p, False, (OP_ATOM, p, -1), atom_c)]
+            if cfg.require_nnf:
+                neg_c = atom_c + h.of(OP_NOT)
+                for entry, p in enumerate(admitted_atoms):
+                    cache.try_admit_atom(dev, p, True, (OP_NOT, entry, -1), neg_c)
+        except CoreOOM:
+            self.outcome = self._finish(OutOfMemory(stats))
+
     def _finish(self, outcome):
         core, stats = self.core, self.stats
         _, bytes_used, stats.offered, stats.admitted, stats.duplicates = core.counters()
@@ -291,6 +345,10 @@ class Enumeration:
         stats.search_seconds = time.perf_counter() - self._t_search
         if hasattr(core, "transfer_stats"):
             stats.h2d_bytes, stats.d2h_bytes = core.transfer_stats()
+        if self._traces is not None:  # the upload of the character matrices and the counters read back belong to the search
+            ti = self._traces.info()
+            stats.h2d_bytes += ti["h2d_bytes"]
+            stats.d2h_bytes += ti["d2h_bytes"]
         if not self.keep_core:
             close = getattr(core, "close", None)
             if close:
@@ -355,8 +413,18 @@ class LearnResult:
         return self.status == "solved"
 
 
-def as_specification(P, N) -> Specification:
-    return P if isinstance(P, Specification) and N is None else Specification(P, N)
+def _is_array_pair(x) -> bool:
+    return isinstance(x, tuple) and len(x) == 2 and isinstance(x[0], np.ndarray) and x[0].ndim == 2
+
+
+def as_specification(P, N, device: int | None = None) -> Specification:
+    """``P`` a `Specification` (``N`` None), two iterables of traces, or two ``(chars uint16[k, L], lengths[k])`` array
+    pairs; array pairs are uploaded to ``device`` (when given) and checked there (`Specification.from_arrays`)."""
+    if isinstance(P, Specification) and N is None:
+        return P
+    if _is_array_pair(P) and _is_array_pair(N):
+        return Specification.from_arrays(P[0], P[1], N[0], N[1], device=device)
+    return Specification(P, N)
 
 
 def learn(P, N=None, alphabet: Alphabet | int | Sequence[str] | None = None, max_cost: int | None = None,
@@ -367,13 +435,14 @@ def learn(P, N=None, alphabet: Alphabet | int | Sequence[str] | None = None, max
           core_factory: Callable | None = None) -> LearnResult:
     """Learn a minimal LTL formula accepting every trace in ``P`` and rejecting every trace in ``N``.
 
-    ``P`` / ``N``: iterables of traces (each a sequence of int character bitmasks), or ``P`` a
-    `Specification`.  ``alphabet``: an `Alphabet`, a list of proposition names or a proposition
+    ``P`` / ``N``: iterables of traces (each a sequence of int character bitmasks), ``(chars, lengths)`` array
+    pairs (``uint16[k, L]`` character matrix + ``k`` lengths: the form for 10^6 traces, checked and packed on the
+    device), or ``P`` a `Specification`.  ``alphabet``: an `Alphabet`, a list of proposition names or a proposition
     count (default: as many as the traces use).  ``max_cost``: inclusive cost bound (the reference's
     exclusive ``ceiling`` is ``max_cost + 1``, `enumerator.py:236`).  ``costs``: 8 per-connective
     weights `(atom, !, &, |, X, F, G, U)`, default uniform.
     """
-    spec = as_specification(P, N)
+    spec = as_specification(P, N, device if core_factory is None else None)
     if alphabet is None:
         alphabet = Alphabet.default(spec.char_width())
     elif isinstance(alphabet, int):

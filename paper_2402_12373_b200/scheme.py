@@ -59,17 +59,20 @@ def fkp_bits_per_row(n_rows: int) -> int:
 
 
 def resolve_scheme(scheme: HashScheme, lengths, suffix_table=None, words_per_row: int = 1) -> ResolvedScheme:
+    import numpy as np
+
+    lengths = np.asarray(lengths, dtype=np.int64).reshape(-1)  # 2^21 traces: no per-element Python work below
     if suffix_table is not None:
         if suffix_table.count <= FP_BITS:
             return ResolvedScheme(V_GATHER, tuple(suffix_table.rows), tuple(suffix_table.offsets), mask_k=scheme.mask_bits)
-    elif sum(int(n) for n in lengths) <= FP_BITS:
+    elif int(lengths.sum()) <= FP_BITS:
         rows = tuple(r for r, n in enumerate(lengths) for _ in range(int(n)))
         offs = tuple(j for n in lengths for j in range(int(n)))
         return ResolvedScheme(V_GATHER, rows, offs, mask_k=scheme.mask_bits)
     if scheme.variant in ("mueller", "mueller_blocked", "nh"):
         big = len(lengths) * int(words_per_row) > REFERENCE_WORDS
         nh = scheme.variant == "nh" or (scheme.variant == "mueller" and big)
-        if nh and int(words_per_row) == 1 and max((int(n) for n in lengths), default=0) <= HALF_WORD:
+        if nh and int(words_per_row) == 1 and (int(lengths.max()) if len(lengths) else 0) <= HALF_WORD:
             return ResolvedScheme(V_NH32, mask_k=scheme.mask_bits)
         return ResolvedScheme(V_NH if nh else V_MUELLER, mask_k=scheme.mask_bits)
     return ResolvedScheme(V_FKP, fkp_bits=fkp_bits_per_row(len(lengths)), mask_k=scheme.mask_bits)

@@ -440,7 +440,15 @@ def row_sharded_core_factory(comm, local_factory: Callable | None = None, **opti
         W = int(words_per_row)
         m = np.ascontiguousarray(masks, dtype=np.uint64).reshape(-1)
         n_rows = len(m) // W
-        r0, r1 = row_slices(n_rows, W, comm.world, half_width=int(variant) == 4)[comm.rank]
+        try:
+            r0, r1 = row_slices(n_rows, W, comm.world, half_width=int(variant) == 4)[comm.rank]
+        except ValueError:
+            if int(variant) != 4:
+                raise
+            # too few rows for whole 128-row blocks of the half-width store on every shard: full-width NH instead
+            # (search results do not depend on which collision-free fingerprint is used, DESIGN 3)
+            variant = 3
+            r0, r1 = row_slices(n_rows, W, comm.world)[comm.rank]
         if local_factory is None:
             from .core import make_core as factory
         else:

@@ -165,11 +165,83 @@ class Specification:
         self._build(pc, pl, nc, nl)
 
     @staticmethod
-    def from_arrays(pos_chars, pos_lengths, neg_chars, neg_lengths) -> "Specification":
-        """Array form: ``chars[k, j]`` is character j of trace k (entries at j >= length ignored)."""
-        pc = np.ascontiguousarray(pos_chars, dtype=np.uint16).reshape(len(pos_lengths), -1)
-        nc = np.ascontiguousarray(neg_chars, dtype=np.uint16).reshape(len(neg_lengths), -1)
-        return Specification(_arrays=(pc, np.asarray(pos_lengths, dtype=np.int64), nc, np.asarray(neg_lengths, dtype=np.int64)))
+    def from_arrays(pos_chars, pos_lengths, neg_chars, neg_lengths, *, device: int | None = None) -> "Specification":
+        """Array form: ``chars[k, j]`` is character j of trace k (entries at j >= length ignored).
+
+        ``device``: upload the character matrices to that GPU and do the specification's checks there
+        (`core.DeviceTraces`: 128-bit row hashes filed with atomicMin screen for duplicate traces, the census of the
+        overfit cost and the widest character are reduced on the device).  The host then touches the traces only if
+        the device reports suspects -- duplicates or, with probability ~2^-128 per pair, a hash clash -- in which case
+        the host path below decides (dropping duplicates with a warning, refusing traces on both sides) and the result
+        is uploaded again.  `learn()` packs such a specification on the device and creates its core over the packed
+        traces in place."""
+        pl, nl = np.asarray(pos_lengths, dtype=np.int64).reshape(-1), np.asarray(neg_lengths, dtype=np.int64).reshape(-1)
+        pc = np.ascontiguousarray(pos_chars, dtype=np.uint16).reshape(len(pl), -1)
+        nc = np.ascontiguousarray(neg_chars, dtype=np.uint16).reshape(len(nl), -1)
+        if device is None:
+            return Specification(_arrays=(pc, pl, nc, nl))
+        if max(int(pl.max()) if len(pl) else 0, int(nl.max()) if len(nl) else 0) > 0xFFFF:
+            raise ValueError("traces longer than 65535 positions are not supported")
+        from .core import DeviceTraces
+
+        if len(pl) + len(nl) == 0:
+            return Specification(_arrays=(pc, pl, nc, nl))
+        dev = DeviceTraces(pc, pl, nc, nl, device)
+        info = dev.info()
+        if info["suspects"]:
+            dev.close()
+            spec = Specification(_arrays=(pc, pl, nc, nl))  # exact comparison, warnings, ValueError: the host rules
+            if spec.size == 0:
+                return spec
+            dev = DeviceTraces(spec.chars[: spec.n_pos], spec.lengths[: spec.n_pos], spec.chars[spec.n_pos:],
+                               spec.lengths[spec.n_pos:], device)
+            info = dev.info()
+            if info["suspects"]:  # pragma: no cover -- a 128-bit clash between different traces
+                dev.close()
+                return spec
+            spec._attach(dev, info)
+            return spec
+        spec = Specification.__new__(Specification)
+        spec.n_pos, spec.n_neg = len(pl), len(nl)
+        spec._chars = spec._lengths = spec._tuples = None
+        spec._sides = (pc, pl, nc, nl)
+        spec._attach(dev, info)
+        return spec
+
+    def _attach(self, dev, info):
+        self.device_traces, self._info = dev, info
+
+    def release_device(self):
+        """Free the device copy (it is also freed when the specification is collected)."""
+        dev, self.device_traces = self.device_traces, None
+        if dev is not None:
+            dev.close()
+
+    device_traces = None  # core.DeviceTraces when the specification is resident on a GPU
+    _info = None          # its census (DeviceTraces.info())
+    _sides = None         # device path: the caller's arrays, concatenated lazily into chars / lengths
+
+    @property
+    def chars(self) -> np.ndarray:
+        """``uint16[R, Lmax]``, positives first, zero beyond each trace's length."""
+        if self._chars is None:
+            pc, pl, nc, nl = self._sides
+            width = max(pc.shape[1] if len(pl) else 1, nc.shape[1] if len(nl) else 1, 1)
+            full = np.zeros((len(pl) + len(nl), width), dtype=np.uint16)
+            full[: len(pl), : pc.shape[1]] = pc
+            full[len(pl):, : nc.shape[1]] = nc
+            lengths = self.lengths
+            if len(lengths) and int(lengths.min()) < width:
+                full *= (np.arange(width)[None, :] < lengths[:, None]).astype(np.uint16)  # canonical zero padding
+            self._chars = full
+        return self._chars
+
+    @property
+    def lengths(self) -> np.ndarray:
+        if self._lengths is None:
+            _, pl, _, nl = self._sides
+            self._lengths = np.concatenate([pl, nl]).astype(np.int64)
+        return self._lengths
 
     def _build(self, pc, pl, nc, nl):
         width = max(pc.shape[1] if len(pl) else 1, nc.shape[1] if len(nl) else 1, 1)
@@ -209,8 +281,8 @@ class Specification:
                     raise ValueError(f"trace occurs on both sides (positive #{int(maybe[i])}, negative #{j})")
         self.n_pos = len(pl)
         self.n_neg = len(nl)
-        self.chars = np.concatenate([pc, nc], axis=0) if (len(pl) + len(nl)) else np.zeros((0, width), np.uint16)
-        self.lengths = np.concatenate([pl, nl]).astype(np.int64)
+        self._chars = np.concatenate([pc, nc], axis=0) if (len(pl) + len(nl)) else np.zeros((0, width), np.uint16)
+        self._lengths = np.concatenate([pl, nl]).astype(np.int64)
         self._tuples = None
 
     # -- views -------------------------------------------------------------------------
@@ -220,7 +292,19 @@ class Specification:
 
     @property
     def max_len(self) -> int:
+        if self._info is not None:
+            return self._info["max_len"]
         return int(self.lengths.max()) if len(self.lengths) else 0
+
+    @property
+    def n_nonempty(self) -> int:
+        return self._info["non_empty"] if self._info is not None else int(np.count_nonzero(self.lengths))
+
+    @property
+    def n_empty_positive(self) -> int:
+        if self._info is not None:
+            return self._info["empty_pos"]
+        return int(np.count_nonzero(self.lengths[: self.n_pos] == 0))
 
     def _materialise(self):
         if self._tuples is None:
@@ -242,12 +326,16 @@ class Specification:
         return self._materialise()[self.n_pos :]
 
     def char_width(self) -> int:
+        if self._info is not None:
+            return max(1, self._info["char_or"].bit_length())
         top = int(np.bitwise_or.reduce(self.chars, axis=None)) if self.chars.size else 0
         return max(1, top.bit_length())
 
     def positive_char_census(self) -> tuple[int, int]:
         """(#positions, #set proposition bits) over the positive traces -- all that the
         closed-form overfit cost needs."""
+        if self._info is not None:
+            return self._info["pos_positions"], self._info["pos_bits"]
         pc = self.chars[: self.n_pos]
         n_positions = int(self.lengths[: self.n_pos].sum())
         # padding beyond each length is canonical zero, so the set bits of the whole matrix are the census
@@ -275,7 +363,7 @@ class SuffixTable:
 
     @staticmethod
     def from_spec(spec: Specification, limit: int | None = None) -> "SuffixTable":
-        if limit is not None and int(np.count_nonzero(spec.lengths)) > limit:
+        if limit is not None and spec.n_nonempty > limit:
             return SuffixTable(limit + 1, (), (), False)
         seen = set()
         rows, offs = [], []

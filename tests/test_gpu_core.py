@@ -429,7 +429,7 @@ def test_device_packing_matches_host_packing(R, L, n_props, W):
     clean = chars.copy()
     clean[np.arange(L)[None, :] >= lengths[:, None]] = 0
     spec = Specification.__new__(Specification)
-    spec.chars, spec.lengths, spec.n_pos, spec.n_neg = clean, lengths, max(R - 1, 1), R - max(R - 1, 1)
+    spec._chars, spec._lengths, spec.n_pos, spec.n_neg = clean, lengths, max(R - 1, 1), R - max(R - 1, 1)
     want = TraceContext.from_spec(spec, Alphabet.default(n_props), words=W)
     assert (masks == want.masks).all()
     assert (atoms == want.atoms).all()

@@ -158,3 +158,28 @@ def test_specification_dedup_matches_naive_on_many_traces():
         warnings.simplefilter("ignore")
         with pytest.raises(ValueError, match="both sides"):
             Specification.from_arrays(chars[:R], lengths[:R], chars[R:], lengths[R:])
+
+
+def test_array_pairs_are_a_specification_and_the_scheme_rules_take_arrays():
+    """`learn` / `as_specification` accept (chars, lengths) pairs (the 10^6-trace input form); without a device they
+    are the host Specification; `resolve_scheme` works on length arrays (no per-trace Python loop)."""
+    from paper_2402_12373_b200.learner import as_specification
+    from paper_2402_12373_b200.scheme import V_GATHER, V_MUELLER, V_NH, V_NH32
+
+    P = [(1, 2, 3), (0, 1), (3,)]
+    N = [(2, 2), (1, 0, 1, 3)]
+    pc = np.array([[1, 2, 3, 9], [0, 1, 7, 7], [3, 5, 5, 5]], dtype=np.uint16)  # junk beyond the lengths
+    nc = np.array([[2, 2, 0, 0], [1, 0, 1, 3]], dtype=np.uint16)
+    spec = as_specification((pc, np.array([3, 2, 1])), (nc, np.array([2, 4])))
+    want = Specification(P, N)
+    assert spec.pos == want.pos and spec.neg == want.neg and spec.device_traces is None
+    assert (spec.n_nonempty, spec.n_empty_positive, spec.max_len) == (5, 0, 4)
+    assert as_specification(want, None) is want
+    res = learn((pc, np.array([3, 2, 1])), (nc, np.array([2, 4])), 2, max_cost=6, core_factory=oracle_factory(1))
+    assert res.text == learn(P, N, 2, max_cost=6, core_factory=oracle_factory(1)).text
+    lengths = np.array([3, 2, 1, 2, 4])
+    assert resolve_scheme(HashScheme(), lengths).variant == V_GATHER
+    assert resolve_scheme(HashScheme(), np.full(60, 20)).variant == V_MUELLER
+    assert resolve_scheme(HashScheme(), np.full(100, 20)).variant == V_NH32
+    assert resolve_scheme(HashScheme(), np.full(100, 33)).variant == V_NH
+    assert resolve_scheme(HashScheme("nh"), np.full(10, 32)).variant == V_NH32

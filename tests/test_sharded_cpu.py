@@ -262,6 +262,9 @@ def _gloo_rows_worker(rank, world, port, out):
     try:
         comm = TorchComm()
         out.put((rank, [_row_sharded(case, comm) for case in ROW_CASES]))
+    except BaseException as exc:  # the parent must not wait for its timeout when a rank dies
+        out.put((rank, f"{type(exc).__name__}: {exc}"))
+        raise
     finally:
         dist.destroy_process_group()
 
