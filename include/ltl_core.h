@@ -41,6 +41,10 @@ extern "C" {
 #define LTL_S_DONE 0
 #define LTL_S_SOLVED 1
 #define LTL_S_OOM 2
+/* not in the reference's status set: a deadline armed with the "deadline_ms" option passed between two passes of a cost
+ * level -- where the reference raises TimeoutExceeded between its chunks (enumerator.py:154-156, 278, 290).  What earlier
+ * passes admitted stays admitted; the caller abandons the search. */
+#define LTL_S_TIMEOUT 3
 
 /* fingerprint variants: reference kernels.py:39-41 */
 #define LTL_V_GATHER 0
@@ -60,6 +64,9 @@ extern "C" {
 #define LTL_ERR_CUDA (-2)       /* CUDA runtime / driver failure, no device */
 #define LTL_ERR_BUDGET (-3)     /* add_entry over the logical budget (the reference raises CoreOOM, _speedups.pyx:275-276) */
 #define LTL_ERR_DEVICE_OOM (-4) /* device memory exhausted before the logical budget */
+#define LTL_ERR_INVARIANT (-5)  /* debug builds of the data: a stored matrix has bits outside the validity masks -- the reference's
+                                 * LTLLEARN_DEBUG_MASKS assertion (bitsem.py:46-61); checked when that variable is set in the
+                                 * environment or after ltl_core_set_option(h, "debug_masks", 1) */
 
 typedef struct ltl_core ltl_core;
 
@@ -160,6 +167,31 @@ LTL_API int ltl_core_screen_binary(ltl_core* h, int op, int64_t a0, int64_t a1, 
 LTL_API int ltl_core_run_level(ltl_core* h, const ltl_segment* segs, int n_segs, int* status, int* seg_index, int64_t* li,
                        int64_t* ri);
 
+/* One whole search: the cost-level loop of reference enumerator.py:234-251 over a core whose atoms (and, for the NNF
+ * fragment, negated atoms) are admitted -- per level the child-cost pairing of enumerator.py:254-268 (_bucket_pairs), the
+ * dispatch order of enumerator.py:271-296 (connective order formula.py:24) and the bookkeeping of cache.py:144-166
+ * (begin_level / end_level), i.e. exactly ltl_core_run_level on the segment list the reference would build, for
+ * cost = first_cost .. ceiling - 1 until a level solves or runs out of memory.  Same results as the per-level calls;
+ * what it removes is the caller's interpreter from between the levels (config 1: nine levels of a few hundred candidates).
+ *   op_cost[8]     cost of each connective, indexed by opcode (reference formula.py:13-20; [0], the atom cost, is unused)
+ *   op_mask        bit k set: connective k is enabled (NOT off for the NNF fragment, UNTIL off for forbid_until)
+ *   bucket_*       the entry ranges admitted so far, by formula cost (atoms, negated atoms)
+ *   store_last_level  0: entries of level ceiling - 1 keep records and fingerprints only (they are never operands)
+ *   rows / n_rows  one row per level that ended (DONE or SOLVED), in order
+ *   status, op, li, ri  outcome: LTL_S_DONE (ceiling reached), LTL_S_SOLVED with the solving connective and operands,
+ *                  LTL_S_OOM, LTL_S_TIMEOUT; *end_cost = the level the search ended in (ceiling if none solved) */
+typedef struct ltl_level_stats {
+    int32_t cost, status;
+    uint64_t offered, admitted, duplicates; /* of this level (reference cache.py:160-165) */
+    uint64_t bytes;                         /* bytes_used after the level */
+    int64_t first_entry, end_entry;         /* the level's bucket */
+    double ms;                              /* host wall time of the level */
+} ltl_level_stats;
+LTL_API int ltl_core_run_search(ltl_core* h, const int32_t op_cost[8], uint32_t op_mask, const int64_t* bucket_cost,
+                                const int64_t* bucket_first, const int64_t* bucket_end, int n_buckets, int first_cost,
+                                int ceiling, int store_last_level, ltl_level_stats* rows, int max_rows, int* n_rows,
+                                int* status, int* op, int64_t* li, int64_t* ri, int* end_cost);
+
 /* contains / fingerprint_of: reference _speedups.pyx:279-287 / 233-241 (hi has its top 2 bits clear). */
 LTL_API int ltl_core_contains(ltl_core* h, const uint64_t* cm, int* found);
 LTL_API int ltl_core_fingerprint_of(ltl_core* h, const uint64_t* cm, uint64_t* hi, uint64_t* lo);
@@ -168,6 +200,10 @@ LTL_API int ltl_core_fingerprint_of(ltl_core* h, const uint64_t* cm, uint64_t* h
  * [first, first + count); cms_out is uint64[count][R*W] row-major. */
 LTL_API int ltl_core_get_cm(ltl_core* h, int64_t idx, uint64_t* out);
 LTL_API int ltl_core_get_record(ltl_core* h, int64_t idx, int* op, int* lhs, int* rhs);
+/* The records of a whole formula in one call: every entry reachable from idx through (lhs, rhs), each once, idx first;
+ * nodes = int32[cap][4] rows (entry, op, lhs, rhs).  What reference cache.py:197-213 (reconstruct) collects with one
+ * get_record per node -- here one kernel and one copy instead of one device round trip per node. */
+LTL_API int ltl_core_get_subtree(ltl_core* h, int64_t idx, int cap, int32_t* nodes, int* n_nodes);
 LTL_API int ltl_core_export_cms(ltl_core* h, int64_t first, int64_t count, uint64_t* cms_out);
 LTL_API int ltl_core_export_records(ltl_core* h, int64_t first, int64_t count, int8_t* op, int32_t* lhs, int32_t* rhs);
 
@@ -181,19 +217,23 @@ LTL_API int ltl_core_counters(ltl_core* h, uint64_t out[5]);
 /* Row-sharded cores (the alternative for specifications with many rows): G cores, one per GPU, each
  * created over a contiguous slice of the ROWS of the specification (masks of its rows, n_pos = its number of
  * positive rows).  Every core enumerates every candidate on its rows; the per-candidate partial fingerprint sums and
- * error counts (device arrays: uint64 s0[count], uint64 s1[count], uint32 err[count]) are handed to `fn`, which must
- * replace them by their element-wise sums over all shards (wrapping 64-bit / 32-bit adds; NCCL all-reduce) and
- * return 0 once the result is visible to the device; every core then completes identical candidates, admits the
- * same entries in the same order and writes its rows of the new matrices.  No reference counterpart (the reference
- * is one process); the results are those of one core over all rows.
+ * error counts -- a device array of 3 uint64 per candidate, (s0, s1, errors) -- are handed to `fn`, which must
+ * replace them by their element-wise sums over all shards (wrapping 64-bit adds; ONE NCCL all-reduce of 3 * count
+ * int64) and return 0 once the result is visible to the device; every core then completes identical candidates, admits
+ * the same entries in the same order and writes its rows of the new matrices.  A pass is handed over in up to
+ * "exchange_parts" (option, default 4) consecutive candidate ranges: `fn` is called for a range as soon as its
+ * evaluation has ended on the device while the next range is still being evaluated on the core's stream, so the
+ * all-reduce (on the caller's stream) overlaps phase A.  No reference counterpart (the reference is one process); the
+ * results are those of one core over all rows.
  * word_base: index of this shard's first word in the whole matrix (rows before it x W), a multiple of 64;
  * total_words: words of the whole matrix (the budget counts whole matrices: reference _speedups.pyx:100, 252-253).
- * Call once, right after ltl_core_create.  Needs a block-combinable fingerprint (LTL_V_MUELLER / LTL_V_NH). */
-typedef int (*ltl_exchange_fn)(void* ctx, void* d_s0, void* d_s1, void* d_err, int64_t count);
+ * Call once, right after ltl_core_create.  Needs a block-combinable fingerprint (LTL_V_MUELLER / LTL_V_NH / LTL_V_NH32). */
+typedef int (*ltl_exchange_fn)(void* ctx, void* d_sums, int64_t count);
 LTL_API int ltl_core_set_row_shard(ltl_core* h, int64_t word_base, int64_t total_words, ltl_exchange_fn fn, void* ctx);
 
 /* Tuning / measurement (no reference counterpart).
- * options: "chunk_candidates" (candidates per device pass), "profile" (1: time every kernel with CUDA
+ * options: "deadline_ms" (run_level / screen_* return LTL_S_TIMEOUT at the first pass boundary more than this many
+ * milliseconds from now; 0 disarms), "chunk_candidates" (candidates per device pass), "profile" (1: time every kernel with CUDA
  * events on the launching stream), "max_split" (cap on row splits), "force_split" (tests),
  * "store_results" (0: from now on admitted entries keep fingerprint + record but their matrices are not
  * written -- for the last cost level of a search, whose entries are never operands; counters, records and
@@ -215,6 +255,11 @@ LTL_API int ltl_core_stream(ltl_core* h, void** stream_out);
  *                solving level rank in the slice (-1: none); stops after the chunk that holds a solver
  *   stage_file   owner side: file (hi, lo, global rank) tuples in this handle's table shard with
  *                atomicMin(rank); d_win[t] = 1 iff tuple t owns its key and the key was not a member before
+ *   stage_route  (hi, lo) fingerprints of level ranks rank_base .. -> (hi, lo, global rank) tuples grouped by owner
+ *                rank = mix(hi ^ lo) mod world (in rank order inside a group: a stable counting sort on the device),
+ *                and the number of tuples per owner -- the send buffer and split sizes of the all-to-all
+ *   stage_winners  the owners' verdict bytes, in the order the tuples were sent -> the level ranks of this slice's
+ *                winners, ascending (device array d_out of at least `count` int64), and how many there are
  *   stage_decode level ranks -> (op, lhs, rhs) records
  *   stage_append append `count` admitted entries (records, in rank order) and advance the counters;
  *                matrices are materialised locally from the records when first needed
@@ -223,6 +268,10 @@ LTL_API int ltl_core_level_size(ltl_core* h, const ltl_segment* segs, int n_segs
 LTL_API int ltl_core_stage_eval(ltl_core* h, const ltl_segment* segs, int n_segs, int64_t lo, int64_t hi, uint64_t* d_fp,
                         int64_t* solver_rank);
 LTL_API int ltl_core_stage_file(ltl_core* h, const uint64_t* d_tuples, int64_t count, unsigned char* d_win, int64_t* n_win);
+LTL_API int ltl_core_stage_route(ltl_core* h, const uint64_t* d_fp, int64_t count, uint64_t rank_base, int world,
+                                 uint64_t* d_send, int64_t* counts_out);
+LTL_API int ltl_core_stage_winners(ltl_core* h, const uint64_t* d_tuples, const unsigned char* d_win, int64_t count,
+                                   uint64_t rank_base, int64_t level_lo, int64_t* d_out, int64_t* n_out);
 LTL_API int ltl_core_stage_decode(ltl_core* h, const ltl_segment* segs, int n_segs, const int64_t* d_ranks, int64_t count,
                           unsigned char* d_op, int32_t* d_lhs, int32_t* d_rhs);
 LTL_API int ltl_core_stage_append(ltl_core* h, const unsigned char* d_op, const int32_t* d_lhs, const int32_t* d_rhs,

@@ -63,6 +63,21 @@ class LanguageCache:
                            "duplicates": duplicates - d0, "bytes": bytes_used})
         self._frontier = cost + 1
 
+    def absorb_levels(self, rows):
+        """Bookkeeping of cost levels that ran inside the core (`CudaCore.run_search`): their buckets and stats rows."""
+        for r in rows:
+            first, end = r["entries"]
+            self._buckets[r["cost"]] = [int(first), int(end)]
+            row = {"cost": r["cost"], "offered": r["offered"], "admitted": r["admitted"], "duplicates": r["duplicates"],
+                   "bytes": r["bytes"]}
+            if r.get("status", 0) == 0:
+                row["ms"] = r["ms"]
+            self._rows.append(row)
+            self._frontier = r["cost"] + 1
+
+    def buckets(self) -> dict:
+        return {c: (rng[0], rng[1]) for c, rng in self._buckets.items()}
+
     def bucket_range(self, cost: int) -> tuple[int, int]:
         got = self._buckets.get(cost)
         return (got[0], got[1]) if got else (0, 0)
@@ -82,6 +97,11 @@ class LanguageCache:
         memo: dict[int, Formula] = {}
         todo = [int(idx)]
         recs: dict[int, tuple] = {}
+        if hasattr(self.core, "get_subtree"):  # every record of the formula in one device round trip
+            try:
+                recs = self.core.get_subtree(int(idx))
+            except IndexError:
+                recs = {}
         while todo:
             e = todo[-1]
             if e in memo:

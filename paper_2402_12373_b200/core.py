@@ -25,7 +25,7 @@ S_DONE, S_SOLVED, S_OOM = 0, 1, 2
 V_GATHER, V_MUELLER, V_FKP, V_NH, V_NH32 = 0, 1, 2, 3, 4
 MAX_WORDS_PER_ROW = 16
 
-ERR_ARG, ERR_CUDA, ERR_BUDGET, ERR_DEVICE_OOM = -1, -2, -3, -4
+ERR_ARG, ERR_CUDA, ERR_BUDGET, ERR_DEVICE_OOM, ERR_INVARIANT = -1, -2, -3, -4, -5
 KERNEL_CLASSES = ("screen", "finalize", "resolve", "scan", "emit", "materialize", "rehash", "purge", "misc")
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
@@ -37,8 +37,14 @@ class Segment(C.Structure):
                 ("b1", C.c_int64)]
 
 
+class LevelStats(C.Structure):
+    _fields_ = [("cost", C.c_int32), ("status", C.c_int32), ("offered", C.c_uint64), ("admitted", C.c_uint64),
+                ("duplicates", C.c_uint64), ("bytes", C.c_uint64), ("first_entry", C.c_int64), ("end_entry", C.c_int64),
+                ("ms", C.c_double)]
+
+
 #: row-shard exchange callback (include/ltl_core.h: ltl_exchange_fn)
-EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64)
+EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64)
 
 _lib = None
 
@@ -70,10 +76,15 @@ def load_library():
     L.ltl_core_screen_binary.argtypes = [vp, C.c_int, C.c_int64, C.c_int64, C.c_int64, C.c_int64, C.c_int, ip, i64p,
                                          i64p]
     L.ltl_core_run_level.argtypes = [vp, C.POINTER(Segment), C.c_int, ip, ip, i64p, i64p]
+    L.ltl_core_run_search.argtypes = [vp, i32p, C.c_uint32, i64p, i64p, i64p, C.c_int, C.c_int, C.c_int, C.c_int,
+                                      C.POINTER(LevelStats), C.c_int, ip, ip, ip, i64p, i64p, ip]
+    L.ltl_core_run_search.restype = C.c_int
     L.ltl_core_contains.argtypes = [vp, u64p, ip]
     L.ltl_core_fingerprint_of.argtypes = [vp, u64p, u64p, u64p]
     L.ltl_core_get_cm.argtypes = [vp, C.c_int64, u64p]
     L.ltl_core_get_record.argtypes = [vp, C.c_int64, ip, ip, ip]
+    L.ltl_core_get_subtree.argtypes = [vp, C.c_int64, C.c_int, i32p, ip]
+    L.ltl_core_get_subtree.restype = C.c_int
     L.ltl_core_export_cms.argtypes = [vp, C.c_int64, C.c_int64, u64p]
     L.ltl_core_export_records.argtypes = [vp, C.c_int64, C.c_int64, C.POINTER(C.c_int8), i32p, i32p]
     L.ltl_core_entry_fingerprints.argtypes = [vp, C.c_int64, C.c_int64, u64p, u64p]
@@ -109,6 +120,9 @@ def load_library():
     L.ltl_core_level_size.argtypes = [vp, C.POINTER(Segment), C.c_int, i64p]
     L.ltl_core_stage_eval.argtypes = [vp, C.POINTER(Segment), C.c_int, C.c_int64, C.c_int64, vp, i64p]
     L.ltl_core_stage_file.argtypes = [vp, vp, C.c_int64, vp, i64p]
+    L.ltl_core_stage_route.argtypes = [vp, vp, C.c_int64, C.c_uint64, C.c_int, vp, i64p]
+    L.ltl_core_stage_winners.argtypes = [vp, vp, vp, C.c_int64, C.c_uint64, C.c_int64, vp, i64p]
+    L.ltl_core_stage_route.restype = L.ltl_core_stage_winners.restype = C.c_int
     L.ltl_core_stage_decode.argtypes = [vp, C.POINTER(Segment), C.c_int, vp, C.c_int64, vp, vp, vp]
     L.ltl_core_stage_append.argtypes = [vp, vp, vp, vp, C.c_int64, C.c_uint64, C.c_uint64]
     L.ltl_core_stage_purge.argtypes = [vp, C.c_uint64]
@@ -181,6 +195,9 @@ class DeviceTraces:
         pc = np.ascontiguousarray(pos_chars, dtype=np.uint16).reshape(len(pl), -1)
         nc = np.ascontiguousarray(neg_chars, dtype=np.uint16).reshape(len(nl), -1)
         width = max(pc.shape[1] if len(pl) else 0, nc.shape[1] if len(nl) else 0)
+        longest = max(int(pl.max()) if len(pl) else 0, int(nl.max()) if len(nl) else 0)
+        if 0 <= longest < width:  # columns no trace reaches: words per row follow the longest trace, as on the host
+            pc, nc, width = np.ascontiguousarray(pc[:, :longest]), np.ascontiguousarray(nc[:, :longest]), longest
         if len(pl) and pc.shape[1] != width:
             pc = np.ascontiguousarray(np.pad(pc, ((0, 0), (0, width - pc.shape[1]))))
         if len(nl) and nc.shape[1] != width:
@@ -320,6 +337,8 @@ class CudaCore:
             raise CoreOOM(msg)
         if rc == ERR_ARG:
             raise ValueError(msg)
+        if rc == ERR_INVARIANT:  # LTLLEARN_DEBUG_MASKS / option debug_masks: the reference raises AssertionError (bitsem.py:58-61)
+            raise AssertionError(msg)
         raise CoreError(f"[{rc}] {msg}")
 
     def _cm(self, cm) -> np.ndarray:
@@ -381,6 +400,16 @@ class CudaCore:
         self._check(rc)
         return op.value, lhs.value, rhs.value
 
+    def get_subtree(self, idx, cap: int = 1024) -> dict:
+        """``{entry: (op, lhs, rhs)}`` for every entry reachable from ``idx`` (`ltl_core_get_subtree`)."""
+        nodes = np.empty((int(cap), 4), dtype=np.int32)
+        n = C.c_int()
+        rc = self._L.ltl_core_get_subtree(self._h, int(idx), int(cap), nodes.ctypes.data_as(C.POINTER(C.c_int32)), C.byref(n))
+        if rc == ERR_ARG:
+            raise IndexError((self._L.ltl_core_last_error(self._h) or b"").decode())
+        self._check(rc)
+        return {int(e): (int(op), int(lhs), int(rhs)) for e, op, lhs, rhs in nodes[: n.value]}
+
     def export_cms(self, first=0, count=None) -> np.ndarray:
         n = self.n_entries
         count = n - first if count is None else count
@@ -435,11 +464,34 @@ class CudaCore:
                                                C.byref(ri)))
         return st.value, seg.value, li.value, ri.value
 
+    def run_search(self, op_cost, op_mask: int, buckets, first_cost: int, ceiling: int, store_last_level: bool = False):
+        """The whole cost-level loop in the library (`ltl_core_run_search`; reference `enumerator.py:234-251`).
+        ``op_cost``: 8 connective costs by opcode; ``buckets``: ``{cost: (first, end)}`` admitted so far.
+        Returns ``(status, op, li, ri, end_cost, rows)`` with one dict per level that ended."""
+        oc = np.ascontiguousarray(list(op_cost), dtype=np.int32)
+        bc = np.ascontiguousarray([c for c in buckets], dtype=np.int64)
+        bf = np.ascontiguousarray([buckets[c][0] for c in buckets], dtype=np.int64)
+        be = np.ascontiguousarray([buckets[c][1] for c in buckets], dtype=np.int64)
+        n_levels = max(0, int(ceiling) - int(first_cost))
+        rows = (LevelStats * max(1, n_levels))()
+        n_rows, st, op, end_cost = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        li, ri = C.c_int64(), C.c_int64()
+        i32p, i64p = C.POINTER(C.c_int32), C.POINTER(C.c_int64)
+        self._check(self._L.ltl_core_run_search(self._h, oc.ctypes.data_as(i32p), int(op_mask), bc.ctypes.data_as(i64p),
+                                                bf.ctypes.data_as(i64p), be.ctypes.data_as(i64p), len(bc), int(first_cost),
+                                                int(ceiling), int(bool(store_last_level)), rows, n_levels, C.byref(n_rows),
+                                                C.byref(st), C.byref(op), C.byref(li), C.byref(ri), C.byref(end_cost)))
+        out = [{"cost": r.cost, "offered": r.offered, "admitted": r.admitted, "duplicates": r.duplicates, "bytes": r.bytes,
+                "ms": round(r.ms, 3), "entries": (r.first_entry, r.end_entry), "status": r.status}
+               for r in rows[: n_rows.value]]
+        return st.value, op.value, li.value, ri.value, end_cost.value, out
+
     # -- row shard (see sharded.RowShardedCore) --------------------------------------------
     def set_row_shard(self, word_base: int, total_words: int, all_reduce_sum):
         """Make this core one row shard of a larger specification.  ``all_reduce_sum(tensors)`` must add, in place
-        and across all shards, the given device tensors (int64, int64, int32: wrapping sums) and return once the
-        result is visible to the device."""
+        and across all shards, the given device tensors (one int64 tensor of 3 words per candidate: wrapping sums) and
+        return once the result is visible to the device.  It is called for up to ``exchange_parts`` consecutive
+        candidate ranges of a pass, each while the next range is still being evaluated on the core's own stream."""
         import torch
 
         dev = torch.device("cuda", self.device_index)
@@ -448,12 +500,9 @@ class CudaCore:
             def __init__(self, ptr, n, typestr):
                 self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (int(ptr), False), "version": 2}
 
-        def hook(_ctx, s0, s1, err, count):
+        def hook(_ctx, sums, count):
             try:
-                n = int(count)
-                ts = [torch.as_tensor(_Dev(s0, n, "<i8"), device=dev), torch.as_tensor(_Dev(s1, n, "<i8"), device=dev),
-                      torch.as_tensor(_Dev(err, n, "<i4"), device=dev)]
-                all_reduce_sum(ts)
+                all_reduce_sum([torch.as_tensor(_Dev(sums, 3 * int(count), "<i8"), device=dev)])
                 return 0
             except BaseException as exc:  # noqa: BLE001 -- no exception may cross the C ABI
                 self._exchange_error = exc
@@ -503,6 +552,36 @@ class CudaCore:
         self._check(self._L.ltl_core_stage_file(self._h, C.c_void_p(tuples.data_ptr()), tuples.shape[0],
                                                 C.c_void_p(win.data_ptr()), C.byref(n_win)))
         return win
+
+    def stage_route(self, fp, rank_base: int, world: int):
+        """Fingerprints int64[N, 2] of consecutive candidates (global ranks ``rank_base ..``) -> int64[N, 3] tuples
+        ``(hi, lo, global rank)`` grouped by owner rank, and the number of tuples per owner (`ltl_core_stage_route`: a
+        stable counting sort by owner on the device)."""
+        import torch
+
+        fp = fp.contiguous()
+        n = fp.shape[0]
+        send = torch.empty((n, 3), dtype=torch.int64, device=fp.device)
+        counts = (C.c_int64 * int(world))()
+        torch.cuda.current_stream(fp.device).synchronize()
+        self._check(self._L.ltl_core_stage_route(self._h, C.c_void_p(fp.data_ptr()), n, int(rank_base) & 0xFFFFFFFFFFFFFFFF,
+                                                 int(world), C.c_void_p(send.data_ptr()), counts))
+        return send, [int(v) for v in counts]
+
+    def stage_winners(self, send, win, rank_base: int, level_lo: int):
+        """Verdict bytes ``win`` (uint8[N], in the order of the tuples ``send``) -> ascending level ranks of the winners
+        (int64 device tensor; `ltl_core_stage_winners`)."""
+        import torch
+
+        win = win.contiguous()
+        n = send.shape[0]
+        out = torch.empty(n, dtype=torch.int64, device=send.device)
+        n_out = C.c_int64()
+        torch.cuda.current_stream(send.device).synchronize()
+        self._check(self._L.ltl_core_stage_winners(self._h, C.c_void_p(send.data_ptr()), C.c_void_p(win.data_ptr()), n,
+                                                   int(rank_base) & 0xFFFFFFFFFFFFFFFF, int(level_lo),
+                                                   C.c_void_p(out.data_ptr()), C.byref(n_out)))
+        return out[: int(n_out.value)]
 
     def stage_decode(self, segments, ranks):
         """Level ranks (int64 device tensor) -> (op uint8, lhs int32, rhs int32) device tensors."""

@@ -124,9 +124,8 @@ struct ScreenParams {
     u64 gbase;  // global rank of chunk-local rank 0
     u32* slot;  // per candidate: contender slot / NONE
     u64* fp_out;  // MODE_FP_ONLY: 2 words per candidate (hi, lo)
-    u64* acc_s0;  // nsplit > 1: per-candidate partial sums
-    u64* acc_s1;
-    u32* acc_err;
+    u64* acc;  // nsplit > 1 or defer: per-candidate partial sums, 3 words each: (s0, s1, errors) -- one contiguous
+               // range per range of candidates, so that row shards all-reduce any part of a pass in one call
     Ctl* ctl;
     // KIND_REWRITE (tile-shaped phase B): winners' matrices go to entry n_base + dest[rank]
     const u32* dest;  // per candidate: position among the winners / NONE
@@ -155,7 +154,23 @@ struct MaterializeParams {
     int n_pos_lo;  // as in ScreenParams (half-width store)
     i64 not_cbase, not_i0;
     u32 blk_base;  // as in ScreenParams
-    u32 pad_;
+    // Processing order of the 32-entry groups ("phase B order"): n_seg == 0: group k of the launch is group
+    // n_base/32 + k; else the launch walks n_seg runs of groups, run s = groups seg_g0[s] .. of length seg_goff[s+1] -
+    // seg_goff[s], ordered so that the runs reading the same block of right operands follow one another
+    int n_seg;
+    const u32* seg_g0;
+    const u32* seg_goff;
+};
+
+// One family of runs of the phase-B order: the candidates (i, j) of RECT piece `piece` with j inside block jb of the right
+// operand bucket (blocks of `block` entries at absolute multiples of it) form run pos_base + jb * stride + off + (i - i0);
+// n_jb == 0: the whole piece is one run at pos_base.
+struct PlanFam {
+    int piece, n_jb;
+    i64 n_i;
+    i64 block;
+    i64 pos_base, stride, off;
+    i64 t_base;  // first plan thread of this family (threads enumerate (jb, i) pairs)
 };
 
 __host__ __device__ __forceinline__ u64 mix64(u64 x) {  // reference kernels.py:50-57

@@ -60,7 +60,7 @@ template <bool MUELLER>
 __global__ void k_finalize(const __grid_constant__ ScreenParams p, u64 total) {
     u64 c = (u64)blockIdx.x * blockDim.x + threadIdx.x;
     if (c >= total) return;
-    finish_candidate<MUELLER>(p, c, p.acc_s0[c], p.acc_s1[c], p.acc_err[c]);
+    finish_candidate<MUELLER>(p, c, p.acc[3 * c], p.acc[3 * c + 1], (u32)p.acc[3 * c + 2]);
 }
 
 // ------------------------------------------------------------------------------------------------
@@ -202,6 +202,169 @@ __global__ void __launch_bounds__(RES_CTA) k_emit(const u32* __restrict__ flagw,
     rec_rhs[e] = (int)j;
 }
 
+// Small passes (cost levels of a few thousand candidates are bound by launch latency, not by work): ONE CTA does what
+// k_finalize + k_resolve + k_scan + k_emit do for big passes -- complete the row-split candidates, decide the winners
+// (lowest rank per key), compact them in rank order and write their records -- 1024 candidates per round with a running
+// offset.  It also zeroes the partial sums it consumed, so the next small pass needs no memset.
+#define LTL_SMALL_ADMIT 32768
+template <bool MUELLER>
+__global__ void __launch_bounds__(RES_CTA) k_admit_small(const __grid_constant__ ScreenParams p, u64 total, int finalize,
+                                                         i64 n_base, u64 cap_left, unsigned char* __restrict__ rec_op,
+                                                         int* __restrict__ rec_lhs, int* __restrict__ rec_rhs,
+                                                         u32* __restrict__ dest_out) {
+    __shared__ u32 wcnt[32];
+    __shared__ u64 carry_s;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (finalize) {
+        for (u64 c = threadIdx.x; c < total; c += RES_CTA) {
+            finish_candidate<MUELLER>(p, c, p.acc[3 * c], p.acc[3 * c + 1], (u32)p.acc[3 * c + 2]);
+            p.acc[3 * c] = 0;
+            p.acc[3 * c + 1] = 0;
+            p.acc[3 * c + 2] = 0;
+        }
+        __threadfence();
+    }
+    if (threadIdx.x == 0) carry_s = 0;
+    __syncthreads();
+    const u64 limit = min(total, *((volatile u64*)&p.ctl->solver_c));  // nothing at or above the first solver is admitted
+    for (u64 base = 0; base < total; base += RES_CTA) {
+        const u64 c = base + threadIdx.x;
+        bool win = false;
+        if (c < limit) {
+            const u32 s = p.slot[c];
+            if (s != LTL_NONE) win = ld_rank(p.table + s) == p.gbase + c;
+        }
+        const unsigned b = __ballot_sync(0xFFFFFFFFu, win);
+        if (lane == 0) wcnt[warp] = __popc(b);
+        __syncthreads();
+        u64 dest = carry_s + __popc(b & ((1u << lane) - 1u));
+        u32 block_total = 0;
+        for (int w = 0; w < 32; w++) {
+            const u32 v = wcnt[w];
+            if (w < warp) dest += v;
+            block_total += v;
+        }
+        if (c < total) dest_out[c] = LTL_NONE;  // every candidate gets a verdict: the tile-shaped phase B reads it
+        if (win) {
+            if (dest == cap_left) p.ctl->oom_c = c;  // the first winner beyond the budget marks OOM
+            else if (dest < cap_left) {
+                dest_out[c] = (u32)dest;
+                int lo = 0, hi = p.n_pieces - 1;
+                while (lo < hi) {
+                    int mid = (lo + hi + 1) >> 1;
+                    if ((u64)p.pieces[mid].cbase <= c) lo = mid;
+                    else hi = mid - 1;
+                }
+                const Piece pc = p.pieces[lo];
+                i64 i, j;
+                piece_unrank(pc, c, &i, &j);
+                const i64 e = n_base + (i64)dest;
+                rec_op[e] = (unsigned char)pc.op;
+                rec_lhs[e] = (int)i;
+                rec_rhs[e] = (int)j;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) carry_s += block_total;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) p.ctl->total = carry_s;
+}
+
+// ---- phase-B order.  Phase B re-derives every winner from its record, in entry order = rank order: for a
+// piece op(i, j) that is "for each left operand i: all right operands j".  When the right bucket is larger than L2 every
+// i streams it from DRAM again (ncu, config 2: 19.7 GB read to write 21 GB, L2 hit rate 12.7 %).  The entry order is
+// fixed, the PROCESSING order is not: the winners of (i, block of right operands) are one run of consecutive entries,
+// found from the winner flags of the admission pass, and phase B walks the runs block by block -- "for each block of j:
+// all i (of every connective over that bucket)" -- so a block is read from DRAM once and from L2 afterwards.
+//
+// winners with chunk-local rank < c (flag words + per-1024 offsets of k_resolve / k_scan)
+__device__ __forceinline__ u64 winners_before(const u32* __restrict__ flagw, const u64* __restrict__ blockoff, u64 c, u64 total,
+                                              u64 all_winners) {
+    if (c >= total) return all_winners;
+    u64 d = blockoff[c >> 10];
+    const u64 w0 = (c >> 10) << 5, w1 = c >> 5;
+    for (u64 w = w0; w < w1; w++) d += __popc(flagw[w]);
+    return d + __popc(flagw[w1] & ((1u << (c & 31)) - 1u));
+}
+
+__global__ void k_mat_plan(const PlanFam* __restrict__ fams, int n_fams, i64 n_threads, const Piece* __restrict__ pieces,
+                           const u32* __restrict__ flagw, const u64* __restrict__ blockoff, const Ctl* __restrict__ ctl,
+                           u64 total, i64 n_base, u64 count, u32* __restrict__ seg_g0, u32* __restrict__ seg_cnt) {
+    const i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= n_threads) return;
+    int lo = 0, hi = n_fams - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (fams[mid].t_base <= t) lo = mid;
+        else hi = mid - 1;
+    }
+    const PlanFam f = fams[lo];
+    const Piece pc = pieces[f.piece];
+    u64 c_lo, c_hi;
+    i64 pos;
+    if (f.n_jb == 0) {
+        c_lo = (u64)pc.cbase;
+        c_hi = (u64)(pc.cbase + pc.count);
+        pos = f.pos_base;
+    } else {
+        const i64 local = t - f.t_base;
+        const i64 jb = local / f.n_i, ii = local - jb * f.n_i;
+        const i64 nj = pc.j1 - pc.j0;
+        const i64 b_lo = (pc.j0 / f.block + jb) * f.block;
+        const i64 jlo = max(pc.j0, b_lo), jhi = min(pc.j1, b_lo + f.block);
+        c_lo = (u64)(pc.cbase + ii * nj + (jlo - pc.j0));
+        c_hi = (u64)(pc.cbase + ii * nj + (jhi - pc.j0));
+        pos = f.pos_base + jb * f.stride + f.off + ii;
+    }
+    const u64 all_winners = ctl->total;
+    const u64 a = min(winners_before(flagw, blockoff, c_lo, total, all_winners), count);
+    const u64 b = min(winners_before(flagw, blockoff, c_hi, total, all_winners), count);
+    // a group belongs to the run that holds its first new entry
+    const i64 g_base = n_base >> 5;
+    const i64 ga = a == 0 ? g_base : ((n_base + (i64)a + 31) >> 5);
+    const i64 gb = b == 0 ? g_base : ((n_base + (i64)b + 31) >> 5);
+    seg_g0[pos] = (u32)(ga - g_base);
+    seg_cnt[pos] = (u32)(gb - ga);
+}
+
+// exclusive scan of up to 2^16 run lengths (single CTA): off[0 .. n], off[n] = total groups
+__global__ void __launch_bounds__(1024) k_plan_scan(const u32* __restrict__ cnt, int n, u32* __restrict__ off) {
+    __shared__ u32 wsum[32];
+    __shared__ u32 carry;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int base = 0; base < n; base += 1024) {
+        const int idx = base + threadIdx.x;
+        const u32 v = idx < n ? cnt[idx] : 0u;
+        u32 x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const u32 y = __shfl_up_sync(0xFFFFFFFFu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            u32 w = wsum[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const u32 y = __shfl_up_sync(0xFFFFFFFFu, w, o);
+                if (lane >= o) w += y;
+            }
+            wsum[lane] = w;
+        }
+        __syncthreads();
+        const u32 before = carry + (warp ? wsum[warp - 1] : 0u) + (x - v);
+        if (idx < n) off[idx] = before;
+        __syncthreads();
+        if (threadIdx.x == 1023) carry = before + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) off[n] = carry;
+}
+
 // entry e <- proposition words resident on the device (ltl_traces): optionally negated inside the mask, optionally
 // packed two rows per word (half-width store).  n = stored words per entry, R = rows (one word each when pair).
 __global__ void k_import_dev(const u64* __restrict__ src, const u64* __restrict__ masks, int negated, int pair, i64 R,
@@ -236,6 +399,18 @@ __global__ void k_export(const u64* __restrict__ cms, i64 first, i64 count, i64 
     const i64 g = gk / n, k = gk - g * n;
     const i64 e = (g0 + g) * 32 + lane;
     if (e >= first && e < first + count) out[(size_t)(e - first) * n + k] = cms[cm_index(e, n, k)];
+}
+
+// debug invariant of the reference (bitsem.py:46-61, LTLLEARN_DEBUG_MASKS): no characteristic bit outside the validity mask
+__global__ void k_check_masks(const u64* __restrict__ cms, const u64* __restrict__ masks, i64 first, i64 count, i64 n,
+                              u64* __restrict__ bad) {
+    const i64 g0 = first >> 5;
+    const i64 t = (i64)blockIdx.x * blockDim.x + threadIdx.x;
+    const i64 lane = t & 31;
+    const i64 gk = t >> 5;
+    const i64 g = gk / n, k = gk - g * n;
+    const i64 e = (g0 + g) * 32 + lane;
+    if (e >= first && e < first + count && (cms[cm_index(e, n, k)] & ~masks[k])) atomicAdd(bad, 1ull);
 }
 
 __global__ void k_set_record(unsigned char* rec_op, int* rec_lhs, int* rec_rhs, i64 e, int op, int lhs, int rhs) {
@@ -285,6 +460,135 @@ __global__ void k_file_verdict(const u64* __restrict__ tuples, const u32* __rest
     }
     const unsigned b = __ballot_sync(0xFFFFFFFFu, w);
     if ((threadIdx.x & 31) == 0 && b) atomicAdd(&ctl->total, (u64)__popc(b));
+}
+
+// ---- candidate-range shards: routing of (fingerprint, rank) tuples to their hash owners, on the device ----------------
+// owner of a fingerprint: same integer mix as sharded.py owner_of
+__host__ __device__ __forceinline__ int fp_owner(u64 hi, u64 lo, int world) {
+    const u64 x = (hi ^ lo) * K_STEP;
+    return (int)(((x >> 33) & 0x7FFFFFFFull) % (u64)world);
+}
+#define LTL_MAX_WORLD 64
+
+// pass 1 of a stable counting sort by owner: hist[d * nb + block] = tuples of this 1024-tuple block owned by rank d
+__global__ void __launch_bounds__(1024) k_route_count(const u64* __restrict__ fp, u64 count, int world, u32* __restrict__ hist, u32 nb) {
+    __shared__ u32 cnt[LTL_MAX_WORLD];
+    if (threadIdx.x < LTL_MAX_WORLD) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    const u64 t = (u64)blockIdx.x * 1024 + threadIdx.x;
+    const int d = t < count ? fp_owner(fp[2 * t], fp[2 * t + 1], world) : LTL_MAX_WORLD;
+    const unsigned m = __match_any_sync(0xFFFFFFFFu, d);
+    if (d < LTL_MAX_WORLD && (threadIdx.x & 31) == __ffs(m) - 1) atomicAdd(&cnt[d], (u32)__popc(m));
+    __syncthreads();
+    if ((int)threadIdx.x < world) hist[(size_t)threadIdx.x * nb + blockIdx.x] = cnt[threadIdx.x];
+}
+
+// pass 2: tuple t goes to off[owner * nb + block] + (tuples of the same owner before it in its block): grouped by owner,
+// in rank order inside a group
+__global__ void __launch_bounds__(1024) k_route_scatter(const u64* __restrict__ fp, u64 count, int world, u64 rank_base,
+                                                        const u32* __restrict__ off, u32 nb, u64* __restrict__ send) {
+    __shared__ u32 wc[32][LTL_MAX_WORLD];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int k = threadIdx.x; k < 32 * LTL_MAX_WORLD; k += 1024) (&wc[0][0])[k] = 0;
+    __syncthreads();
+    const u64 t = (u64)blockIdx.x * 1024 + threadIdx.x;
+    u64 hi = 0, lo = 0;
+    int d = LTL_MAX_WORLD;
+    if (t < count) {
+        hi = fp[2 * t];
+        lo = fp[2 * t + 1];
+        d = fp_owner(hi, lo, world);
+    }
+    const unsigned m = __match_any_sync(0xFFFFFFFFu, d);
+    const u32 in_warp = (u32)__popc(m & ((1u << lane) - 1u));
+    if (d < LTL_MAX_WORLD && lane == __ffs(m) - 1) wc[warp][d] = (u32)__popc(m);
+    __syncthreads();
+    if ((int)threadIdx.x < world) {  // exclusive prefix over the warps, per owner
+        u32 run = 0;
+        for (int w = 0; w < 32; w++) {
+            const u32 v = wc[w][threadIdx.x];
+            wc[w][threadIdx.x] = run;
+            run += v;
+        }
+    }
+    __syncthreads();
+    if (d < LTL_MAX_WORLD) {
+        const size_t pos = (size_t)off[(size_t)d * nb + blockIdx.x] + wc[warp][d] + in_warp;
+        send[3 * pos] = hi;
+        send[3 * pos + 1] = lo;
+        send[3 * pos + 2] = rank_base + t;
+    }
+}
+
+// verdicts come back in the order the tuples were sent: set the winner bit of the tuple's candidate
+__global__ void k_win_flags(const u64* __restrict__ tuples, const unsigned char* __restrict__ win, u64 count, u64 rank_base,
+                            u32* __restrict__ flagw) {
+    const u64 t = (u64)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= count || !win[t]) return;
+    const u64 c = tuples[3 * t + 2] - rank_base;
+    atomicOr(flagw + (c >> 5), 1u << (c & 31));
+}
+
+__global__ void __launch_bounds__(RES_CTA) k_flag_count(const u32* __restrict__ flagw, u64 count, u32* __restrict__ blocksum) {
+    __shared__ u32 cnt;
+    if (threadIdx.x == 0) cnt = 0;
+    __syncthreads();
+    const u64 c = (u64)blockIdx.x * RES_CTA + threadIdx.x;
+    if ((threadIdx.x & 31) == 0 && c < count) {
+        const u32 b = flagw[c >> 5];
+        if (b) atomicAdd(&cnt, (u32)__popc(b));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) blocksum[blockIdx.x] = cnt;
+}
+
+// the winners' level ranks, ascending
+__global__ void __launch_bounds__(RES_CTA) k_emit_ranks(const u32* __restrict__ flagw, const u64* __restrict__ blockoff, u64 count,
+                                                        i64 level_lo, i64* __restrict__ out) {
+    __shared__ u32 wcnt[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const u64 c = (u64)blockIdx.x * RES_CTA + threadIdx.x;
+    const u32 fw = c < count ? flagw[c >> 5] : 0u;
+    if (lane == 0) wcnt[warp] = __popc(fw);
+    __syncthreads();
+    if (!((fw >> lane) & 1u)) return;
+    u64 dest = blockoff[blockIdx.x] + __popc(fw & ((1u << lane) - 1u));
+    for (int w = 0; w < warp; w++) dest += wcnt[w];
+    out[dest] = level_lo + (i64)c;
+}
+
+// the records of a formula: every entry reachable from `root` through (lhs, rhs), each once, root first -- one launch and
+// one copy instead of one device round trip per node (reference cache.py:197-213 walks get_record node by node)
+#define LTL_SUBTREE_MAX 4096
+__global__ void k_subtree(const unsigned char* __restrict__ rec_op, const int* __restrict__ rec_lhs, const int* __restrict__ rec_rhs,
+                          i64 root, i64 n_entries, int cap, int* __restrict__ out /* [cap][4]: entry, op, lhs, rhs */, int* __restrict__ n_out) {
+    int n = 0, head = 0;
+    if (root >= 0 && root < n_entries && cap > 0) {
+        out[0] = (int)root;
+        n = 1;
+    }
+    while (head < n) {  // breadth first over the list itself
+        const int e = out[4 * head];
+        const int op = rec_op[e], lhs = rec_lhs[e], rhs = rec_rhs[e];
+        out[4 * head + 1] = op;
+        out[4 * head + 2] = lhs;
+        out[4 * head + 3] = rhs;
+        head++;
+        if (op == OP_IDENT) continue;  // an atom: lhs is the proposition
+        const bool unary = op == OP_NOT || op == OP_NEXT || op == OP_FINALLY || op == OP_GLOBALLY;
+        for (int k = 0; k < (unary ? 1 : 2); k++) {
+            const int child = k == 0 ? lhs : rhs;
+            if (child < 0 || child >= n_entries) continue;  // dangling: the caller reports it
+            bool seen = false;
+            for (int q = 0; q < n; q++) seen |= out[4 * q] == child;
+            if (!seen && n < cap) out[4 * n++] = child;
+            else if (!seen) {
+                *n_out = -1;  // more nodes than the buffer holds
+                return;
+            }
+        }
+    }
+    *n_out = n;
 }
 
 // level ranks -> records
@@ -487,6 +791,7 @@ struct PendingEvent {
 struct PendingMat {
     u64 n_base = 0, count = 0;
     bool tiled = false;
+    int n_seg = 0;  // > 0: the phase-B order of this range is in the core's plan buffers
     std::vector<Piece> pieces;
     i64 total = 0, tiles = 0;
 };
@@ -519,8 +824,7 @@ struct Arena {
     u32* d_flagw = nullptr;
     u32* d_blocksum = nullptr;
     u64* d_blockoff = nullptr;
-    u64 *d_acc_s0 = nullptr, *d_acc_s1 = nullptr;
-    u32* d_acc_err = nullptr;
+    u64* d_acc = nullptr;  // per-candidate partial sums (s0, s1, errors): row-split passes, row shards
     i64 acc_cap = 0;
     u64* d_fp = nullptr;
     i64 fp_cap = 0;
@@ -556,9 +860,7 @@ struct Arena {
         cudaFree(d_flagw);
         cudaFree(d_blocksum);
         cudaFree(d_blockoff);
-        cudaFree(d_acc_s0);
-        cudaFree(d_acc_s1);
-        cudaFree(d_acc_err);
+        cudaFree(d_acc);
         cudaFree(d_fp);
         cudaFree(d_pieces);
         cudaFree(d_ctl);
@@ -626,6 +928,7 @@ struct ltl_core : Arena {
     int n_dep = 0;
     u64 keys_upper = 0;
     i64 chunk_cap = 1 << 28;  // candidates per ordered-admission pass (normally a whole cost level)
+    double deadline_at = 0;   // steady-clock seconds after which run_level stops between passes (0: none)
     i64 sub_tiles = 1 << 16;  // warp tiles per phase-A launch: little work is issued after a solver shows up (2^15: +2.4 %
                               // step time on the bench workload from the drained tails between launches; >= 2^16: equal)
     u64 n_entries = 0, offered = 0, admitted = 0, duplicates = 0;
@@ -647,6 +950,23 @@ struct ltl_core : Arena {
     int tiled_materialize = -1;  // phase B over phase A's tiles instead of per record: 1 always, 0 never, -1 by size
     bool device_oom = false;      // an S_OOM came from the device, not from the logical budget
     bool store_results = true;    // false: admitted entries get records and fingerprints but no matrix
+    bool debug_masks = false;     // check every matrix written against the validity masks (reference LTLLEARN_DEBUG_MASKS)
+    u64* d_dbg = nullptr;
+    int* d_subtree = nullptr;
+    u32 *d_route_hist = nullptr, *d_route_off = nullptr;  // candidate-range shards: owner histogram / offsets of stage_route
+    size_t route_cap = 0;
+    cudaEvent_t part_ev[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    int exchange_parts = 4;       // row shards: parts of a pass whose exchange overlaps the evaluation of the next part
+    u64 exchange_calls = 0;
+    bool order_mat = true;        // phase B walks big right-operand buckets block by block (k_mat_plan)
+    i64 order_min = 1 << 16;      // ... for passes that admit at least this many entries
+    i64 order_block_bytes = 16 << 20;
+    u32 *d_plan_g0 = nullptr, *d_plan_cnt = nullptr, *d_plan_off = nullptr;
+    PlanFam* d_plan_fams = nullptr;
+    int plan_cap = 0, plan_fams_cap = 0;
+    bool plan_in_use = false;
+    bool small_admit = true;      // passes of <= LTL_SMALL_ADMIT candidates: one bookkeeping kernel instead of four
+    bool acc_dirty = true;        // the partial-sum arrays may hold something other than zeros
     u64 unstored_from = ~0ull;    // first entry index without a stored matrix
     bool profile = false;
     KStat stats[LTL_K_COUNT];
@@ -775,17 +1095,13 @@ static int ensure_scratch(ltl_core* h, i64 total) {
 static int ensure_acc(ltl_core* h, i64 total) {
     if (total <= h->acc_cap) return LTL_OK;
     CK(cudaStreamSynchronize(h->stream));
-    cudaFree(h->d_acc_s0);
-    cudaFree(h->d_acc_s1);
-    cudaFree(h->d_acc_err);
-    h->d_acc_s0 = h->d_acc_s1 = nullptr;
-    h->d_acc_err = nullptr;
+    cudaFree(h->d_acc);
+    h->d_acc = nullptr;
     h->acc_cap = 0;
     i64 cap = std::max<i64>(total, 1 << 12);
-    CK(cudaMalloc(&h->d_acc_s0, (size_t)cap * 8));
-    CK(cudaMalloc(&h->d_acc_s1, (size_t)cap * 8));
-    CK(cudaMalloc(&h->d_acc_err, (size_t)cap * 4));
+    CK(cudaMalloc(&h->d_acc, (size_t)cap * 24));
     h->acc_cap = cap;
+    h->acc_dirty = true;
     return LTL_OK;
 }
 
@@ -994,6 +1310,111 @@ static int apply_purge(ltl_core* h) {
     return LTL_OK;
 }
 
+// Phase-B order of the range just admitted (see k_mat_plan): runs of consecutive new entries, by (right-operand bucket,
+// block of it, connective, left operand).  Needs the winner flags of the admission pass that is still in the scratch
+// arrays, so it is issued right behind it.  Returns the number of runs (0: keep the entry order).
+static int plan_materialize(ltl_core* h, const std::vector<Piece>& pieces, i64 total, u64 n_base, u64 count, int* n_seg_out) {
+    *n_seg_out = 0;
+    if (!h->order_mat || h->plan_in_use || (i64)count < h->order_min) return LTL_OK;
+    const i64 block = std::max<i64>(32, (h->order_block_bytes / (8 * h->n)) & ~(i64)31);
+    std::vector<PlanFam> fams;
+    fams.reserve(pieces.size());
+    // pieces over the same right bucket share its blocks: their runs interleave block by block
+    struct Group {
+        i64 j0, j1, n_jb, sum_i, pos_base;
+    };
+    std::vector<Group> groups;
+    std::vector<int> fam_group;
+    bool any_split = false;
+    for (size_t k = 0; k < pieces.size(); k++) {
+        const Piece& pc = pieces[k];
+        if (pc.count <= 0) continue;
+        PlanFam f;
+        memset(&f, 0, sizeof(f));
+        f.piece = (int)k;
+        f.block = block;
+        const i64 nj = pc.j1 - pc.j0;
+        const bool split = pc.kind == PIECE_RECT && nj >= 2 * block && pc.i1 - pc.i0 >= 2;
+        int gi = -1;
+        if (split) {
+            f.n_i = pc.i1 - pc.i0;
+            f.n_jb = (int)((pc.j1 - 1) / block - pc.j0 / block + 1);
+            for (size_t g = 0; g < groups.size(); g++)
+                if (groups[g].j0 == pc.j0 && groups[g].j1 == pc.j1) gi = (int)g;
+            if (gi < 0) {
+                groups.push_back({pc.j0, pc.j1, f.n_jb, 0, 0});
+                gi = (int)groups.size() - 1;
+            }
+            f.off = groups[(size_t)gi].sum_i;
+            groups[(size_t)gi].sum_i += f.n_i;
+            any_split = true;
+        }
+        fams.push_back(f);
+        fam_group.push_back(gi);
+    }
+    if (!any_split) return LTL_OK;
+    // positions: runs in rank order, except that the pieces of a group are laid out together where its first piece stands
+    i64 pos = 0, threads = 0;
+    std::vector<char> placed(groups.size(), 0);
+    for (size_t k = 0; k < fams.size(); k++) {
+        PlanFam& f = fams[k];
+        f.t_base = threads;
+        const int gi = fam_group[k];
+        if (gi < 0) {
+            f.pos_base = pos++;
+            threads += 1;
+            continue;
+        }
+        Group& g = groups[(size_t)gi];
+        if (!placed[(size_t)gi]) {
+            placed[(size_t)gi] = 1;
+            g.pos_base = pos;
+            pos += g.n_jb * g.sum_i;
+        }
+        f.pos_base = g.pos_base;
+        f.stride = g.sum_i;
+        threads += (i64)f.n_jb * f.n_i;
+    }
+    if (pos > (1 << 16) || pos < 2) return LTL_OK;
+    const int n_seg = (int)pos;
+    if (n_seg + 1 > h->plan_cap) {
+        CK(cudaStreamSynchronize(h->stream));
+        cudaFree(h->d_plan_g0);
+        cudaFree(h->d_plan_cnt);
+        cudaFree(h->d_plan_off);
+        h->d_plan_g0 = h->d_plan_cnt = h->d_plan_off = nullptr;
+        h->plan_cap = 0;
+        const int cap = std::max(n_seg + 1, 4096);
+        CK(cudaMalloc(&h->d_plan_g0, (size_t)cap * 4));
+        CK(cudaMalloc(&h->d_plan_cnt, (size_t)cap * 4));
+        CK(cudaMalloc(&h->d_plan_off, (size_t)cap * 4));
+        h->plan_cap = cap;
+    }
+    if ((int)fams.size() > h->plan_fams_cap) {
+        CK(cudaStreamSynchronize(h->stream));
+        cudaFree(h->d_plan_fams);
+        h->d_plan_fams = nullptr;
+        h->plan_fams_cap = 0;
+        const int cap = std::max((int)fams.size(), 256);
+        CK(cudaMalloc(&h->d_plan_fams, sizeof(PlanFam) * (size_t)cap));
+        h->plan_fams_cap = cap;
+    }
+    CK(cudaMemcpyAsync(h->d_plan_fams, fams.data(), sizeof(PlanFam) * fams.size(), cudaMemcpyHostToDevice, h->stream));
+    CK(cudaStreamSynchronize(h->stream));  // `fams` is pageable and goes out of scope (the caller syncs here anyway)
+    h->h2d_bytes += sizeof(PlanFam) * fams.size();
+    {
+        ScopedTimer t(h, LTL_K_MISC, (u64)threads, (double)threads * 64.0);
+        k_mat_plan<<<(unsigned)((threads + 255) / 256), 256, 0, h->stream>>>(h->d_plan_fams, (int)fams.size(), threads, h->d_pieces,
+                                                                            h->d_flagw, h->d_blockoff, h->d_ctl, (u64)total,
+                                                                            (i64)n_base, count, h->d_plan_g0, h->d_plan_cnt);
+        k_plan_scan<<<1, 1024, 0, h->stream>>>(h->d_plan_cnt, n_seg, h->d_plan_off);
+    }
+    CK(cudaGetLastError());
+    h->plan_in_use = true;
+    *n_seg_out = n_seg;
+    return LTL_OK;
+}
+
 static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 tiles, int mode, bool check_solve,
                      bool materialize, ChunkOut* out, int fused_not = -1) {
     int rc;
@@ -1012,8 +1433,13 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     memcpy(h->h_pieces, pieces.data(), sizeof(Piece) * pieces.size());
     CK(cudaMemcpyAsync(h->d_pieces, h->h_pieces, sizeof(Piece) * pieces.size(), cudaMemcpyHostToDevice, h->stream));
     h->h2d_bytes += sizeof(Piece) * pieces.size();
-    CK(cudaMemsetAsync(h->d_ctl, 0xFF, 2 * sizeof(u64), h->stream));  // solver_c = oom_c = none
-    CK(cudaMemsetAsync((char*)h->d_ctl + 2 * sizeof(u64), 0, sizeof(Ctl) - 2 * sizeof(u64), h->stream));
+    if (mode == MODE_INSERT) {  // solver_c = oom_c = none; `total` is assigned by the scan, nothing else is read
+        CK(cudaMemsetAsync(h->d_ctl, 0xFF, sizeof(Ctl), h->stream));
+    } else {
+        CK(cudaMemsetAsync(h->d_ctl, 0xFF, 2 * sizeof(u64), h->stream));
+        CK(cudaMemsetAsync((char*)h->d_ctl + 2 * sizeof(u64), 0, sizeof(Ctl) - 2 * sizeof(u64), h->stream));
+    }
+    const bool small = mode == MODE_INSERT && h->small_admit && total <= LTL_SMALL_ADMIT;
 
     ScreenParams p;
     memset(&p, 0, sizeof(p));
@@ -1047,12 +1473,13 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     const bool acc_path = p.nsplit > 1 || p.defer;
     if (acc_path) {
         if ((rc = ensure_acc(h, total))) return rc;
-        p.acc_s0 = h->d_acc_s0;
-        p.acc_s1 = h->d_acc_s1;
-        p.acc_err = h->d_acc_err;
-        CK(cudaMemsetAsync(h->d_acc_s0, 0, (size_t)total * 8, h->stream));
-        CK(cudaMemsetAsync(h->d_acc_s1, 0, (size_t)total * 8, h->stream));
-        CK(cudaMemsetAsync(h->d_acc_err, 0, (size_t)total * 4, h->stream));
+        p.acc = h->d_acc;
+        // (the small-pass bookkeeping kernel leaves the sums it consumed zeroed: nothing to clear between small passes)
+        const size_t clear = (size_t)(small ? std::max<i64>(total, std::min<i64>(h->acc_cap, LTL_SMALL_ADMIT)) : total);
+        if (!small || h->acc_dirty) {
+            CK(cudaMemsetAsync(h->d_acc, 0, clear * 24, h->stream));
+        }
+        h->acc_dirty = !small;
     }
     u64 issued_units = 0;       // what the phase-A launches of this pass were booked with (statistics)
     double issued_bytes = 0;
@@ -1062,60 +1489,106 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
         const Piece& fp = pieces[(size_t)fused_not];
         if ((rc = flush_materialize(h, &p, screen_kind, fp.cbase, fp.i0))) return rc;
     }
-    // Phase A goes out in launches of sub_tiles warp tiles, in enumeration order, with no host wait in
-    // between (two in flight); after each one the solver rank is copied to pinned memory, and once a solver is
-    // known no launch is issued whose first tile lies above it.
-    {
-        // (fingerprint-only passes that look for a solver -- the sharded evaluation stage -- stop early too)
-        const bool whole = acc_path || mode == MODE_LOOKUP || (mode == MODE_FP_ONLY && !check_solve);
-        const i64 per = whole ? tiles : std::max<i64>(h->sub_tiles, LTL_WARPS_PER_CTA);
-        const double bytes_all = screen_bytes(h, pieces);
-        issued_units = 0;
-        issued_bytes = 0;
-        u64 known_solver = ~0ull;
-        int k = 0;
-        for (i64 t0 = 0; t0 < tiles; t0 += per, k++) {
-            const i64 t1 = std::min(tiles, t0 + per);
-            if (per < tiles) {
-                if (k >= 2) {
-                    HostTimer ht(&h->sync_ms);
-                    CK(cudaEventSynchronize(h->sub_ev[k & 1]));
-                    known_solver = std::min(known_solver, h->h_solver[k & 1]);
-                }
-                if (known_solver != ~0ull && check_solve) {
-                    // first tile of this launch: its piece and the lowest rank it can hold
-                    size_t pi = 0;
-                    for (size_t q = 0; q < pieces.size(); q++)
-                        if (pieces[q].owns_tiles && pieces[q].tile_base <= t0) pi = q;
-                    if ((u64)tile_min_rank(pieces[pi], t0 - pieces[pi].tile_base) > known_solver) break;
-                }
-            }
-            p.tile_offset = t0;
-            const double frac = (double)(t1 - t0) / (double)tiles;
-            ScopedTimer t(h, LTL_K_SCREEN, (u64)((double)total * frac), bytes_all * frac);
-            issued_units += (u64)((double)total * frac);
-            issued_bytes += bytes_all * frac;
-            dim3 grid((unsigned)(((t1 - t0) * p.nsplit + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), 1);
-            ScreenParams q = p;
-            q.total_tiles = t1;
-            (h->pair ? ltl_launch_screen_w1p : SCREEN_FN[h->W])(q, screen_kind, grid, h->stream);
-            if (per < tiles) {
-                CK(cudaMemcpyAsync(h->h_solver + (k & 1), &h->d_ctl->solver_c, sizeof(u64), cudaMemcpyDeviceToHost, h->stream));
-                CK(cudaEventRecord(h->sub_ev[k & 1], h->stream));
-            }
-        }
-    }
-    CK(cudaGetLastError());
-    if (p.defer) {  // row shards: every shard adds its partial sums, then all of them complete identical candidates
+    if (p.defer) {
+        // Row shards: every shard adds its partial sums, then all of them complete identical candidates.  The pass is cut
+        // at piece boundaries into up to `exchange_parts` parts (contiguous ranges of tiles AND of ranks); all parts are
+        // launched at once, and while part k + 1 is still being evaluated the sums of part k -- complete as soon as its
+        // launch has ended -- are already being all-reduced: the exchange overlaps phase A instead of following it.
+        struct Part {
+            i64 t0, t1, c0, c1;
+        };
+        std::vector<Part> parts;
         {
-            HostTimer ht(&h->sync_ms);
-            CK(cudaStreamSynchronize(h->stream));
+            const i64 want = std::max<i64>(1, std::min<i64>(h->exchange_parts, 8));
+            i64 t_start = 0, c_start = 0;
+            for (size_t k = 1; k < pieces.size(); k++) {
+                if (!pieces[k].owns_tiles || pieces[k].ext) continue;  // siblings stay with the piece that evaluates them
+                const i64 goal = tiles * (i64)(parts.size() + 1) / want;
+                if ((i64)parts.size() + 1 < want && pieces[k].tile_base >= goal && pieces[k].tile_base > t_start) {
+                    parts.push_back({t_start, pieces[k].tile_base, c_start, pieces[k].cbase});
+                    t_start = pieces[k].tile_base;
+                    c_start = pieces[k].cbase;
+                }
+            }
+            parts.push_back({t_start, tiles, c_start, total});
         }
-        HostTimer ht(&h->exchange_ms);
-        if (h->exchange(h->exchange_ctx, h->d_acc_s0, h->d_acc_s1, h->d_acc_err, (int64_t)total))
-            return h->fail(LTL_ERR_CUDA, "row-shard exchange failed");
+        const double bytes_all = screen_bytes(h, pieces);
+        for (size_t k = 0; k < parts.size(); k++) {
+            const Part& pt = parts[k];
+            if (pt.t1 > pt.t0) {
+                const double frac = tiles > 0 ? (double)(pt.t1 - pt.t0) / (double)tiles : 0.0;
+                ScopedTimer t(h, LTL_K_SCREEN, (u64)((double)total * frac), bytes_all * frac);
+                issued_units += (u64)((double)total * frac);
+                issued_bytes += bytes_all * frac;
+                dim3 grid((unsigned)(((pt.t1 - pt.t0) * p.nsplit + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), 1);
+                ScreenParams q = p;
+                q.tile_offset = pt.t0;
+                q.total_tiles = pt.t1;
+                (h->pair ? ltl_launch_screen_w1p : SCREEN_FN[h->W])(q, screen_kind, grid, h->stream);
+            }
+            if (!h->part_ev[k]) CK(cudaEventCreateWithFlags(&h->part_ev[k], cudaEventDisableTiming));
+            CK(cudaEventRecord(h->part_ev[k], h->stream));
+        }
+        CK(cudaGetLastError());
+        for (size_t k = 0; k < parts.size(); k++) {
+            const Part& pt = parts[k];
+            {
+                HostTimer ht(&h->sync_ms);
+                CK(cudaEventSynchronize(h->part_ev[k]));
+            }
+            if (pt.c1 <= pt.c0) continue;
+            HostTimer ht(&h->exchange_ms);
+            if (h->exchange(h->exchange_ctx, h->d_acc + 3 * pt.c0, (int64_t)(pt.c1 - pt.c0)))
+                return h->fail(LTL_ERR_CUDA, "row-shard exchange failed");
+            h->exchange_calls++;
+        }
+    } else {
+        // Phase A goes out in launches of sub_tiles warp tiles, in enumeration order, with no host wait in
+        // between (two in flight); after each one the solver rank is copied to pinned memory, and once a solver is
+        // known no launch is issued whose first tile lies above it.
+        {
+            // (fingerprint-only passes that look for a solver -- the sharded evaluation stage -- stop early too)
+            const bool whole = acc_path || mode == MODE_LOOKUP || (mode == MODE_FP_ONLY && !check_solve);
+            const i64 per = whole ? tiles : std::max<i64>(h->sub_tiles, LTL_WARPS_PER_CTA);
+            const double bytes_all = screen_bytes(h, pieces);
+            issued_units = 0;
+            issued_bytes = 0;
+            u64 known_solver = ~0ull;
+            int k = 0;
+            for (i64 t0 = 0; t0 < tiles; t0 += per, k++) {
+                const i64 t1 = std::min(tiles, t0 + per);
+                if (per < tiles) {
+                    if (k >= 2) {
+                        HostTimer ht(&h->sync_ms);
+                        CK(cudaEventSynchronize(h->sub_ev[k & 1]));
+                        known_solver = std::min(known_solver, h->h_solver[k & 1]);
+                    }
+                    if (known_solver != ~0ull && check_solve) {
+                        // first tile of this launch: its piece and the lowest rank it can hold
+                        size_t pi = 0;
+                        for (size_t q = 0; q < pieces.size(); q++)
+                            if (pieces[q].owns_tiles && pieces[q].tile_base <= t0) pi = q;
+                        if ((u64)tile_min_rank(pieces[pi], t0 - pieces[pi].tile_base) > known_solver) break;
+                    }
+                }
+                p.tile_offset = t0;
+                const double frac = (double)(t1 - t0) / (double)tiles;
+                ScopedTimer t(h, LTL_K_SCREEN, (u64)((double)total * frac), bytes_all * frac);
+                issued_units += (u64)((double)total * frac);
+                issued_bytes += bytes_all * frac;
+                dim3 grid((unsigned)(((t1 - t0) * p.nsplit + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), 1);
+                ScreenParams q = p;
+                q.total_tiles = t1;
+                (h->pair ? ltl_launch_screen_w1p : SCREEN_FN[h->W])(q, screen_kind, grid, h->stream);
+                if (per < tiles) {
+                    CK(cudaMemcpyAsync(h->h_solver + (k & 1), &h->d_ctl->solver_c, sizeof(u64), cudaMemcpyDeviceToHost, h->stream));
+                    CK(cudaEventRecord(h->sub_ev[k & 1], h->stream));
+                }
+            }
+        }
+        CK(cudaGetLastError());
     }
-    if (acc_path) {
+    if (acc_path && !small) {
         ScopedTimer t(h, LTL_K_FINALIZE, (u64)total, (double)total * 36.0);
         if (mueller) k_finalize<true><<<(unsigned)((total + 255) / 256), 256, 0, h->stream>>>(p, (u64)total);
         else k_finalize<false><<<(unsigned)((total + 255) / 256), 256, 0, h->stream>>>(p, (u64)total);
@@ -1132,7 +1605,26 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     // ---- ordered admission.  The resolve limit min(total, solver rank) is read from ctl on the device, so
     // phase A and the three bookkeeping kernels run back to back with one host round trip per chunk.
     const u64 room = h->cap_entries > h->n_entries ? h->cap_entries - h->n_entries : 0;
-    {
+    if (small) {
+        {
+            ScopedTimer t(h, LTL_K_RESOLVE, (u64)total, (double)total * (acc_path ? 72.0 : 36.0));
+            if (mueller)
+                k_admit_small<true><<<1, RES_CTA, 0, h->stream>>>(p, (u64)total, acc_path ? 1 : 0, (i64)h->n_entries, room,
+                                                                  (unsigned char*)h->rec_op.base, (int*)h->rec_lhs.base,
+                                                                  (int*)h->rec_rhs.base, h->d_dest);
+            else
+                k_admit_small<false><<<1, RES_CTA, 0, h->stream>>>(p, (u64)total, acc_path ? 1 : 0, (i64)h->n_entries, room,
+                                                                   (unsigned char*)h->rec_op.base, (int*)h->rec_lhs.base,
+                                                                   (int*)h->rec_rhs.base, h->d_dest);
+        }
+        CK(cudaGetLastError());
+        CK(cudaMemcpyAsync(h->h_ctl, h->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
+        {
+            HostTimer ht(&h->sync_ms);
+            CK(cudaStreamSynchronize(h->stream));
+        }
+        h->d2h_bytes += sizeof(Ctl);
+    } else {
         const unsigned nb = (unsigned)((total + RES_CTA - 1) / RES_CTA);
         {
             ScopedTimer t(h, LTL_K_RESOLVE, (u64)total, (double)total * 36.0);
@@ -1179,6 +1671,8 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
             pm.pieces = pieces;
             pm.total = total;
             pm.tiles = tiles;
+        } else if (!small) {
+            if ((rc = plan_materialize(h, pieces, total, pm.n_base, pm.count, &pm.n_seg))) return rc;
         }
         h->pending_mat.push_back(std::move(pm));
     }
@@ -1224,6 +1718,24 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     } else {
         h->keys_upper += count;
     }
+    return LTL_OK;
+}
+
+// LTLLEARN_DEBUG_MASKS / option "debug_masks": the reference's debug invariant (bitsem.py:46-61) on stored entries
+static int check_masks(ltl_core* h, u64 first, u64 count) {
+    if (!count) return LTL_OK;
+    if (!h->d_dbg) CK(cudaMalloc(&h->d_dbg, 8));
+    CK(cudaMemsetAsync(h->d_dbg, 0, 8, h->stream));
+    const u64 groups = (first + count + 31) / 32 - first / 32;
+    const u64 threads = groups * (u64)h->n * 32;
+    k_check_masks<<<(unsigned)((threads + 255) / 256), 256, 0, h->stream>>>((const u64*)h->cms.base, h->d_masks, (i64)first, (i64)count,
+                                                                               h->n, h->d_dbg);
+    CK(cudaGetLastError());
+    u64 bad = 0;
+    CK(cudaMemcpyAsync(&bad, h->d_dbg, 8, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    if (bad) return h->fail(LTL_ERR_INVARIANT, "characteristic bits escaped the validity mask (" + std::to_string(bad) + " words, entries " +
+                                                   std::to_string(first) + ".." + std::to_string(first + count - 1) + ")");
     return LTL_OK;
 }
 
@@ -1281,6 +1793,12 @@ static int flush_materialize(ltl_core* h, const ScreenParams* sp, int fuse_kind,
         m.rec_lhs = (const int*)h->rec_lhs.base;
         m.rec_rhs = (const int*)h->rec_rhs.base;
         m.blk_base = h->blk_base;
+        if (pm.n_seg > 0) {
+            m.n_seg = pm.n_seg;
+            m.seg_g0 = h->d_plan_g0;
+            m.seg_goff = h->d_plan_off;
+            h->plan_in_use = false;  // (the launch below is the last reader; later plans are written behind it in stream order)
+        }
         const i64 groups = (i64)((n_base + count + 31) / 32 - n_base / 32);
         choose_split(h, groups, &m.nsplit, &m.rows_per_split);
         ScreenParams none;
@@ -1300,12 +1818,22 @@ static int flush_materialize(ltl_core* h, const ScreenParams* sp, int fuse_kind,
         (h->pair ? ltl_launch_materialize_w1p : MATERIALIZE_FN[h->W])(m, fk ? *sp : none, fk, grid, h->stream);
         CK(cudaGetLastError());
     }
+    if (h->debug_masks)
+        for (auto& pm : h->pending_mat)
+            if ((rc = check_masks(h, pm.n_base, pm.count))) {
+                h->pending_mat.clear();
+                return rc;
+            }
     h->pending_mat.clear();
     return LTL_OK;
 }
 
 // ------------------------------------------------------------------------------------------------
 // level driver: units -> chunks of <= chunk_cap candidates, consecutive in enumeration order
+
+static double steady_seconds() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
 
 static int run_units(ltl_core* h, const std::vector<Unit>& units, bool check_solve, int* status, int* seg_index,
                      int64_t* li, int64_t* ri) {
@@ -1320,6 +1848,10 @@ static int run_units(ltl_core* h, const std::vector<Unit>& units, bool check_sol
     // exhausts it is found sooner with smaller passes (everything after the first over-budget candidate is wasted work:
     // a 150 M candidate level evaluated to admit the last 3 M entries cost 120 ms of a 215 ms search).
     i64 level_cap = h->chunk_cap;
+    // A deadline is looked at between passes, like the reference's check between its 2^22-candidate chunks of 64-word
+    // matrices (enumerator.py:278, 290): passes are bounded by about 2^31 matrix words so that the check comes round
+    // every ~0.1 s whatever the number of rows.
+    if (h->deadline_at > 0) level_cap = std::min<i64>(level_cap, std::max<i64>((i64)1 << 15, ((i64)1 << 31) / std::max<i64>(h->n, 1)));
     if (check_solve) {
         const u64 room = h->cap_entries > h->n_entries ? h->cap_entries - h->n_entries : 0;
         if (room < (u64)level_cap / 2) level_cap = std::min<i64>(level_cap, std::max<i64>((i64)room * 2, (i64)1 << 21));
@@ -1349,6 +1881,10 @@ static int run_units(ltl_core* h, const std::vector<Unit>& units, bool check_sol
     i64 row = units.empty() ? 0 : units[0].i0;  // next row (left index) of the current unit
     i64 col = -1;                               // >= 0: next column inside a partially emitted row
     while (ui < units.size()) {
+        if (h->deadline_at > 0 && steady_seconds() > h->deadline_at) {
+            *status = LTL_S_TIMEOUT;
+            return LTL_OK;
+        }
         pieces.clear();
         i64 total = 0, tiles = 0;
         int fused_piece = -1;
@@ -1660,6 +2196,16 @@ void ltl_core_destroy(ltl_core* h) {
         cudaSetDevice(h->device);
         if (h->stream) cudaStreamSynchronize(h->stream);
         drain_events(h);
+        if (h->d_dbg) cudaFree(h->d_dbg);
+        cudaFree(h->d_subtree);
+        cudaFree(h->d_route_hist);
+        cudaFree(h->d_route_off);
+        for (auto& ev : h->part_ev)
+            if (ev) cudaEventDestroy(ev);
+        cudaFree(h->d_plan_g0);
+        cudaFree(h->d_plan_cnt);
+        cudaFree(h->d_plan_off);
+        cudaFree(h->d_plan_fams);
         cudaGetLastError();
         pool_give(*static_cast<Arena*>(h));
     }
@@ -1811,6 +2357,7 @@ static int core_create_impl(const uint64_t* masks, const ltl_traces* tr, int R, 
         ltl_core_destroy(h);
         return rc;
     }
+    if (getenv("LTLLEARN_DEBUG_MASKS")) h->debug_masks = true;  // the reference's switch (bitsem.py:48)
     *out = h;
     return LTL_OK;
 }
@@ -1857,6 +2404,7 @@ int ltl_core_add_entry(ltl_core* h, const uint64_t* cm, int op, int lhs, int rhs
     const i64 e = (i64)h->n_entries;
     int rc;
     if ((rc = stage_matrix(h, cm, e))) return rc;
+    if (h->debug_masks && (rc = check_masks(h, (u64)e, 1))) return rc;
     ChunkOut co;
     if ((rc = single_chunk(h, e, MODE_INSERT, &co))) return rc;
     if (co.status == LTL_S_OOM) return h->fail(LTL_ERR_BUDGET, "memory budget exhausted");
@@ -1907,6 +2455,98 @@ int ltl_core_run_level(ltl_core* h, const ltl_segment* segs, int n_segs, int* st
     int rc = expand_segments(h, segs, n_segs, units);
     if (rc) return rc;
     return run_units(h, units, true, status, seg_index, li, ri);
+}
+
+// The whole cost-level loop in one call (include/ltl_core.h).  Host work per level is a handful of integer operations
+// here instead of a trip through the caller's interpreter: searches of small levels are bound by exactly that.
+int ltl_core_run_search(ltl_core* h, const int32_t op_cost[8], uint32_t op_mask, const int64_t* bucket_cost,
+                        const int64_t* bucket_first, const int64_t* bucket_end, int n_buckets, int first_cost, int ceiling,
+                        int store_last_level, ltl_level_stats* rows, int max_rows, int* n_rows, int* status, int* op,
+                        int64_t* li, int64_t* ri, int* end_cost) {
+    ENTER(h);
+    if (!op_cost || (n_buckets && (!bucket_cost || !bucket_first || !bucket_end)) || n_buckets < 0 || !n_rows || !status || !op ||
+        !li || !ri || !end_cost || (max_rows && !rows) || max_rows < 0)
+        return h->fail(LTL_ERR_ARG, "null argument");
+    *n_rows = 0;
+    *status = LTL_S_DONE;
+    *op = -1;
+    *li = *ri = -1;
+    *end_cost = first_cost;
+    // connective order of a level: reference formula.py:24
+    static const int ORDER[7] = {OP_NOT, OP_AND, OP_OR, OP_NEXT, OP_FINALLY, OP_GLOBALLY, OP_UNTIL};
+    for (int k = 1; k < 8; k++)
+        if (((op_mask >> k) & 1u) && op_cost[k] < 1) return h->fail(LTL_ERR_ARG, "connective costs must be positive");
+    if (ceiling - first_cost > max_rows) return h->fail(LTL_ERR_ARG, "run_search: fewer stats rows than cost levels");
+    std::vector<std::pair<i64, i64>> bucket((size_t)std::max(ceiling, 1), std::make_pair((i64)0, (i64)0));  // by cost
+    std::vector<char> known((size_t)std::max(ceiling, 1), 0);
+    for (int b = 0; b < n_buckets; b++) {
+        if (bucket_cost[b] < 0 || bucket_first[b] < 0 || bucket_end[b] < bucket_first[b] || (u64)bucket_end[b] > h->n_entries)
+            return h->fail(LTL_ERR_ARG, "run_search: bucket outside the store");
+        if (bucket_cost[b] < ceiling) {
+            bucket[(size_t)bucket_cost[b]] = std::make_pair((i64)bucket_first[b], (i64)bucket_end[b]);
+            known[(size_t)bucket_cost[b]] = 1;
+        }
+    }
+    std::vector<ltl_segment> segs;
+    std::vector<Unit> units;
+    for (int c = first_cost; c < ceiling; c++) {
+        *end_cost = c;
+        const auto t0 = std::chrono::steady_clock::now();
+        // begin_level: reference cache.py:144-152
+        const u64 n0 = h->n_entries, o0 = h->offered, a0 = h->admitted, d0 = h->duplicates;
+        if (c == ceiling - 1 && !store_last_level && h->unstored_from == ~0ull) h->store_results = false;
+        // the level's segments: child-cost pairing of reference enumerator.py:254-268, dispatch order of 271-296
+        segs.clear();
+        for (int oi = 0; oi < 7; oi++) {
+            const int o = ORDER[oi];
+            if (!((op_mask >> o) & 1u)) continue;
+            const int w = op_cost[o];
+            const bool unary = o == OP_NOT || o == OP_NEXT || o == OP_FINALLY || o == OP_GLOBALLY;
+            if (unary) {
+                const int a = c - w;
+                if (a >= 1 && bucket[(size_t)a].second > bucket[(size_t)a].first)
+                    segs.push_back(ltl_segment{o, 0, bucket[(size_t)a].first, bucket[(size_t)a].second, -1, -1});
+                continue;
+            }
+            const bool commutative = o == OP_AND || o == OP_OR;
+            for (int a = 1; a < c - w; a++) {
+                const int b = c - w - a;
+                if (b < 1) continue;
+                if (commutative && a > b) break;
+                const auto& A = bucket[(size_t)a];
+                const auto& B = bucket[(size_t)b];
+                if (A.second == A.first || B.second == B.first) continue;
+                segs.push_back(ltl_segment{o, commutative && a == b ? 1 : 0, A.first, A.second, B.first, B.second});
+            }
+        }
+        units.clear();
+        int rc = expand_segments(h, segs.data(), (int)segs.size(), units);
+        if (rc) return rc;
+        int seg_index = -1;
+        rc = run_units(h, units, true, status, &seg_index, li, ri);
+        if (rc) return rc;
+        if (*status == LTL_S_OOM || *status == LTL_S_TIMEOUT) return LTL_OK;  // no row for a level that did not end (enumerator.py:243-245)
+        // end_level: reference cache.py:154-166
+        // (a bucket that exists already -- negated atoms of the NNF fragment can cost as much as this level -- grows)
+        bucket[(size_t)c] = std::make_pair(known[(size_t)c] ? bucket[(size_t)c].first : (i64)n0, (i64)h->n_entries);
+        known[(size_t)c] = 1;
+        ltl_level_stats& row = rows[(*n_rows)++];
+        row.cost = c;
+        row.status = *status;
+        row.offered = h->offered - o0;
+        row.admitted = h->admitted - a0;
+        row.duplicates = h->duplicates - d0;
+        row.bytes = h->admitted * h->entry_bytes;  // reference _speedups.pyx:260
+        row.first_entry = (int64_t)bucket[(size_t)c].first;
+        row.end_entry = (int64_t)bucket[(size_t)c].second;
+        row.ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+        if (*status == LTL_S_SOLVED) {
+            *op = seg_index >= 0 ? segs[(size_t)seg_index].op : -1;
+            return LTL_OK;
+        }
+    }
+    *end_cost = ceiling;
+    return LTL_OK;
 }
 
 int ltl_core_screen_unary(ltl_core* h, int op, int64_t c0, int64_t c1, int* status, int64_t* li, int64_t* ri) {
@@ -2050,6 +2690,31 @@ int ltl_core_export_records(ltl_core* h, int64_t first, int64_t count, int8_t* o
     return LTL_OK;
 }
 
+int ltl_core_get_subtree(ltl_core* h, int64_t idx, int cap, int32_t* nodes, int* n_nodes) {
+    ENTER(h);
+    if (!nodes || !n_nodes || cap < 1) return h->fail(LTL_ERR_ARG, "null argument");
+    *n_nodes = 0;
+    if (idx < 0 || (u64)idx >= h->n_entries) return h->fail(LTL_ERR_ARG, "entry index out of range");
+    cap = std::min(cap, LTL_SUBTREE_MAX);
+    if (!h->d_subtree) CK(cudaMalloc(&h->d_subtree, (size_t)(4 * LTL_SUBTREE_MAX + 1) * sizeof(int)));
+    {
+        ScopedTimer t(h, LTL_K_MISC, 1, 9.0 * cap);
+        k_subtree<<<1, 1, 0, h->stream>>>((const unsigned char*)h->rec_op.base, (const int*)h->rec_lhs.base, (const int*)h->rec_rhs.base,
+                                          (i64)idx, (i64)h->n_entries, cap, h->d_subtree + 1, h->d_subtree);
+    }
+    CK(cudaGetLastError());
+    // (count and nodes in one copy: the count sits in front of the node list)
+    std::vector<int> host((size_t)4 * cap + 1);
+    CK(cudaMemcpyAsync(host.data(), h->d_subtree, host.size() * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->d2h_bytes += host.size() * sizeof(int);
+    drain_events(h);
+    if (host[0] < 0) return h->fail(LTL_ERR_ARG, "get_subtree: the formula has more nodes than the buffer");
+    *n_nodes = host[0];
+    memcpy(nodes, host.data() + 1, (size_t)host[0] * 4 * sizeof(int));
+    return LTL_OK;
+}
+
 int ltl_core_get_record(ltl_core* h, int64_t idx, int* op, int* lhs, int* rhs) {
     if (!h) return LTL_ERR_ARG;
     if (idx < 0 || (u64)idx >= h->n_entries) return h->fail(LTL_ERR_ARG, "entry index out of range");
@@ -2078,6 +2743,8 @@ int ltl_core_set_option(ltl_core* h, const char* name, int64_t value) {
     if (!strcmp(name, "chunk_candidates")) {
         if (value < 1 || value > ((int64_t)1 << 30)) return h->fail(LTL_ERR_ARG, "chunk_candidates outside [1, 2^30]");
         h->chunk_cap = value;
+    } else if (!strcmp(name, "deadline_ms")) {
+        h->deadline_at = value > 0 ? steady_seconds() + (double)value * 1e-3 : 0.0;
     } else if (!strcmp(name, "sub_tiles")) {
         h->sub_tiles = std::max<int64_t>(LTL_WARPS_PER_CTA, value);
     } else if (!strcmp(name, "store_results")) {
@@ -2089,6 +2756,18 @@ int ltl_core_set_option(ltl_core* h, const char* name, int64_t value) {
         h->fuse_unary = value != 0;
     } else if (!strcmp(name, "fuse_not")) {
         h->fuse_not = value != 0;
+    } else if (!strcmp(name, "debug_masks")) {
+        h->debug_masks = value != 0;
+    } else if (!strcmp(name, "exchange_parts")) {
+        h->exchange_parts = (int)std::max<int64_t>(1, std::min<int64_t>(8, value));
+    } else if (!strcmp(name, "order_mat")) {
+        h->order_mat = value != 0;
+    } else if (!strcmp(name, "order_min")) {
+        h->order_min = value;
+    } else if (!strcmp(name, "order_block_bytes")) {
+        h->order_block_bytes = std::max<int64_t>(1, value);
+    } else if (!strcmp(name, "small_admit")) {
+        h->small_admit = value != 0;
     } else if (!strcmp(name, "fuse_not_min")) {
         h->fuse_not_min = value;
     } else if (!strcmp(name, "profile")) {
@@ -2223,6 +2902,69 @@ int ltl_core_stage_file(ltl_core* h, const uint64_t* d_tuples, int64_t count, un
     drain_events(h);
     *n_win = (int64_t)h->h_ctl->total;
     h->keys_upper += h->h_ctl->total;
+    return LTL_OK;
+}
+
+int ltl_core_stage_route(ltl_core* h, const uint64_t* d_fp, int64_t count, uint64_t rank_base, int world, uint64_t* d_send,
+                         int64_t* counts_out) {
+    ENTER(h);
+    if (count < 0 || world < 1 || world > LTL_MAX_WORLD || !counts_out) return h->fail(LTL_ERR_ARG, "stage_route: bad argument");
+    for (int d = 0; d < world; d++) counts_out[d] = 0;
+    if (count == 0) return LTL_OK;
+    if (!d_fp || !d_send) return h->fail(LTL_ERR_ARG, "null argument");
+    const u32 nb = (u32)((count + 1023) / 1024);
+    const size_t cells = (size_t)world * nb;
+    if (cells + 1 > h->route_cap) {
+        CK(cudaStreamSynchronize(h->stream));
+        cudaFree(h->d_route_hist);
+        cudaFree(h->d_route_off);
+        h->d_route_hist = h->d_route_off = nullptr;
+        h->route_cap = 0;
+        const size_t cap = std::max<size_t>(cells + 1, 1 << 14);
+        CK(cudaMalloc(&h->d_route_hist, cap * 4));
+        CK(cudaMalloc(&h->d_route_off, cap * 4));
+        h->route_cap = cap;
+    }
+    {
+        ScopedTimer t(h, LTL_K_MISC, (u64)count, (double)count * 56.0);
+        k_route_count<<<nb, 1024, 0, h->stream>>>((const u64*)d_fp, (u64)count, world, h->d_route_hist, nb);
+        k_plan_scan<<<1, 1024, 0, h->stream>>>(h->d_route_hist, (int)cells, h->d_route_off);
+        k_route_scatter<<<nb, 1024, 0, h->stream>>>((const u64*)d_fp, (u64)count, world, rank_base, h->d_route_off, nb, (u64*)d_send);
+    }
+    CK(cudaGetLastError());
+    u32 bounds[LTL_MAX_WORLD + 1];
+    CK(cudaMemcpy2DAsync(bounds, 4, h->d_route_off, (size_t)nb * 4, 4, (size_t)world + 1, cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->d2h_bytes += 4 * (size_t)(world + 1);
+    drain_events(h);
+    for (int d = 0; d < world; d++) counts_out[d] = (int64_t)(bounds[d + 1] - bounds[d]);
+    return LTL_OK;
+}
+
+int ltl_core_stage_winners(ltl_core* h, const uint64_t* d_tuples, const unsigned char* d_win, int64_t count, uint64_t rank_base,
+                           int64_t level_lo, int64_t* d_out, int64_t* n_out) {
+    ENTER(h);
+    if (count < 0 || !n_out) return h->fail(LTL_ERR_ARG, "stage_winners: bad argument");
+    *n_out = 0;
+    if (count == 0) return LTL_OK;
+    if (!d_tuples || !d_win || !d_out) return h->fail(LTL_ERR_ARG, "null argument");
+    int rc;
+    if ((rc = ensure_scratch(h, count))) return rc;
+    const unsigned nb = (unsigned)((count + RES_CTA - 1) / RES_CTA);
+    CK(cudaMemsetAsync(h->d_flagw, 0, (size_t)nb * (RES_CTA / 32) * 4, h->stream));
+    {
+        ScopedTimer t(h, LTL_K_MISC, (u64)count, (double)count * 33.0);
+        k_win_flags<<<(unsigned)((count + 255) / 256), 256, 0, h->stream>>>((const u64*)d_tuples, d_win, (u64)count, rank_base, h->d_flagw);
+        k_flag_count<<<nb, RES_CTA, 0, h->stream>>>(h->d_flagw, (u64)count, h->d_blocksum);
+        k_scan<<<1, 1024, 0, h->stream>>>(h->d_blocksum, nb, h->d_blockoff, h->d_ctl);
+        k_emit_ranks<<<nb, RES_CTA, 0, h->stream>>>(h->d_flagw, h->d_blockoff, (u64)count, (i64)level_lo, (i64*)d_out);
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(h->h_ctl, h->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
+    CK(cudaStreamSynchronize(h->stream));
+    h->d2h_bytes += sizeof(Ctl);
+    drain_events(h);
+    *n_out = (int64_t)h->h_ctl->total;
     return LTL_OK;
 }
 

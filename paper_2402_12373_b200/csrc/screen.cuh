@@ -517,9 +517,9 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
         u64 c;
         if (!slot_rank(t, &c)) continue;
         if (p.nsplit > 1 || p.defer) {
-            atomicAdd(p.acc_s0 + c, s0[t]);
-            atomicAdd(p.acc_s1 + c, s1[t]);
-            if (err[t]) atomicAdd(p.acc_err + c, err[t]);
+            atomicAdd(p.acc + 3 * c, s0[t]);
+            atomicAdd(p.acc + 3 * c + 1, s1[t]);
+            if (err[t]) atomicAdd(p.acc + 3 * c + 2, (u64)err[t]);
         } else {
             finish_candidate<HASHED>(p, c, s0[t], s1[t], err[t]);
         }
@@ -545,12 +545,22 @@ __global__ void __launch_bounds__(LTL_CTA, (W == 1 ? LTL_MIN_CTAS_W1 : 2)) k_scr
     const int warp = threadIdx.x >> 5;
     u64* sbuf = reinterpret_cast<u64*>(smem_raw) + warp * Ring<W>::WARP_U64;
     u64* bars = reinterpret_cast<u64*>(smem_raw) + LTL_WARPS_PER_CTA * Ring<W>::WARP_U64 + warp * Ring<W>::STAGES;
-    // warps are numbered over (row split, tile) so that every CTA is full even when a level has few tiles
+    // Warps are numbered over (tile, row split), split fastest, so that every CTA is full even when a level has few
+    // tiles AND the warps of a CTA (and of the CTAs resident beside it) run the same tile variant on different row
+    // ranges: with the splits of one tile far apart, the six warps of an SM sub-partition ran six different variants of
+    // ~4 KB each through a ~6 KB L0 instruction cache, and ncu showed `no_instruction` as the top stall of every
+    // row-split launch (46 % of the samples on BASELINE config 4, cost level 5).
     const i64 gw = (i64)blockIdx.x * LTL_WARPS_PER_CTA + warp;
-    const i64 launch_tiles = p.total_tiles - p.tile_offset;
     int split = 0;
     i64 T = p.tile_offset + gw;
-    if (p.nsplit > 1) {
+    if (p.nsplit > 1 && KIND != KIND_REWRITE) {
+        const i64 tl = gw / p.nsplit;
+        split = (int)(gw - tl * p.nsplit);
+        T = p.tile_offset + tl;
+    } else if (p.nsplit > 1) {
+        // the tile-shaped phase B keeps (row split, tile): neighbouring tiles write neighbouring winners, whose partial
+        // lines meet in L2 only if they are written at about the same time (tile-major: 10.0 -> 14.5 ms on config 4)
+        const i64 launch_tiles = p.total_tiles - p.tile_offset;
         split = (int)(gw / launch_tiles);
         T = p.tile_offset + (gw - (i64)split * launch_tiles);
         if (split >= p.nsplit) return;
@@ -704,16 +714,29 @@ __device__ __forceinline__ void mat_rows(const MaterializeParams& p, const bool 
         }
         apply_row<OP, W, PAIR>(out, x, y, m);
 #pragma unroll
-        for (int w = 0; w < W; w++) po[(kb + w) * 32] = out[w];
+        for (int w = 0; w < W; w++) __stcs(po + (kb + w) * 32, out[w]);  // streaming: next read is a cost level away
     }
+}
+
+// group handled by warp `widx` of a phase-B launch (MaterializeParams: processing order), or -1 past the end
+__device__ __forceinline__ i64 mat_group(const MaterializeParams& p, const i64 widx) {
+    if (p.n_seg == 0) return (p.n_base >> 5) + widx;
+    if (widx >= (i64)p.seg_goff[p.n_seg]) return -1;
+    int lo = 0, hi = p.n_seg - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if ((i64)p.seg_goff[mid] <= widx) lo = mid;
+        else hi = mid - 1;
+    }
+    return (p.n_base >> 5) + (i64)p.seg_g0[lo] + (widx - (i64)p.seg_goff[lo]);
 }
 
 template <int W, bool PAIR = false>
 __global__ void __launch_bounds__(LTL_CTA) k_materialize(const __grid_constant__ MaterializeParams p) {
     const int lane = threadIdx.x & 31;
-    const i64 g = (p.n_base >> 5) + (i64)blockIdx.x * LTL_WARPS_PER_CTA + (threadIdx.x >> 5);
+    const i64 g = mat_group(p, (i64)blockIdx.x * LTL_WARPS_PER_CTA + (threadIdx.x >> 5));
     const i64 dst = g * 32 + lane;
-    if (g * 32 >= p.n_base + p.count) return;
+    if (g < 0 || g * 32 >= p.n_base + p.count) return;
     const bool valid = dst >= p.n_base && dst < p.n_base + p.count;
     const int op = valid ? (int)p.rec_op[dst] : -1;
     const int lhs = valid ? p.rec_lhs[dst] : 0;
@@ -816,7 +839,7 @@ __device__ __forceinline__ void mat_rows_not(const MaterializeParams& p, const b
         y[0] = BIN ? ld_nc(py + (size_t)r * 32) : 0ull;
         m[0] = ld_nc(pm + r);
         apply_row<OP, 1, PAIR>(out, x, y, m);
-        po[(size_t)r * 32] = out[0];
+        __stcs(po + (size_t)r * 32, out[0]);  // streaming store: keeps the operand blocks in L2
         f.template word<PAIR>(~out[0] & m[0], kbase + (u32)r, pk, r < n_pos, r < n_pos_lo);
     };
     constexpr int UNROLL = LTL_MATF_UNROLL;
@@ -836,9 +859,9 @@ template <int FK, bool PAIR = false>
 __global__ void __launch_bounds__(LTL_CTA, LTL_MATF_MINB) k_materialize_not(const __grid_constant__ MaterializeParams p,
                                                                             const __grid_constant__ ScreenParams sp) {
     const int lane = threadIdx.x & 31;
-    const i64 g = (p.n_base >> 5) + (i64)blockIdx.x * LTL_WARPS_PER_CTA + (threadIdx.x >> 5);
+    const i64 g = mat_group(p, (i64)blockIdx.x * LTL_WARPS_PER_CTA + (threadIdx.x >> 5));
     const i64 dst = g * 32 + lane;
-    if (g * 32 >= p.n_base + p.count) return;
+    if (g < 0 || g * 32 >= p.n_base + p.count) return;
     const bool valid = dst >= p.n_base && dst < p.n_base + p.count;
     const int op = valid ? (int)p.rec_op[dst] : -1;
     const int lhs = valid ? p.rec_lhs[dst] : 0;
@@ -867,9 +890,9 @@ __global__ void __launch_bounds__(LTL_CTA, LTL_MATF_MINB) k_materialize_not(cons
     if (valid) {  // file NOT(dst) as candidate not_cbase + (dst - not_i0) of the pass in flight
         const u64 c = (u64)p.not_cbase + (u64)(dst - p.not_i0);
         if (sp.nsplit > 1 || sp.defer) {  // the pass combines row splits (or GPUs): hand the sums to k_finalize
-            atomicAdd(sp.acc_s0 + c, f.s0);
-            atomicAdd(sp.acc_s1 + c, f.s1);
-            if (f.err) atomicAdd(sp.acc_err + c, f.err);
+            atomicAdd(sp.acc + 3 * c, f.s0);
+            atomicAdd(sp.acc + 3 * c + 1, f.s1);
+            if (f.err) atomicAdd(sp.acc + 3 * c + 2, (u64)f.err);
         } else {
             finish_candidate<true>(sp, c, f.s0, f.s1, f.err);
         }

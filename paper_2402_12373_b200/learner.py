@@ -44,7 +44,7 @@ from .packing import TraceContext
 from .scheme import HashScheme, resolve_scheme
 from .traces import Alphabet, Specification, SuffixTable
 
-S_DONE, S_SOLVED, S_OOM = 0, 1, 2
+S_DONE, S_SOLVED, S_OOM, S_TIMEOUT = 0, 1, 2, 3
 MAX_WORDS_PER_ROW = 16  # device kernels are instantiated for rows of up to 1024 positions
 
 
@@ -212,7 +212,13 @@ def _check_deadline(cfg: LearnerConfig):
 def _run_level(core, segs: list[Segment], cfg: LearnerConfig):
     """(status, op, li, ri) of the first non-DONE event, or None."""
     if hasattr(core, "run_level"):
+        if cfg.deadline is not None and hasattr(core, "set_option"):
+            # the level is one call: the core checks the deadline between its passes, as the reference does between its
+            # 2^22-candidate chunks (`enumerator.py:278`, `290`)
+            core.set_option("deadline_ms", max(1, int(1e3 * (cfg.deadline - time.monotonic()))))
         status, k, li, ri = core.run_level(segs)
+        if status == S_TIMEOUT:
+            raise TimeoutExceeded("learner deadline exceeded")
         return None if status == S_DONE else (status, segs[k].op if k >= 0 else -1, li, ri)
     for s in segs:
         _check_deadline(cfg)
@@ -358,6 +364,33 @@ class Enumeration:
         return outcome
 
     keep_core = False
+    #: run the cost-level loop inside the library (`ltl_core_run_search`) when the core offers it; False: one
+    #: `run_level` call per level from this module (what cores without `run_search` -- oracle, sharded -- always get)
+    native_loop = True
+
+    def _run_in_core(self, ops, atom_c: int) -> EnumOutcome:
+        """The level loop of `run` as one library call (reference `enumerator.py:234-251`): same segments, same
+        bookkeeping, no interpreter between the levels."""
+        cfg, cache, core, stats = self.cfg, self.cache, self.core, self.stats
+        _check_deadline(cfg)
+        if cfg.deadline is not None:
+            core.set_option("deadline_ms", max(1, int(1e3 * (cfg.deadline - time.monotonic()))))
+        op_cost = [cfg.cost.of(op) for op in range(8)]
+        mask = sum(1 << op for op in ops)
+        status, op, li, ri, end_cost, rows = core.run_search(op_cost, mask, cache.buckets(), atom_c + 1, self.ceiling,
+                                                             cfg.store_last_level)
+        cache.absorb_levels(rows)
+        if status == S_TIMEOUT:
+            raise TimeoutExceeded("learner deadline exceeded")
+        if status == S_OOM:
+            start = max((rng[1] for rng in cache._buckets.values()), default=0)  # begin_level of the level that ran out
+            cache._buckets.setdefault(end_cost, [start, start])
+            self.outcome = self._finish(OutOfMemory(stats))
+        elif status == S_SOLVED:
+            self.outcome = self._finish(Solved(cache.build_candidate(op, li, ri), end_cost, stats))
+        else:
+            self.outcome = self._finish(CeilingReached(self.spec, self.alphabet, self.ceiling, stats))
+        return self.outcome
 
     def run(self) -> EnumOutcome:
         if self.outcome is not None:
@@ -365,6 +398,8 @@ class Enumeration:
         cfg, cache, core, stats = self.cfg, self.cache, self.core, self.stats
         ops = enabled_ops(cfg)
         atom_c = cfg.cost.of(OP_ATOM)
+        if self.native_loop and hasattr(core, "run_search"):
+            return self._run_in_core(ops, atom_c)
         for c in range(atom_c + 1, self.ceiling):
             _check_deadline(cfg)
             t0 = time.perf_counter()

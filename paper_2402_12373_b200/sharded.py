@@ -227,6 +227,8 @@ class ShardedCore:
     n_entries = property(lambda s: s.local.counters()[0])
 
     def set_option(self, name, value):
+        if name == "deadline_ms":
+            return  # ranks must take every decision together: the deadline stays a per-level check of the caller
         if hasattr(self.local, "set_option"):
             self.local.set_option(name, value)
 
@@ -273,14 +275,9 @@ class ShardedCore:
         fp = fp[:keep]
         tk = self._tick("solver_allreduce", tk)
 
-        # 3: route to hash owners, file, route the verdicts back
-        owner = owner_of(fp, G)
-        # stable grouping by destination: one radix pass over byte keys (G <= 255 ranks on a box)
-        order = torch.sort(owner.to(torch.uint8), stable=True)[1] if G > 1 else torch.arange(keep, device=dev)
-        # per-destination counts: G compare-and-sum passes (bincount funnels 10^7 atomics into G addresses)
-        counts = torch.stack([(owner == d).sum() for d in range(G)]).tolist() if keep else [0] * G
-        ranks_global = gbase + lo + torch.arange(keep, dtype=torch.int64, device=dev)
-        send = torch.cat([fp[order], ranks_global[order].unsqueeze(1)], 1).contiguous()
+        # 3: route to hash owners, file, route the verdicts back.  Grouping by owner (a stable counting sort) and the
+        # extraction of the winners' ranks run in the library (`ltl_core_stage_route` / `_winners`), not as tensor ops
+        send, counts = local.stage_route(fp, gbase + lo, G)
         tk = self._tick("route_sort", tk)
         recv, recv_counts = comm.all_to_all(send, counts)
         tk = self._tick("all_to_all", tk)
@@ -288,9 +285,7 @@ class ShardedCore:
         tk = self._tick("file", tk)
         win_sorted, _ = comm.all_to_all(win_recv, recv_counts)
         tk = self._tick("all_to_all_back", tk)
-        win = torch.zeros(keep, dtype=torch.uint8, device=dev)
-        win[order] = win_sorted
-        winners = lo + torch.nonzero(win, as_tuple=False).flatten()  # ascending level ranks
+        winners = local.stage_winners(send, win_sorted, gbase + lo, lo)  # ascending level ranks
         tk = self._tick("winners", tk)
 
         # 4: global numbering in rank order, budget cut
@@ -416,6 +411,8 @@ class RowShardedCore:
     n_entries = property(lambda s: s.local.counters()[0])
 
     def set_option(self, name, value):
+        if name == "deadline_ms":
+            return  # every pass is collective: a rank that stopped alone would leave the others in the all-reduce
         self.local.set_option(name, value)
 
     def transfer_stats(self):

@@ -12,6 +12,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2402_12373_b200 import workloads as Wl  # noqa: E402
 from paper_2402_12373_b200.core import make_core  # noqa: E402
 from paper_2402_12373_b200.learner import learn  # noqa: E402
+from paper_2402_12373_b200.scheme import HashScheme  # noqa: E402
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c2_planted")
@@ -19,6 +20,7 @@ ap.add_argument("--max-cost", type=int, default=None)
 ap.add_argument("--budget-gb", type=float, default=150.0)
 ap.add_argument("--stats", action="store_true")
 ap.add_argument("--repeat", type=int, default=1)
+ap.add_argument("--hash", default="mueller", help="fingerprint scheme (scheme.py): mueller | mueller_blocked | nh | fkp")
 ap.add_argument("--unsolvable", action="store_true", help="random traces of the config's shape: every level is exhaustive")
 a = ap.parse_args()
 t0 = time.time()
@@ -47,7 +49,7 @@ def factory(*args, **kw):
 for rep in range(a.repeat):
     t0 = time.time()
     res = learn(spec, None, alphabet, max_cost=a.max_cost or wl["max_cost"], budget_bytes=int(a.budget_gb * (1 << 30)),
-                core_factory=factory)
+                core_factory=factory, hash=HashScheme(a.hash))
     dt = time.time() - t0
     print(f"run {rep}: {res.status} {res.text!r} cost={res.cost} offered={res.stats.offered} admitted={res.stats.admitted} "
           f"wall={dt * 1e3:.1f} ms  search={res.stats.search_seconds * 1e3:.1f} ms  "

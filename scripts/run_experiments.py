@@ -24,6 +24,8 @@ ap.add_argument("--base-seed", type=int, default=0)
 ap.add_argument("--sweep-formula", default="F (p0 & X p1) & G (p1 | X p0)")
 ap.add_argument("--sweep-traces", type=int, default=24, help="traces per side of the masking-sweep specification")
 ap.add_argument("--sweep-len", default="20,40")
+ap.add_argument("--hashes", default="mueller,fkp",
+                help="schemes of the RUC experiment; 'nh' / 'mueller_blocked' force this build's hashes at every size")
 ap.add_argument("--out", default=None)
 a = ap.parse_args()
 
@@ -37,7 +39,7 @@ for variant in ("mueller", "fkp"):
     sweeps[variant] = [{k: r.get(k) for k in ("k", "status", "cost", "wall_ms", "offered", "admitted")} for r in rows]
 t1 = time.perf_counter()
 ruc = B.run_ruc_experiment(a.seeds, ext_sizes=tuple(int(v) for v in a.ext.split(",")), base_seed=a.base_seed,
-                           skip_failed_generations=True)
+                           skip_failed_generations=True, hashes=tuple(a.hashes.split(",")))
 t2 = time.perf_counter()
 report = {"masking_sweep": {"formula": a.sweep_formula, "traces_per_side": a.sweep_traces, "lengths": [lo, hi],
                             "rows": sweeps, "wall_s": round(t1 - t0, 3)},

@@ -120,6 +120,23 @@ class OracleStageCore:
                 break
         return fp, solver
 
+    def stage_route(self, fp, rank_base, world):
+        """(hi, lo, global rank) tuples grouped by owner, in rank order inside a group, and the per-owner counts
+        (`ltl_core_stage_route`)."""
+        from paper_2402_12373_b200.sharded import owner_of
+
+        keep = fp.shape[0]
+        owner = owner_of(fp, world)
+        order = torch.sort(owner, stable=True)[1] if keep else torch.zeros(0, dtype=torch.int64)
+        counts = [int((owner == d).sum()) for d in range(world)]
+        ranks = int(rank_base) + torch.arange(keep, dtype=torch.int64)
+        return torch.cat([fp[order], ranks[order].unsqueeze(1)], 1).contiguous(), counts
+
+    def stage_winners(self, send, win, rank_base, level_lo):
+        """Ascending level ranks of the winners among the tuples sent (`ltl_core_stage_winners`)."""
+        ranks = send[:, 2][win.to(torch.bool)] - int(rank_base) + int(level_lo)
+        return torch.sort(ranks)[0]
+
     def stage_file(self, tuples):
         gbase = self.offered
         rows = [(_u64(int(a)), _u64(int(b)), int(c)) for a, b, c in tuples.tolist()]

@@ -196,9 +196,13 @@ def test_transcripts_golden():
         cuda.close()
 
 
+@pytest.mark.parametrize("native_loop", [True, False], ids=["run_search", "run_level"])
 @pytest.mark.parametrize("case", golden()["learn"], ids=lambda c: c["name"])
-def test_learn_golden_cases(case):
-    """The product path end to end (learner -> C ABI -> CUDA) against the reference's recorded outcomes."""
+def test_learn_golden_cases(case, native_loop, monkeypatch):
+    """The product path end to end (learner -> C ABI -> CUDA) against the reference's recorded outcomes, with the
+    cost-level loop inside the library (`ltl_core_run_search`, the default) and with one `run_level` call per level
+    from `learner.py`."""
+    monkeypatch.setattr(L.Enumeration, "native_loop", native_loop)
     spec, alphabet = spec_from_golden(case)
     cfg = cfg_from_golden(case["cfg"])
     cores = []
@@ -474,3 +478,109 @@ def test_fused_not_levels_match_unfused(R, err_max, budget_entries, chunk, varia
     assert (records_array(a) == records_array(b)).all()
     a.close()
     b.close()
+
+
+def test_deadline_interrupts_a_level_between_passes():
+    """The reference checks its deadline between the chunks of a level (`enumerator.py:278`, `290`); here a level is one
+    library call, so the core checks it between its passes (`deadline_ms`, status LTL_S_TIMEOUT): a search whose last
+    level alone takes seconds is abandoned shortly after the deadline, not at the end of the level; what earlier passes
+    admitted stays admitted, and a deadline that never fires changes nothing."""
+    import time
+
+    from paper_2402_12373_b200 import workloads as Wl
+    from paper_2402_12373_b200.errors import TimeoutExceeded
+    from paper_2402_12373_b200.learner import S_TIMEOUT, Segment, learn
+
+    spec, alphabet = Wl.random_spec(3, 512, 512, 64, 64, 77)  # nothing solves: every level is exhaustive
+    free = learn(spec, None, alphabet, max_cost=8)
+    timed = learn(spec, None, alphabet, max_cost=8, deadline_s=600.0)  # armed, never fires: smaller passes, same result
+    assert (timed.status, timed.stats.offered, timed.stats.admitted) == (free.status, free.stats.offered, free.stats.admitted)
+    assert [(r["cost"], r["offered"], r["admitted"]) for r in timed.stats.levels] == \
+        [(r["cost"], r["offered"], r["admitted"]) for r in free.stats.levels]
+    t0 = time.monotonic()
+    with pytest.raises(TimeoutExceeded):
+        # cost levels up to 10 take ~5 ms, level 11 (12 M candidates, six passes with a deadline armed) ~15 ms
+        learn(spec, None, alphabet, max_cost=13, deadline_s=0.01, budget_bytes=100 << 30)
+    assert time.monotonic() - t0 < 1.0
+    # on the core itself: the status, and the entries of the passes that ran
+    masks = np.full(1024, ~np.uint64(0), dtype=np.uint64)
+    core = CudaCore(masks, 512, -1, V_NH, budget_bytes=8 << 30)
+    rng = np.random.default_rng(5)
+    for k in range(3):
+        assert core.add_entry(rng.integers(0, 1 << 63, size=1024, dtype=np.uint64), 0, k, -1) == k
+    assert core.run_level([Segment(2, 0, 3, 0, 3, False)])[0] == 0
+    core.set_option("chunk_candidates", 4)
+    core.set_option("deadline_ms", 1)
+    time.sleep(0.01)
+    n0 = core.n_entries
+    assert core.run_level([Segment(3, 0, n0, 0, n0, False)])[0] == S_TIMEOUT and core.n_entries == n0
+    core.set_option("deadline_ms", 0)
+    assert core.run_level([Segment(3, 0, n0, 0, n0, False)])[0] == 0 and core.n_entries > n0
+    core.close()
+
+
+def test_debug_mask_invariant(monkeypatch):
+    """The reference's LTLLEARN_DEBUG_MASKS assertion (`bitsem.py:46-61`: no characteristic bit outside the validity
+    mask after any operation) on the device: with the variable set (or option ``debug_masks``) every matrix the core
+    stores is checked -- a whole search over ragged traces passes unchanged, a bad matrix is refused."""
+    from paper_2402_12373_b200.learner import learn
+
+    spec, alphabet = random_spec(np.random.default_rng(91), 2, 70, 70, 0, 90)  # ragged lengths, two words per row
+    plain = learn(spec, None, alphabet, max_cost=6)
+    monkeypatch.setenv("LTLLEARN_DEBUG_MASKS", "1")
+    checked = learn(spec, None, alphabet, max_cost=6)
+    assert (checked.status, checked.text, checked.stats.offered, checked.stats.admitted) == \
+        (plain.status, plain.text, plain.stats.offered, plain.stats.admitted)
+    half, al3 = random_spec(np.random.default_rng(92), 3, 90, 90, 0, 30)       # half-width store
+    assert learn(half, None, al3, max_cost=5).stats.admitted > 0
+    monkeypatch.delenv("LTLLEARN_DEBUG_MASKS")
+    masks = length_masks(np.array([5, 64, 0, 17]), 1).reshape(-1)
+    core = CudaCore(masks, 2, -1, V_MUELLER)
+    ok = np.array([0xF8 << 56, 1, 0, 1 << 63], dtype=np.uint64) & masks
+    bad = ok.copy()
+    bad[2] = 1 << 40  # a bit in an empty trace
+    assert core.add_entry(bad, 0, 0, -1) == 0  # unchecked by default, like the reference
+    core.set_option("debug_masks", 1)
+    assert core.add_entry(ok, 0, 1, -1) == 1
+    with pytest.raises(AssertionError, match="escaped the validity mask"):
+        core.add_entry(bad ^ np.uint64(1 << 41), 0, 2, -1)
+    core.close()
+
+
+@pytest.mark.parametrize("R,W,variant,fuse_not_min", [(64, 1, V_NH, 1), (200, 1, V_MUELLER, 1 << 30), (100, 2, V_NH, 1), (40, 16, V_NH, 1)])
+def test_phase_b_order_matches_oracle(R, W, variant, fuse_not_min):
+    """Phase B walks big right-operand buckets block by block (`k_mat_plan`: runs of consecutive new entries found from
+    the winner flags, processed as "for each block of j: all i"); the entries, their order and their matrices are those
+    of the entry-order walk.  Forced onto small levels here: blocks of 32 entries, every pass planned."""
+    from paper_2402_12373_b200.learner import Segment
+
+    rng = np.random.default_rng(R * 3 + W)
+    masks = random_masks(rng, R, W)
+    cuda, ora = make_pair(masks, R // 2, err_max=-1, variant=variant, W=W)
+    plain = CudaCore(masks, R // 2, -1, variant, words_per_row=W)
+    for name, value in (("small_admit", 0), ("order_min", 1), ("order_block_bytes", 8 * R * W * 32), ("fuse_not_min", fuse_not_min)):
+        cuda.set_option(name, value)
+    plain.set_option("order_mat", 0)
+    for k in range(6):
+        cm = random_cm(rng, masks)
+        assert cuda.add_entry(cm, 0, k, -1) == ora.add_entry(cm, 0, k, -1) == plain.add_entry(cm, 0, k, -1)
+    lo = 0
+    for _ in range(3):
+        hi = ora.n_entries
+        segs = [Segment(1, lo, hi), Segment(2, 0, hi, 0, hi, True), Segment(3, 0, lo, lo, hi, False), Segment(4, lo, hi),
+                Segment(5, lo, hi), Segment(6, lo, hi), Segment(7, 0, hi, 0, hi, False), Segment(7, 0, 3, 0, hi, False)]
+        segs = [s for s in segs if s.a1 > s.a0 and (s.unary or s.b1 > s.b0)]
+        st = cuda.run_level(segs)
+        assert plain.run_level(segs) == st
+        for s in segs:
+            got = ora.screen_unary(s.op, s.a0, s.a1) if s.unary else ora.screen_binary(s.op, s.a0, s.a1, s.b0, s.b1, s.tri)
+            assert got[0] == 0
+        assert st[0] == 0
+        lo = hi
+        if ora.n_entries > 4000:
+            break
+    assert ora.n_entries > 300
+    assert_same_state(cuda, ora)
+    assert (plain.export_cms() == cuda.export_cms()).all()
+    cuda.close()
+    plain.close()

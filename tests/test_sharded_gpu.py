@@ -208,3 +208,30 @@ def test_cli_learn_under_torchrun(tmp_path, sharding):
     rep = json.loads(out.read_text())
     assert rep["status"] == "solved" and rep["formula"] == "F G p0 & (p0 U p1)" and rep["cost"] == 7
     assert rep["verified_errors"] == 0 and rep["stats"]["offered"] == 5762
+
+
+@pytest.mark.parametrize("n,world", [(0, 2), (1, 1), (1, 3), (31, 2), (1025, 8), (5000, 3), (70000, 8), (4096, 64)])
+def test_stage_route_and_winners_match_the_tensor_formulation(n, world):
+    """`ltl_core_stage_route` (stable counting sort of (hi, lo, rank) tuples by hash owner) and `ltl_core_stage_winners`
+    (verdict bytes -> ascending winner ranks) against the tensor formulation they replace (stable sort by `owner_of`,
+    scatter, nonzero)."""
+    import torch
+
+    from paper_2402_12373_b200.core import CudaCore, V_NH
+    from paper_2402_12373_b200.sharded import owner_of
+
+    core = CudaCore(np.full(4, ~np.uint64(0), dtype=np.uint64), 2, -1, V_NH)
+    g = torch.Generator().manual_seed(n * 131 + world)
+    fp = torch.randint(-(1 << 62), 1 << 62, (n, 2), generator=g, dtype=torch.int64).cuda()
+    rank_base, level_lo = 10_000_000_019, 777
+    send, counts = core.stage_route(fp, rank_base, world)
+    owner = owner_of(fp, world)
+    order = torch.sort(owner, stable=True)[1] if n else torch.zeros(0, dtype=torch.int64, device="cuda")
+    want = torch.cat([fp[order], (rank_base + torch.arange(n, dtype=torch.int64, device="cuda"))[order].unsqueeze(1)], 1)
+    assert counts == [int((owner == d).sum()) for d in range(world)] and sum(counts) == n
+    assert torch.equal(send, want)
+    win = (torch.rand(n, generator=g) < 0.4).to(torch.uint8).cuda()
+    got = core.stage_winners(send, win, rank_base, level_lo)
+    want_ranks = torch.sort(send[:, 2][win.bool()] - rank_base + level_lo)[0]
+    assert torch.equal(got, want_ranks)
+    core.close()
