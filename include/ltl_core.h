@@ -140,6 +140,17 @@ LTL_API int ltl_core_create_on_traces(ltl_traces* t, int err_max, int variant, c
                                       ltl_core** out);
 LTL_API int ltl_core_add_atom(ltl_core* h, ltl_traces* t, int prop, int negated, int op, int lhs, int rhs, int64_t* index_out);
 
+/* Trace files (reference traces.py:180-253: one trace per line, positions separated by ';', each position a
+ * comma-separated 0/1 vector over the alphabet, a '---' line between positives and negatives; later sections ignored).
+ * Host code, two passes over the file's bytes: scan sizes the matrices (traces per side, longest trace, propositions per
+ * position, '---' lines beyond the first), fill writes uint16[n][L] character matrices (zero beyond each length) and
+ * the lengths.  Files not in canonical form (bytes other than 0 1 , ; - CR LF, ragged vectors, stray separators) are
+ * refused with LTL_ERR_ARG and *bad_line = the 1-based line: the caller's line-by-line reader owns the messages. */
+LTL_API int ltl_trace_file_scan(const char* data, uint64_t n, int64_t counts_out[2], int* max_len, int* width,
+                                int* extra_sections, int64_t* bad_line);
+LTL_API int ltl_trace_file_fill(const char* data, uint64_t n, int width, int L, uint16_t* pos_chars, int64_t* pos_lengths,
+                                uint16_t* neg_chars, int64_t* neg_lengths);
+
 /* Constructor: reference _speedups.pyx:79-111 (Core.__cinit__) / kernels.py:140-172 (make_core).
  * masks: uint64[R*W] length masks.  proj_rows/proj_offs (n_proj <= 126 pairs): gather projection
  * (row, position).  fkp_bits: per-row prefix width of the fkp variant.  mask_k: low fingerprint bits

@@ -117,6 +117,9 @@ def load_library():
     for name in ("ltl_traces_create", "ltl_traces_pack", "ltl_traces_info", "ltl_traces_suspects", "ltl_traces_export",
                  "ltl_core_create_on_traces", "ltl_core_add_atom"):
         getattr(L, name).restype = C.c_int
+    L.ltl_trace_file_scan.argtypes = [C.c_char_p, C.c_uint64, i64p, ip, ip, ip, i64p]
+    L.ltl_trace_file_fill.argtypes = [C.c_char_p, C.c_uint64, C.c_int, C.c_int, u16p, i64p, u16p, i64p]
+    L.ltl_trace_file_scan.restype = L.ltl_trace_file_fill.restype = C.c_int
     L.ltl_core_level_size.argtypes = [vp, C.POINTER(Segment), C.c_int, i64p]
     L.ltl_core_stage_eval.argtypes = [vp, C.POINTER(Segment), C.c_int, C.c_int64, C.c_int64, vp, i64p]
     L.ltl_core_stage_file.argtypes = [vp, vp, C.c_int64, vp, i64p]
@@ -176,6 +179,28 @@ def pack_traces(chars: np.ndarray, lengths: np.ndarray, n_props: int, words_per_
             raise ValueError(msg)
         raise CoreError(f"ltl_pack_traces failed ({rc}): {msg}")
     return masks, atoms
+
+
+def parse_trace_file(data: bytes):
+    """Canonical-form trace file bytes -> ``(pos_chars, pos_lengths, neg_chars, neg_lengths, width, extra_sections)``
+    through the library's two-pass reader (`ltl_trace_file_scan` / `_fill`; host code, no device needed), or None when the
+    file is not in canonical form (the line-by-line reader then owns the error message)."""
+    L = load_library()
+    counts = (C.c_int64 * 2)()
+    max_len, width, extra = C.c_int(), C.c_int(), C.c_int()
+    bad = C.c_int64()
+    if L.ltl_trace_file_scan(data, len(data), counts, C.byref(max_len), C.byref(width), C.byref(extra), C.byref(bad)):
+        return None
+    if width.value < 1:
+        return None
+    n_pos, n_neg, width_l = int(counts[0]), int(counts[1]), max(int(max_len.value), 1)
+    pc, nc = np.zeros((n_pos, width_l), dtype=np.uint16), np.zeros((n_neg, width_l), dtype=np.uint16)
+    pl, nl = np.zeros(n_pos, dtype=np.int64), np.zeros(n_neg, dtype=np.int64)
+    u16p, i64p = C.POINTER(C.c_uint16), C.POINTER(C.c_int64)
+    if L.ltl_trace_file_fill(data, len(data), width.value, width_l, pc.ctypes.data_as(u16p), pl.ctypes.data_as(i64p),
+                             nc.ctypes.data_as(u16p), nl.ctypes.data_as(i64p)):
+        return None
+    return pc, pl, nc, nl, int(width.value), int(extra.value)
 
 
 class DeviceTraces:

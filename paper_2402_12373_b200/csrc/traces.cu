@@ -420,4 +420,109 @@ int ltl_traces_export(ltl_traces* t, uint64_t* masks_out, uint64_t* atoms_out) {
     return LTL_OK;
 }
 
+// ---- trace files (reference traces.py:180-253: one trace per line, positions separated by ';', each position a
+// comma-separated 0/1 vector over the alphabet, a '---' line between positives and negatives).  Host code: one pass to
+// size the matrices, one to fill them; files that are not in canonical form (any other byte, ragged vectors, stray
+// separators) are refused with the line number and left to the caller's line-by-line reader, which owns the messages.
+static int trace_file_walk(const char* data, size_t n, int* width_io, int64_t counts[2], int* max_len, int* extra_sections,
+                           int64_t* bad_line, uint16_t* chars[2], int64_t* lengths[2], int L) {
+    int width = *width_io;
+    int section = 0;
+    int64_t line_no = 0, rows[2] = {0, 0};
+    size_t i = 0;
+    int longest = 0;
+    while (i < n) {
+        line_no++;
+        size_t e = i;
+        while (e < n && data[e] != '\n') e++;
+        size_t a = i, b = e;
+        while (b > a && data[b - 1] == '\r') b--;
+        i = e + 1;
+        if (a == b) continue;  // blank line
+        if (data[a] == '-') {
+            if (b - a != 3 || data[a + 1] != '-' || data[a + 2] != '-') {
+                *bad_line = line_no;
+                return LTL_ERR_ARG;
+            }
+            section++;
+            continue;
+        }
+        // one trace: digits separated by ',' inside a position and ';' between positions
+        int positions = 0, in_pos = 0;
+        uint16_t ch = 0;
+        uint16_t* out = (chars && section < 2) ? chars[section] + (size_t)rows[section] * (size_t)L : nullptr;
+        bool expect_digit = true;
+        for (size_t k = a; k < b; k++) {
+            const char c = data[k];
+            if (expect_digit) {
+                if (c != '0' && c != '1') {
+                    *bad_line = line_no;
+                    return LTL_ERR_ARG;
+                }
+                if (c == '1' && in_pos < 16) ch |= (uint16_t)(1u << in_pos);
+                in_pos++;
+                expect_digit = false;
+            } else {
+                if (c == ',') {
+                    expect_digit = true;
+                } else if (c == ';') {
+                    if (width < 0) width = in_pos;
+                    if (in_pos != width) {
+                        *bad_line = line_no;
+                        return LTL_ERR_ARG;
+                    }
+                    if (out && positions < L) out[positions] = ch;
+                    positions++;
+                    in_pos = 0;
+                    ch = 0;
+                    expect_digit = true;
+                } else {
+                    *bad_line = line_no;
+                    return LTL_ERR_ARG;
+                }
+            }
+        }
+        if (expect_digit) {  // the line ended in a separator
+            *bad_line = line_no;
+            return LTL_ERR_ARG;
+        }
+        if (width < 0) width = in_pos;
+        if (in_pos != width || width > 16) {
+            *bad_line = line_no;
+            return LTL_ERR_ARG;
+        }
+        if (out && positions < L) out[positions] = ch;
+        positions++;
+        if (section < 2) {
+            if (lengths) lengths[section][rows[section]] = positions;
+            rows[section]++;
+            longest = std::max(longest, positions);
+        }
+    }
+    *width_io = width;
+    counts[0] = rows[0];
+    counts[1] = rows[1];
+    *max_len = longest;
+    *extra_sections = section - 1;
+    return LTL_OK;
+}
+
+int ltl_trace_file_scan(const char* data, uint64_t n, int64_t counts_out[2], int* max_len, int* width, int* extra_sections,
+                        int64_t* bad_line) {
+    if ((n && !data) || !counts_out || !max_len || !width || !extra_sections || !bad_line) return LTL_ERR_ARG;
+    *bad_line = 0;
+    *width = -1;
+    return trace_file_walk(data, (size_t)n, width, counts_out, max_len, extra_sections, bad_line, nullptr, nullptr, 0);
+}
+
+int ltl_trace_file_fill(const char* data, uint64_t n, int width, int L, uint16_t* pos_chars, int64_t* pos_lengths,
+                        uint16_t* neg_chars, int64_t* neg_lengths) {
+    if ((n && !data) || width < 1 || L < 0) return LTL_ERR_ARG;
+    int64_t counts[2], bad = 0;
+    int max_len = 0, extra = 0, w = width;
+    uint16_t* chars[2] = {pos_chars, neg_chars};
+    int64_t* lengths[2] = {pos_lengths, neg_lengths};
+    return trace_file_walk(data, (size_t)n, &w, counts, &max_len, &extra, &bad, chars, lengths, L);
+}
+
 }  // extern "C"

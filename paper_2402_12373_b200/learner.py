@@ -309,17 +309,21 @@ class Enumeration:
         stats.ceiling = overfit_cost(spec, alphabet, h)
         self.ceiling = stats.ceiling if cfg.ceiling is None else min(cfg.ceiling, stats.ceiling)
         atom_c = h.of(OP_ATOM)
+        fast = None
         for p in range(alphabet.size):
             if info["atom_errors"][p] <= err_max:
-                stats.atom_fast_path = True
-                self.outcome = Solved(Atom(p), atom_c, stats)
-                return
-        if cfg.require_nnf:
+                fast = Solved(Atom(p), atom_c, stats)
+                break
+        if fast is None and cfg.require_nnf:
             for p in range(alphabet.size):
                 if info["neg_atom_errors"][p] <= err_max:
-                    stats.atom_fast_path = True
-                    self.outcome = Solved(Not(Atom(p)), atom_c + h.of(OP_NOT), stats)
-                    return
+                    fast = Solved(Not(Atom(p)), atom_c + h.of(OP_NOT), stats)
+                    break
+        if fast is not None:
+            stats.atom_fast_path = True
+            stats.h2d_bytes, stats.d2h_bytes = info["h2d_bytes"], info["d2h_bytes"]  # the upload is all this search moved
+            self.outcome = fast
+            return
         t_scheme = time.perf_counter()
         words = info["words"]
         rs = resolve_scheme(cfg.hash, spec.lengths, SuffixTable.from_spec(spec, limit=126), words_per_row=words)

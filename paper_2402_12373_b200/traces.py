@@ -403,7 +403,8 @@ def _parse_line(line: str, line_no: int, width):
     return tuple(chars), width
 
 
-def load_spec(path) -> tuple[Specification, Alphabet]:
+def _load_spec_lines(path) -> tuple[Specification, Alphabet]:
+    """Line-by-line parser: the reference's reader (`traces.py:185-253`), with its error messages."""
     sections: list[list] = [[]]
     width = None
     with open(path, "r", encoding="utf-8") as fh:
@@ -423,6 +424,108 @@ def load_spec(path) -> tuple[Specification, Alphabet]:
     if width is None:
         raise TraceFormatError("empty trace file")
     return Specification(tuple(sections[0]), tuple(sections[1])), Alphabet.default(width)
+
+
+def _load_spec_arrays(data: bytes):
+    """Whole-file parser for files in canonical form (only the bytes ``0 1 , ; -`` and line ends): every step is one
+    numpy pass over the file, so 2^21 traces parse in seconds instead of minutes.  Returns ``(pc, pl, nc, nl, width,
+    extra_sections)`` or None when the file needs the line-by-line reader (other bytes, malformed lines: that reader owns
+    the error messages)."""
+    b = np.frombuffer(data, dtype=np.uint8)
+    if len(b) == 0:
+        return None
+    if b[-1] != 10:
+        b = np.concatenate([b, np.array([10], dtype=np.uint8)])
+    is_nl, is_cr = b == 10, b == 13
+    is_d = (b == 48) | (b == 49)
+    is_c, is_s, is_m = b == 44, b == 59, b == 45
+    if not (is_nl | is_cr | is_d | is_c | is_s | is_m).all():
+        return None
+    line_of = np.cumsum(is_nl) - is_nl  # line index of every byte (the newline belongs to its line)
+    n_lines = int(line_of[-1]) + 1
+
+    def per_line(mask):
+        return np.bincount(line_of[mask], minlength=n_lines)
+
+    n_d, n_c, n_s, n_m = per_line(is_d), per_line(is_c), per_line(is_s), per_line(is_m)
+    blank = (n_d + n_c + n_s + n_m) == 0
+    sep = (n_m == 3) & (n_d + n_c + n_s == 0)
+    if ((n_m > 0) & ~sep).any():
+        return None
+    trace = ~blank & ~sep
+    if not trace.any():
+        return None
+    first = int(np.flatnonzero(trace)[0])
+    n_pos_first = int(n_s[first]) + 1
+    if n_d[first] % n_pos_first:
+        return None
+    width = int(n_d[first]) // n_pos_first
+    if width < 1 or width > 16:
+        return None
+    n_positions = n_s + 1
+    ok = (n_d == n_positions * width) & (n_c == n_positions * (width - 1))
+    if not ok[trace].all():
+        return None
+    # token structure: between two digits of a line sits exactly one separator (so no "01", ",," or ";," forms)
+    body = ~(is_nl | is_cr | is_m)
+    prev_is_d = np.concatenate([[False], is_d[:-1]])
+    prev_is_body = np.concatenate([[False], body[:-1]])
+    if (is_d & prev_is_d).any() or ((is_c | is_s) & ~prev_is_d).any():
+        return None
+    line_end_sep = is_nl & np.concatenate([[False], (is_c | is_s)[:-1]])  # a line must not end in a separator
+    if line_end_sep.any():
+        return None
+    del prev_is_body
+    # digit k of a line is proposition k % width of position k // width
+    d_idx = np.flatnonzero(is_d)
+    d_line = line_of[d_idx]
+    first_digit = np.zeros(n_lines, dtype=np.int64)
+    first_digit[1:] = np.cumsum(n_d)[:-1]
+    k = np.arange(len(d_idx), dtype=np.int64) - first_digit[d_line]
+    ones = b[d_idx] == 49
+    # separators must alternate correctly: the separator before digit k > 0 is ';' iff k % width == 0
+    sep_before = np.zeros(len(d_idx), dtype=np.uint8)
+    has_prev = k > 0
+    sep_before[has_prev] = b[d_idx[has_prev] - 1]
+    if ((sep_before[has_prev] == 59) != (k[has_prev] % width == 0)).any():
+        return None
+    section = np.cumsum(sep)[trace]  # section index of every trace line
+    t_lines = np.flatnonzero(trace)
+    t_index = np.full(n_lines, -1, dtype=np.int64)
+    t_index[t_lines] = np.arange(len(t_lines))
+    lengths = n_positions[t_lines].astype(np.int64)
+    L = int(lengths.max())
+    rows = t_index[d_line[ones]]
+    kk = k[ones]
+    flat = np.bincount(rows * L + kk // width, weights=(1 << (kk % width)).astype(np.float64), minlength=len(t_lines) * L)
+    chars = flat.astype(np.uint16).reshape(len(t_lines), L)
+    p_sel, n_sel = section == 0, section == 1
+    return chars[p_sel], lengths[p_sel], chars[n_sel], lengths[n_sel], width, int(sep.sum()) - 1
+
+
+def load_spec(path, *, device: int | None = None) -> tuple[Specification, Alphabet]:
+    """Read a trace file (reference `traces.py:185-253`).  Big files in canonical form are parsed by the library's two-pass
+    byte reader (`core.parse_trace_file`; 2^21 traces: about a second), or with whole-file numpy passes when the library
+    is not built (`_load_spec_arrays`); anything else -- and every malformed file -- goes through the reference's line-by-line reader,
+    which owns the error messages.  ``device``: keep the specification resident on that GPU (`from_arrays`)."""
+    with open(path, "rb") as fh:
+        data = fh.read()
+    got = None
+    if len(data) > (1 << 14) or device is not None:
+        try:  # the library's two-pass byte reader (host code); without the library: the numpy passes
+            from .core import parse_trace_file
+
+            got = parse_trace_file(data)
+        except Exception:  # noqa: BLE001 -- e.g. the library is not built
+            got = _load_spec_arrays(data)
+    if got is None:
+        return _load_spec_lines(path)
+    pc, pl, nc, nl, width, extra = got
+    if extra < 0:
+        raise TraceFormatError("missing '---' separator between trace blocks")
+    if extra > 0:
+        warnings.warn(f"{path}: ignoring {extra} extra '---' section(s)")
+    return Specification.from_arrays(pc, pl, nc, nl, device=device), Alphabet.default(width)
 
 
 def format_trace(tr, width: int) -> str:

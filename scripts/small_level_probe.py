@@ -15,12 +15,17 @@ from paper_2402_12373_b200.learner import learn  # noqa: E402
 name = sys.argv[1] if len(sys.argv) > 1 else "c1_tiny"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 200
 opts = dict(kv.split("=") for kv in sys.argv[3:])
+if "native_loop" in opts:  # 0: one run_level call per cost level from learner.py instead of ltl_core_run_search
+    from paper_2402_12373_b200 import learner as _L
+
+    _L.Enumeration.native_loop = bool(int(opts.pop("native_loop")))
 spec, al, f, cfg = Wl.make_config(name)
 P = (spec.chars[: spec.n_pos].copy(), spec.lengths[: spec.n_pos].copy())
 N = (spec.chars[spec.n_pos:].copy(), spec.lengths[spec.n_pos:].copy())
 
 acc = {"run_level": 0.0, "calls": 0, "sync": 0.0, "launches": 0}
 real_run_level = C.CudaCore.run_level
+real_run_search = C.CudaCore.run_search
 real_close = C.CudaCore.close
 
 
@@ -32,6 +37,14 @@ def timed_run_level(self, segs):
     return out
 
 
+def timed_run_search(self, *a, **kw):
+    t0 = time.perf_counter()
+    out = real_run_search(self, *a, **kw)
+    acc["run_level"] += time.perf_counter() - t0
+    acc["calls"] += len(out[5])
+    return out
+
+
 def close(self):
     if getattr(self, "_h", None):
         acc["sync"] += self.host_times()["sync_ms"]
@@ -40,6 +53,7 @@ def close(self):
 
 
 C.CudaCore.run_level = timed_run_level
+C.CudaCore.run_search = timed_run_search
 C.CudaCore.close = close
 C.CudaCore.__del__ = close
 

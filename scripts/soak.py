@@ -34,6 +34,10 @@ if os.environ.get("SOAK_ONLY"):
 FORMULAS = ["p0 U (p1 & X p0)", "F (p0 & X p1)", "G (p0 | X p1)", "(p0 U p1) & F G p0", "X X p1 | G p0", "!p0 & F p1"]
 
 
+def W_ALL(spec):
+    return -(-spec.max_len // 64)
+
+
 def summary(res):
     lv = [(x["cost"], x["offered"], x["admitted"], x["duplicates"], x["bytes"]) for x in res.stats.levels]
     return res.status, res.text, res.cost, res.stats.offered, res.stats.admitted, res.stats.duplicates, lv
@@ -108,6 +112,24 @@ while time.time() < t_end:
     runs["single"] = [summary(L.learn(spec, None, al, **kw))]
     os.environ["LTL_CORE_OPTIONS"] = fused_opts
     runs["fused"] = [summary(L.learn(spec, None, al, **kw))]
+    # round 2 paths: the level loop driven from Python (one run_level per level) with the big-pass bookkeeping kernels and
+    # the phase-B order forced onto every pass (blocks of 32 entries); the specification uploaded as array pairs and
+    # checked / packed / searched on the device; the reference's debug invariant on every stored matrix
+    n_words = spec.size * W_ALL(spec)
+    os.environ["LTL_CORE_OPTIONS"] = f"small_admit=0,order_min=1,order_block_bytes={8 * n_words * 32}" + (",fuse_not_min=0" if rng.random() < 0.5 else "")
+    L.Enumeration.native_loop = False
+    try:
+        runs["pyloop_ordered"] = [summary(L.learn(spec, None, al, **kw))]
+    finally:
+        L.Enumeration.native_loop = True
+    os.environ.pop("LTL_CORE_OPTIONS", None)
+    P_arr = (spec.chars[: spec.n_pos].copy(), spec.lengths[: spec.n_pos].copy())
+    N_arr = (spec.chars[spec.n_pos:].copy(), spec.lengths[spec.n_pos:].copy())
+    os.environ["LTLLEARN_DEBUG_MASKS"] = "1"
+    try:
+        runs["arrays_debug"] = [summary(L.learn(P_arr, N_arr, al, **kw))]
+    finally:
+        os.environ.pop("LTLLEARN_DEBUG_MASKS", None)
     hashed = kw.get("hash", HashScheme()).variant != "fkp" and want is not None
     W = -(-spec.max_len // 64)
     for world in (2, 3):
