@@ -19,7 +19,7 @@ elif case == "rowsplit":
     from paper_2402_12373_b200.learner import learn
     spec, alphabet = Wl.random_spec(2, 300, 300, 70, 150, 5)
     r = learn(spec, None, alphabet, max_cost=5)
-    print("rowsplit", r.status, r.text, r.stats.offered)
+    print("rowsplit", r.status, (r.text or "")[:60], r.stats.offered)
     spec, alphabet = Wl.random_spec(3, 260, 260, 20, 64, 9)
     r = learn(spec, None, alphabet, max_cost=5, budget_bytes=3000 * (520 * 8 + 16))
     print("budget", r.status, r.stats.offered, r.stats.admitted)
