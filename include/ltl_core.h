@@ -241,6 +241,12 @@ LTL_API int ltl_core_counters(ltl_core* h, uint64_t out[5]);
  * Call once, right after ltl_core_create.  Needs a block-combinable fingerprint (LTL_V_MUELLER / LTL_V_NH / LTL_V_NH32). */
 typedef int (*ltl_exchange_fn)(void* ctx, void* d_sums, int64_t count);
 LTL_API int ltl_core_set_row_shard(ltl_core* h, int64_t word_base, int64_t total_words, ltl_exchange_fn fn, void* ctx);
+/* Optional, right after ltl_core_set_row_shard: shard the uniqueness table as well.  Core `shard` of `n_shards` then
+ * files only the candidates whose fingerprint it owns (owner = mix(hi ^ lo) mod n_shards, the rule of the
+ * candidate-range shards), the winner flags -- one bit per candidate, set by one shard at most -- are OR-ed over the
+ * shards through `fn` (a wrapping sum of disjoint bits), and every core compacts the same winners.  The table's memory
+ * and the work of filing keys then scale with the number of GPUs like everything else; results are unchanged. */
+LTL_API int ltl_core_set_table_shard(ltl_core* h, int shard, int n_shards);
 
 /* Tuning / measurement (no reference counterpart).
  * options: "deadline_ms" (run_level / screen_* return LTL_S_TIMEOUT at the first pass boundary more than this many

@@ -91,6 +91,8 @@ def load_library():
     L.ltl_core_counters.argtypes = [vp, u64p]
     L.ltl_core_set_option.argtypes = [vp, C.c_char_p, C.c_int64]
     L.ltl_core_set_row_shard.argtypes = [vp, C.c_int64, C.c_int64, EXCHANGE_FN, vp]
+    L.ltl_core_set_table_shard.argtypes = [vp, C.c_int, C.c_int]
+    L.ltl_core_set_table_shard.restype = C.c_int
     L.ltl_core_kernel_stats.argtypes = [vp, C.c_int, u64p, C.POINTER(C.c_double), C.POINTER(C.c_double), u64p]
     L.ltl_core_reset_kernel_stats.argtypes = [vp]
     L.ltl_core_info.argtypes = [vp, u64p]
@@ -536,6 +538,10 @@ class CudaCore:
         self._exchange_error = None
         self._exchange_cb = EXCHANGE_FN(hook)  # keep the trampoline alive as long as the core
         self._check(self._L.ltl_core_set_row_shard(self._h, int(word_base), int(total_words), self._exchange_cb, None))
+
+    def set_table_shard(self, shard: int, n_shards: int):
+        """Row shards: also shard the uniqueness table by fingerprint owner (`ltl_core_set_table_shard`)."""
+        self._check(self._L.ltl_core_set_table_shard(self._h, int(shard), int(n_shards)))
 
     # -- multi-GPU stages (device tensors in / out; see sharded.py) -----------------------
     @staticmethod

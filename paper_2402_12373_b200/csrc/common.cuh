@@ -136,6 +136,9 @@ struct ScreenParams {
     // go to acc_* -- they are summed across GPUs before k_finalize completes the candidates
     u32 blk_base;
     int defer;
+    // row shards with a sharded uniqueness table: a candidate is filed only by the shard that owns its fingerprint
+    // (fp_owner); the winner flags are OR-ed over the shards afterwards.  owner_world <= 1: every key is ours
+    int owner_world, owner_rank;
 };
 
 struct MaterializeParams {
@@ -203,6 +206,12 @@ struct NhKeys {
 static __constant__ NhKeys c_nh = NhKeys();
 #endif
 static constexpr NhKeys h_nh = NhKeys();
+
+// owner shard of a fingerprint: same integer mix as sharded.py owner_of
+__host__ __device__ __forceinline__ int fp_owner(u64 hi, u64 lo, int world) {
+    const u64 x = (hi ^ lo) * K_STEP;
+    return (int)(((x >> 33) & 0x7FFFFFFFull) % (u64)world);
+}
 
 __host__ __device__ __forceinline__ size_t cm_index(i64 e, i64 n, i64 k) {
     return ((size_t)(e >> 5) * (size_t)n + (size_t)k) * LTL_GROUP + (size_t)(e & 31);

@@ -206,7 +206,8 @@ __global__ void __launch_bounds__(RES_CTA) k_emit(const u32* __restrict__ flagw,
 // k_finalize + k_resolve + k_scan + k_emit do for big passes -- complete the row-split candidates, decide the winners
 // (lowest rank per key), compact them in rank order and write their records -- 1024 candidates per round with a running
 // offset.  It also zeroes the partial sums it consumed, so the next small pass needs no memset.
-#define LTL_SMALL_ADMIT 32768
+#define LTL_SMALL_ADMIT 8192  // (one CTA takes ~1.5 us per 1024 candidates: at 20 K candidates -- config 5, cost level 6 --
+                              // it cost 32 us where the four full-width kernels need 18)
 template <bool MUELLER>
 __global__ void __launch_bounds__(RES_CTA) k_admit_small(const __grid_constant__ ScreenParams p, u64 total, int finalize,
                                                          i64 n_base, u64 cap_left, unsigned char* __restrict__ rec_op,
@@ -413,6 +414,15 @@ __global__ void k_check_masks(const u64* __restrict__ cms, const u64* __restrict
     if (e >= first && e < first + count && (cms[cm_index(e, n, k)] & ~masks[k])) atomicAdd(bad, 1ull);
 }
 
+__global__ void k_found_to_acc(const Ctl* ctl, u64* acc) {
+    acc[0] = ctl->found;
+    acc[1] = acc[2] = 0;
+}
+__global__ void k_acc_to_found(Ctl* ctl, u64* acc) {
+    ctl->found = acc[0] ? 1ull : 0ull;
+    acc[0] = 0;
+}
+
 __global__ void k_set_record(unsigned char* rec_op, int* rec_lhs, int* rec_rhs, i64 e, int op, int lhs, int rhs) {
     rec_op[e] = (unsigned char)op;
     rec_lhs[e] = lhs;
@@ -463,11 +473,6 @@ __global__ void k_file_verdict(const u64* __restrict__ tuples, const u32* __rest
 }
 
 // ---- candidate-range shards: routing of (fingerprint, rank) tuples to their hash owners, on the device ----------------
-// owner of a fingerprint: same integer mix as sharded.py owner_of
-__host__ __device__ __forceinline__ int fp_owner(u64 hi, u64 lo, int world) {
-    const u64 x = (hi ^ lo) * K_STEP;
-    return (int)(((x >> 33) & 0x7FFFFFFFull) % (u64)world);
-}
 #define LTL_MAX_WORLD 64
 
 // pass 1 of a stable counting sort by owner: hist[d * nb + block] = tuples of this 1024-tuple block owned by rank d
@@ -958,6 +963,7 @@ struct ltl_core : Arena {
     cudaEvent_t part_ev[8] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     int exchange_parts = 4;       // row shards: parts of a pass whose exchange overlaps the evaluation of the next part
     u64 exchange_calls = 0;
+    int table_shard = 0, table_shards = 1;  // row shards: this core files only the keys it owns (fp_owner), see set_table_shard
     bool order_mat = true;        // phase B walks big right-operand buckets block by block (k_mat_plan)
     i64 order_min = 1 << 16;      // ... for passes that admit at least this many entries
     i64 order_block_bytes = 16 << 20;
@@ -1037,6 +1043,8 @@ static void drain_events(ltl_core* h) {  // stream must be idle
 }
 
 static int ensure_table(ltl_core* h, u64 need_keys) {
+    if (h->exchange && h->table_shards > 1)  // a shard of the table: the keys this core owns (+ 25 % for an uneven split)
+        need_keys = need_keys / (u64)h->table_shards + need_keys / (4 * (u64)h->table_shards) + 1024;
     u64 want = 1u << 16;
     while (want < need_keys * 2) want <<= 1;
     if (want <= h->table_cap) return LTL_OK;
@@ -1085,7 +1093,8 @@ static int ensure_scratch(ltl_core* h, i64 total) {
     h->scratch_cap = 0;
     CK(cudaMalloc(&h->d_slot, (size_t)cap * 4));
     CK(cudaMalloc(&h->d_dest, (size_t)cap * 4));
-    CK(cudaMalloc(&h->d_flagw, (size_t)(cap / 32) * 4));
+    CK(cudaMalloc(&h->d_flagw, (size_t)(cap / 32) * 4 + 64));  // (+ zeroed slack: the flags are exchanged in units of 3 words)
+    CK(cudaMemsetAsync((char*)h->d_flagw + (size_t)(cap / 32) * 4, 0, 64, h->stream));
     CK(cudaMalloc(&h->d_blocksum, (size_t)(cap / RES_CTA) * 4));
     CK(cudaMalloc(&h->d_blockoff, (size_t)(cap / RES_CTA) * 8));
     h->scratch_cap = cap;
@@ -1439,7 +1448,8 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
         CK(cudaMemsetAsync(h->d_ctl, 0xFF, 2 * sizeof(u64), h->stream));
         CK(cudaMemsetAsync((char*)h->d_ctl + 2 * sizeof(u64), 0, sizeof(Ctl) - 2 * sizeof(u64), h->stream));
     }
-    const bool small = mode == MODE_INSERT && h->small_admit && total <= LTL_SMALL_ADMIT;
+    // (row shards with a sharded table exchange the winner flags between resolve and scan: the four-kernel path)
+    const bool small = mode == MODE_INSERT && h->small_admit && total <= LTL_SMALL_ADMIT && !(h->exchange && h->table_shards > 1);
 
     ScreenParams p;
     memset(&p, 0, sizeof(p));
@@ -1470,6 +1480,8 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     p.ctl = h->d_ctl;
     p.blk_base = h->blk_base;
     p.defer = h->exchange ? 1 : 0;
+    p.owner_world = h->exchange ? h->table_shards : 1;
+    p.owner_rank = h->table_shard;
     const bool acc_path = p.nsplit > 1 || p.defer;
     if (acc_path) {
         if ((rc = ensure_acc(h, total))) return rc;
@@ -1594,6 +1606,14 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
         else k_finalize<false><<<(unsigned)((total + 255) / 256), 256, 0, h->stream>>>(p, (u64)total);
         CK(cudaGetLastError());
     }
+    if (mode == MODE_LOOKUP && p.owner_world > 1) {  // only the key's owner knows: OR over the shards
+        k_found_to_acc<<<1, 1, 0, h->stream>>>(h->d_ctl, h->d_acc);
+        CK(cudaGetLastError());
+        CK(cudaStreamSynchronize(h->stream));
+        if (h->exchange(h->exchange_ctx, h->d_acc, 1)) return h->fail(LTL_ERR_CUDA, "row-shard exchange failed");
+        k_acc_to_found<<<1, 1, 0, h->stream>>>(h->d_ctl, h->d_acc);
+        CK(cudaGetLastError());
+    }
     if (mode != MODE_INSERT) {
         CK(cudaMemcpyAsync(h->h_ctl, h->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
         CK(cudaStreamSynchronize(h->stream));
@@ -1630,6 +1650,22 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
             ScopedTimer t(h, LTL_K_RESOLVE, (u64)total, (double)total * 36.0);
             k_resolve<<<nb, RES_CTA, 0, h->stream>>>(h->d_slot, h->table, h->offered, (u64)total, h->d_ctl, h->d_flagw,
                                                       h->d_blocksum);
+        }
+        if (p.owner_world > 1) {
+            // every shard decided the keys it owns: the winner flags (one bit per candidate, set by one shard at most)
+            // are OR-ed over the shards -- as a wrapping sum of disjoint bits, 3 words per exchange unit
+            const i64 words = (i64)nb * (RES_CTA / 64);
+            {
+                HostTimer ht(&h->sync_ms);
+                CK(cudaStreamSynchronize(h->stream));
+            }
+            {
+                HostTimer ht(&h->exchange_ms);
+                if (h->exchange(h->exchange_ctx, h->d_flagw, (words + 2) / 3)) return h->fail(LTL_ERR_CUDA, "row-shard exchange failed");
+                h->exchange_calls++;
+            }
+            ScopedTimer t(h, LTL_K_RESOLVE, (u64)total, (double)total * 0.125);
+            k_flag_count<<<nb, RES_CTA, 0, h->stream>>>(h->d_flagw, (u64)nb * RES_CTA, h->d_blocksum);
         }
         {
             ScopedTimer t(h, LTL_K_SCAN, nb, (double)nb * 12.0);
@@ -2840,6 +2876,16 @@ int ltl_core_set_row_shard(ltl_core* h, int64_t word_base, int64_t total_words, 
     // the budget counts whole matrices, like the reference's (reference _speedups.pyx:100, 252-253)
     h->entry_bytes = (u64)total_words * 8 + 16;
     h->cap_entries = std::min<u64>(h->cap_entries, h->budget / h->entry_bytes);
+    return LTL_OK;
+}
+
+int ltl_core_set_table_shard(ltl_core* h, int shard, int n_shards) {
+    ENTER(h);
+    if (!h->exchange) return h->fail(LTL_ERR_ARG, "set_table_shard: call ltl_core_set_row_shard first");
+    if (h->n_entries || h->offered) return h->fail(LTL_ERR_ARG, "set_table_shard: the core is already in use");
+    if (n_shards < 1 || n_shards > LTL_MAX_WORLD || shard < 0 || shard >= n_shards) return h->fail(LTL_ERR_ARG, "set_table_shard: bad shard");
+    h->table_shard = shard;
+    h->table_shards = n_shards;
     return LTL_OK;
 }
 

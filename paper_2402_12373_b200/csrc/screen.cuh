@@ -113,6 +113,11 @@ __device__ __forceinline__ void finish_candidate(const ScreenParams& p, u64 c, u
         }
         return;
     }
+    if (p.owner_world > 1 && fp_owner(hi, lo, p.owner_world) != p.owner_rank) {  // another shard's key
+        if (p.mode == MODE_LOOKUP) p.ctl->found = 0ull;
+        else p.slot[c] = LTL_NONE;
+        return;
+    }
     if (p.mode == MODE_LOOKUP) {
         u64 s = table_find(p.table, p.table_mask, hi, lo);
         p.ctl->found = (s != ~0ull && ld_rank(p.table + s) != LTL_RANK_NONE) ? 1ull : 0ull;

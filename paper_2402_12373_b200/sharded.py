@@ -428,9 +428,11 @@ class RowShardedCore:
         self.local.close()
 
 
-def row_sharded_core_factory(comm, local_factory: Callable | None = None, **options):
+def row_sharded_core_factory(comm, local_factory: Callable | None = None, shard_table: bool = True, **options):
     """A `core_factory` for `learner.Enumeration` / `learn`: this rank's `CudaCore` over its slice of the rows
-    (``local_factory``: a CPU stand-in with the same `set_row_shard` contract, for the gloo tests)."""
+    (``local_factory``: a CPU stand-in with the same `set_row_shard` contract, for the gloo tests).
+    ``shard_table``: the uniqueness table is sharded by fingerprint owner too (`ltl_core_set_table_shard`), so that its
+    memory and the filing of keys scale with the GPUs; False keeps a replica of the whole table on every GPU."""
 
     def make(masks, n_pos, err_max, variant, proj_rows, proj_offs, fkp_bits, mask_k, budget_bytes, *,
              words_per_row=1, device=0):
@@ -453,6 +455,8 @@ def row_sharded_core_factory(comm, local_factory: Callable | None = None, **opti
         local = factory(m[r0 * W: r1 * W], max(0, min(int(n_pos), r1) - r0), err_max, variant, proj_rows, proj_offs,
                         fkp_bits, mask_k, budget_bytes, words_per_row=W, device=device, **options)
         local.set_row_shard(r0 * W, n_rows * W, comm.all_reduce_sum)
+        if shard_table and comm.world > 1 and hasattr(local, "set_table_shard"):
+            local.set_table_shard(comm.rank, comm.world)
         # A solver is only known after the exchange, so a pass cannot stop early inside a chunk: keep chunks at 2^22
         # candidates (the search stops after the first chunk that holds a solver; the level it ends in is the largest)
         if "chunk_candidates" not in options:

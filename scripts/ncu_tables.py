@@ -66,8 +66,12 @@ def traffic(path, config, hash_name, max_cost, merge_into=None, source=None):
     import os
 
     d = read_launches(path)
-    scr = [e for e in d.values() if e["name"].startswith("k_screen")]
-    mat = [e for e in d.values() if e["name"].startswith("k_materialize")]
+    def rewrite(name):  # k_screen<W, 2, PAIR> is the tile-shaped phase B (KIND_REWRITE), not screening
+        m = re.match(r"k_screen<\s*\d+,\s*(\d+)", name)
+        return bool(m) and m.group(1) == "2"
+
+    scr = [e for e in d.values() if e["name"].startswith("k_screen") and not rewrite(e["name"])]
+    mat = [e for e in d.values() if e["name"].startswith("k_materialize") or rewrite(e["name"])]
     small = [e for e in d.values() if e["name"].startswith("k_level")]
     scr_ms = sum(e["ms"] for e in scr)
     sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))

@@ -131,8 +131,11 @@ def test_row_sharded_matches_single_core_and_oracle(world, n_props, n_pos, n_neg
     want = _summary(L.learn(spec, None, alphabet, core_factory=oracle_factory(8), **kw))
     single = _summary(L.learn(spec, None, alphabet, **kw))
     assert single == want
-    for got in _run_sharded(world, spec, alphabet, kw, make_factory=row_sharded_core_factory):
-        assert got == want
+    # with the uniqueness table sharded by fingerprint owner (the default: winner flags OR-ed over the shards) and with a
+    # replica of the whole table on every shard
+    for shard_table in (True, False):
+        for got in _run_sharded(world, spec, alphabet, kw, make_factory=row_sharded_core_factory, shard_table=shard_table):
+            assert got == want, shard_table
 
 
 def test_row_sharded_matrices_and_membership():
