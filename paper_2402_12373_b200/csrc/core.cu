@@ -37,6 +37,7 @@ LTL_DECL_W(9) LTL_DECL_W(10) LTL_DECL_W(11) LTL_DECL_W(12) LTL_DECL_W(13) LTL_DE
 #undef LTL_DECL_W
 // half-width store (two 32-bit rows per word): screen_inst.cu compiled with -DLTL_W=1 -DLTL_PAIR
 extern "C" void ltl_launch_screen_w1p(const ScreenParams&, int, dim3, cudaStream_t);
+extern "C" void ltl_launch_screen_small(const ScreenParams&, int, unsigned long long, cudaStream_t);
 extern "C" void ltl_launch_materialize_w1p(const MaterializeParams&, const ScreenParams&, int, dim3, cudaStream_t);
 
 static const screen_launch_fn SCREEN_FN[LTL_MAX_W + 1] = {
@@ -206,6 +207,7 @@ __global__ void __launch_bounds__(RES_CTA) k_emit(const u32* __restrict__ flagw,
 // k_finalize + k_resolve + k_scan + k_emit do for big passes -- complete the row-split candidates, decide the winners
 // (lowest rank per key), compact them in rank order and write their records -- 1024 candidates per round with a running
 // offset.  It also zeroes the partial sums it consumed, so the next small pass needs no memset.
+#define LTL_SMALL_SCREEN 8192
 #define LTL_SMALL_ADMIT 8192  // (one CTA takes ~1.5 us per 1024 candidates: at 20 K candidates -- config 5, cost level 6 --
                               // it cost 32 us where the four full-width kernels need 18)
 template <bool MUELLER>
@@ -971,6 +973,7 @@ struct ltl_core : Arena {
     PlanFam* d_plan_fams = nullptr;
     int plan_cap = 0, plan_fams_cap = 0;
     bool plan_in_use = false;
+    bool small_screen = true;     // small passes over one-word rows: the compact phase-A kernel (k_screen_small)
     bool small_admit = true;      // passes of <= LTL_SMALL_ADMIT candidates: one bookkeeping kernel instead of four
     bool acc_dirty = true;        // the partial-sum arrays may hold something other than zeros
     u64 unstored_from = ~0ull;    // first entry index without a stored matrix
@@ -1466,6 +1469,14 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     p.n = h->n;
     p.total_tiles = tiles;
     choose_split(h, tiles, &p.nsplit, &p.rows_per_split);
+    // small passes over one-word rows go through the compact kernel: blocks of 64 rows per thread
+    const bool small_screen = h->small_screen && h->W == 1 && !h->pair && mode != MODE_REWRITE && total <= LTL_SMALL_SCREEN &&
+                              (i64)total * (i64)h->R <= ((i64)1 << 24) && h->force_split == 0 && !h->exchange &&
+                              h->R <= 65535 * LTL_SPLIT_ROWS;
+    if (small_screen) {
+        p.rows_per_split = LTL_SPLIT_ROWS;
+        p.nsplit = (h->R + LTL_SPLIT_ROWS - 1) / LTL_SPLIT_ROWS;
+    }
     p.variant = h->variant;
     p.mask_k = h->mask_k;
     p.n_dep = h->n_dep;
@@ -1501,7 +1512,13 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
         const Piece& fp = pieces[(size_t)fused_not];
         if ((rc = flush_materialize(h, &p, screen_kind, fp.cbase, fp.i0))) return rc;
     }
-    if (p.defer) {
+    if (small_screen) {
+        ScopedTimer t(h, LTL_K_SCREEN, (u64)total, screen_bytes(h, pieces));
+        issued_units = (u64)total;
+        issued_bytes = screen_bytes(h, pieces);
+        ltl_launch_screen_small(p, screen_kind, (unsigned long long)total, h->stream);
+        CK(cudaGetLastError());
+    } else if (p.defer) {
         // Row shards: every shard adds its partial sums, then all of them complete identical candidates.  The pass is cut
         // at piece boundaries into up to `exchange_parts` parts (contiguous ranges of tiles AND of ranks); all parts are
         // launched at once, and while part k + 1 is still being evaluated the sums of part k -- complete as soon as its
@@ -2802,6 +2819,8 @@ int ltl_core_set_option(ltl_core* h, const char* name, int64_t value) {
         h->order_min = value;
     } else if (!strcmp(name, "order_block_bytes")) {
         h->order_block_bytes = std::max<int64_t>(1, value);
+    } else if (!strcmp(name, "small_screen")) {
+        h->small_screen = value != 0;
     } else if (!strcmp(name, "small_admit")) {
         h->small_admit = value != 0;
     } else if (!strcmp(name, "fuse_not_min")) {

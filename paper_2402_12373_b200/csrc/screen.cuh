@@ -695,6 +695,110 @@ __global__ void __launch_bounds__(LTL_CTA, (W == 1 ? LTL_MIN_CTAS_W1 : 2)) k_scr
 }
 
 // ------------------------------------------------------------------------------------------------
+// phase A for small passes (one-word rows)
+//
+// k_screen is ~54 K instructions of specialised tiles; a pass of a few hundred candidates touches a long path through it
+// once, and ncu shows `no_instruction` (instruction-cache misses) as its top stall by far: 25 us per launch whatever the
+// work (config 1: every cost level; every config: its first five or six levels).  This kernel does the same arithmetic
+// with a few hundred instructions: one thread per (candidate, block of 64 rows), operands read straight from the entry
+// store (consecutive candidates share their left operand and read consecutive right operands), connective chosen by a
+// switch, partial sums combined with atomics like any row-split pass.  Bit-identical results: same connectives
+// (semantics.cuh), same fingerprint definitions as tile_eval, same finish_candidate.
+template <int KIND>
+__global__ void __launch_bounds__(256) k_screen_small(const __grid_constant__ ScreenParams p, const u64 total) {
+    constexpr bool NH = KIND == KIND_NH, MUELLER = KIND == KIND_MUELLER, HASHED = NH || MUELLER;
+    const u64 c = (u64)blockIdx.x * 256 + threadIdx.x;
+    if (c >= total) return;
+    int lo = 0, hi = p.n_pieces - 1;
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if ((u64)p.pieces[mid].cbase <= c) lo = mid;
+        else hi = mid - 1;
+    }
+    const Piece& pc = p.pieces[lo];
+    if (pc.ext) return;  // evaluated by phase B of the entries it ranges over (fused NOT)
+    i64 i, j;
+    piece_unrank(pc, c, &i, &j);
+    const int op = pc.op;
+    const i64 n = p.n;
+    const int r0 = (int)blockIdx.y * p.rows_per_split, r1 = min(p.R, r0 + p.rows_per_split);
+    const u64* __restrict__ px = p.cms + cm_index(i, n, 0);
+    const u64* __restrict__ py = j >= 0 ? p.cms + cm_index(j, n, 0) : px;
+    u64 s0 = 0, s1 = 0, h0 = NH ? 0ull : K_SEED0, h1 = NH ? 0ull : K_SEED1;
+    u32 err = 0;
+    int d = 0;
+    if (KIND == KIND_BITS) {
+        int a = 0, b = p.n_dep;
+        while (a < b) {
+            const int mid = (a + b) >> 1;
+            if (p.deps[mid].k < (u32)r0) a = mid + 1;
+            else b = mid;
+        }
+        d = a;
+    }
+    for (int r = r0; r < r1; r++) {
+        const u64 x = ld_nc(px + (size_t)r * 32), y = ld_nc(py + (size_t)r * 32), m = ld_nc(p.masks + r);
+        u64 xs[1] = {x}, ys[1] = {y}, ms[1] = {m}, out[1];
+        switch (op) {
+            case OP_NOT: apply_row<OP_NOT, 1>(out, xs, ys, ms); break;
+            case OP_AND: apply_row<OP_AND, 1>(out, xs, ys, ms); break;
+            case OP_OR: apply_row<OP_OR, 1>(out, xs, ys, ms); break;
+            case OP_NEXT: apply_row<OP_NEXT, 1>(out, xs, ys, ms); break;
+            case OP_FINALLY: apply_row<OP_FINALLY, 1>(out, xs, ys, ms); break;
+            case OP_GLOBALLY: apply_row<OP_GLOBALLY, 1>(out, xs, ys, ms); break;
+            case OP_UNTIL: apply_row<OP_UNTIL, 1>(out, xs, ys, ms); break;
+            default: out[0] = x; break;
+        }
+        const u64 v = out[0];
+        const u32 bit = (u32)(v >> 63);
+        err += r < p.n_pos ? 1u - bit : bit;  // reference _speedups.pyx:327-333
+        if (NH) {  // oracle fp_nh
+            const u32 pk = (u32)r & 63u;
+            const u64 key0 = c_nh.k[pk], key1 = c_nh.k[pk + 1];
+            const u32 xl = (u32)v, xh = (u32)(v >> 32);
+            h0 = mad_wide(xl + (u32)key0, xh + (u32)(key0 >> 32), h0);
+            h1 = mad_wide(xl + (u32)key1, xh + (u32)(key1 >> 32), h1);
+        } else if (MUELLER) {  // reference _speedups.pyx:196-202, blocked
+            const u64 mm = mix64(v ^ (((u64)p.blk_base * 64ull + (u64)r + 1ull) * K_STEP));
+            h0 = (h0 ^ mm) * K_FOLD0;
+            h1 = (h1 ^ ((mm << 32) | (mm >> 32))) * K_FOLD1;
+        } else {  // gather / fkp deposits (reference _speedups.pyx:188-195, 205-222)
+            while (d < p.n_dep && p.deps[d].k <= (u32)r) {
+                const Deposit dp = p.deps[d];
+                const u64 w = (v >> dp.rsh) & dp.mask;
+                if (dp.pos >= 64) s0 += w << (dp.pos - 64);
+                else {
+                    s1 += w << dp.pos;
+                    if (dp.pos > 0) s0 += w >> (64 - dp.pos);
+                }
+                d++;
+            }
+        }
+        if (HASHED && ((((u32)r + 1u) & 63u) == 0 || r + 1 == p.R)) {  // the hash block ends with this word
+            const u32 blk = ((u32)r >> 6) + p.blk_base;
+            if (NH) {
+                const u64 u = (u64)(blk + 1) * K_STEP;
+                s0 += mix64(h0 ^ u);
+                s1 += mix64(h1 + u);
+                h0 = h1 = 0;
+            } else {
+                s0 += blk == 0 ? h0 : mix64(h0);
+                s1 += blk == 0 ? h1 : mix64(h1);
+                h0 = K_SEED0;
+                h1 = K_SEED1;
+            }
+        }
+    }
+    if (p.nsplit > 1 || p.defer) {
+        atomicAdd(p.acc + 3 * c, s0);
+        atomicAdd(p.acc + 3 * c + 1, s1);
+        if (err) atomicAdd(p.acc + 3 * c + 2, (u64)err);
+    } else {
+        finish_candidate<HASHED>(p, c, s0, s1, err);
+    }
+}
+
+// ------------------------------------------------------------------------------------------------
 // phase B kernel
 
 template <int W, int OP, bool PAIR>

@@ -45,6 +45,16 @@ extern "C" void LTL_CAT(ltl_launch_screen_w, LTL_W)(const ScreenParams& p, int k
     else k_screen<LTL_W, KIND_REWRITE><<<grid, LTL_CTA, Ring<LTL_W>::CTA_BYTES, stream>>>(p);
 }
 
+#if LTL_W == 1
+// small passes over one-word rows: the compact kernel (screen.cuh: k_screen_small)
+extern "C" void ltl_launch_screen_small(const ScreenParams& p, int kind, unsigned long long total, cudaStream_t stream) {
+    dim3 grid((unsigned)((total + 255) / 256), (unsigned)p.nsplit);
+    if (kind == KIND_MUELLER) k_screen_small<KIND_MUELLER><<<grid, 256, 0, stream>>>(p, total);
+    else if (kind == KIND_NH) k_screen_small<KIND_NH><<<grid, 256, 0, stream>>>(p, total);
+    else k_screen_small<KIND_BITS><<<grid, 256, 0, stream>>>(p, total);
+}
+#endif
+
 // fuse_kind != 0 (one-word rows only; the host never asks otherwise): phase B that also screens NOT(new entry)
 extern "C" void LTL_CAT(ltl_launch_materialize_w, LTL_W)(const MaterializeParams& p, const ScreenParams& sp, int fuse_kind,
                                                           dim3 grid, cudaStream_t stream) {

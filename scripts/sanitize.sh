@@ -27,7 +27,9 @@ elif case == "rowsplit":
     r = learn(spec, None, alphabet, max_cost=5)
     print("halfwidth", r.status, r.stats.offered, r.stats.admitted)
 elif case == "traces":
+    from paper_2402_12373_b200 import learner
     from paper_2402_12373_b200.learner import learn
+    learner.DEVICE_SPEC_MIN_CHARS = 0
     rng = np.random.default_rng(3)
     R, L = 5000, 40
     lengths = rng.integers(20, L + 1, size=R).astype(np.int64)  # long enough for 5000 random traces to be distinct

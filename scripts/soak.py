@@ -126,6 +126,7 @@ while time.time() < t_end:
     P_arr = (spec.chars[: spec.n_pos].copy(), spec.lengths[: spec.n_pos].copy())
     N_arr = (spec.chars[spec.n_pos:].copy(), spec.lengths[spec.n_pos:].copy())
     os.environ["LTLLEARN_DEBUG_MASKS"] = "1"
+    L.DEVICE_SPEC_MIN_CHARS = 0  # the device-resident path whatever the size
     try:
         runs["arrays_debug"] = [summary(L.learn(P_arr, N_arr, al, **kw))]
     finally:

@@ -17,6 +17,16 @@ pytestmark = pytest.mark.gpu
 UNARY = (1, 4, 5, 6)
 
 
+@pytest.fixture(params=["compact", "tiles"])
+def screen_path(request, monkeypatch):
+    """Small passes over one-word rows run through the compact phase-A kernel (`k_screen_small`) by default; "tiles" forces
+    them through the tile kernel (`k_screen`), which big passes always use -- every variant of it stays covered by the small
+    differential cases."""
+    if request.param == "tiles":
+        monkeypatch.setenv("LTL_CORE_OPTIONS", "small_screen=0")
+    return request.param
+
+
 def assert_same_state(cuda, ora):
     assert cuda.counters() == ora._counters()
     n = ora.n_entries
@@ -65,7 +75,7 @@ def drive(cuda, ora, rng, n_seed=5, rounds=2):
 @pytest.mark.parametrize("R,W", [(2, 1), (16, 1), (64, 1), (65, 1), (200, 1), (1024, 1), (7, 2), (33, 3), (20, 4),
                                  (9, 5), (12, 7), (40, 8), (5, 11), (24, 16), (130, 16)])
 @pytest.mark.parametrize("variant", [V_MUELLER, V_NH], ids=["mueller", "nh"])
-def test_differential_random(R, W, variant):
+def test_differential_random(R, W, variant, screen_path):
     rng = np.random.default_rng(1000 * R + W)
     masks = random_masks(rng, R, W)
     n_pos = int(rng.integers(1, R)) if R > 1 else 1
@@ -86,7 +96,7 @@ def test_differential_random(R, W, variant):
 @pytest.mark.parametrize("R,W,split,chunk", [(200, 1, 3, 97), (1024, 1, 16, 1000), (130, 16, 2, 333), (64, 3, 1, 50),
                                              (300, 2, 4, 1 << 20)])
 @pytest.mark.parametrize("variant", [V_MUELLER, V_NH], ids=["mueller", "nh"])
-def test_differential_split_and_chunked(R, W, split, chunk, variant):
+def test_differential_split_and_chunked(R, W, split, chunk, variant, screen_path):
     """Row-split evaluation (partial fingerprints combined by atomics) and tiny chunks (rows cut mid-way)."""
     rng = np.random.default_rng(77 * R + W)
     masks = random_masks(rng, R, W)
@@ -99,7 +109,7 @@ def test_differential_split_and_chunked(R, W, split, chunk, variant):
 
 
 @pytest.mark.parametrize("seed", range(6))
-def test_solver_and_counters(seed):
+def test_solver_and_counters(seed, screen_path):
     """First solver in enumeration order wins; counters stop at the solver (reference _speedups.pyx:372-374)."""
     rng = np.random.default_rng(500 + seed)
     R, W = (24, 1) if seed % 2 == 0 else (12, 2)
@@ -129,7 +139,7 @@ def test_solver_and_counters(seed):
     cuda.close()
 
 
-def test_budget_oom_matches_oracle():
+def test_budget_oom_matches_oracle(screen_path):
     rng = np.random.default_rng(9)
     R = 32
     masks = random_masks(rng, R, 1)
@@ -196,13 +206,16 @@ def test_transcripts_golden():
         cuda.close()
 
 
-@pytest.mark.parametrize("native_loop", [True, False], ids=["run_search", "run_level"])
+@pytest.mark.parametrize("native_loop,options", [(True, ""), (False, ""), (True, "small_screen=0,small_admit=0")],
+                         ids=["run_search", "run_level", "big_kernels"])
 @pytest.mark.parametrize("case", golden()["learn"], ids=lambda c: c["name"])
-def test_learn_golden_cases(case, native_loop, monkeypatch):
+def test_learn_golden_cases(case, native_loop, options, monkeypatch):
     """The product path end to end (learner -> C ABI -> CUDA) against the reference's recorded outcomes, with the
     cost-level loop inside the library (`ltl_core_run_search`, the default) and with one `run_level` call per level
     from `learner.py`."""
     monkeypatch.setattr(L.Enumeration, "native_loop", native_loop)
+    if options:  # small passes through the kernels big passes use (tile phase A, four bookkeeping kernels)
+        monkeypatch.setenv("LTL_CORE_OPTIONS", options)
     spec, alphabet = spec_from_golden(case)
     cfg = cfg_from_golden(case["cfg"])
     cores = []
@@ -337,7 +350,7 @@ def test_last_level_matrices_can_be_skipped():
     cuda.close()
 
 
-def test_fused_unary_levels_match_unfused():
+def test_fused_unary_levels_match_unfused(screen_path):
     """run_level fuses the unary connectives of a level into one pass per operand group; same results as
     screening them one at a time."""
     from paper_2402_12373_b200.learner import Segment

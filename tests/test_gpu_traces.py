@@ -135,7 +135,7 @@ LEARN_CASES = [
 
 
 @pytest.mark.parametrize("case", LEARN_CASES, ids=[str(c["seed"]) for c in LEARN_CASES])
-def test_learn_from_arrays_matches_host_path_and_oracle(case):
+def test_learn_from_arrays_matches_host_path_and_oracle(case, monkeypatch):
     """`learn((chars, lengths), (chars, lengths), ...)`: the specification is uploaded, checked, packed and searched on
     the device -- same outcome, counters and per-level rows as the host-packed search and as the CPU oracle."""
     from paper_2402_12373_b200 import workloads as Wl
@@ -149,6 +149,7 @@ def test_learn_from_arrays_matches_host_path_and_oracle(case):
         P, N = _random_arrays(np.random.default_rng(case["seed"]), case["n_props"], case["n_pos"], case["n_neg"],
                               case["lo"], case["hi"])
         alphabet = Alphabet.default(case["n_props"])
+    monkeypatch.setattr(L, "DEVICE_SPEC_MIN_CHARS", 0)  # these small inputs must take the device-resident path
     host_spec = Specification.from_arrays(P[0], P[1], N[0], N[1])
     want = _summary(L.learn(host_spec, None, alphabet, core_factory=oracle_factory(2), **case["kw"]))
     host = L.learn(host_spec, None, alphabet, **case["kw"])
