@@ -1499,10 +1499,12 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
         p.acc = h->d_acc;
         // (the small-pass bookkeeping kernel leaves the sums it consumed zeroed: nothing to clear between small passes)
         const size_t clear = (size_t)(small ? std::max<i64>(total, std::min<i64>(h->acc_cap, LTL_SMALL_ADMIT)) : total);
-        if (!small || h->acc_dirty) {
+        // (a row shard without row split stores every candidate's sums exactly once: nothing to clear)
+        const bool stored = p.defer && p.nsplit == 1;
+        if (!stored && (!small || h->acc_dirty)) {
             CK(cudaMemsetAsync(h->d_acc, 0, clear * 24, h->stream));
         }
-        h->acc_dirty = !small;
+        h->acc_dirty = stored ? true : !small;
     }
     u64 issued_units = 0;       // what the phase-A launches of this pass were booked with (statistics)
     double issued_bytes = 0;

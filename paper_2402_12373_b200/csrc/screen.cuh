@@ -521,10 +521,14 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
     for (int t = 0; t < TI; t++) {
         u64 c;
         if (!slot_rank(t, &c)) continue;
-        if (p.nsplit > 1 || p.defer) {
+        if (p.nsplit > 1) {
             atomicAdd(p.acc + 3 * c, s0[t]);
             atomicAdd(p.acc + 3 * c + 1, s1[t]);
             if (err[t]) atomicAdd(p.acc + 3 * c + 2, (u64)err[t]);
+        } else if (p.defer) {  // row shard, no row split: this warp is the only writer of the candidate's sums
+            p.acc[3 * c] = s0[t];
+            p.acc[3 * c + 1] = s1[t];
+            p.acc[3 * c + 2] = (u64)err[t];
         } else {
             finish_candidate<HASHED>(p, c, s0[t], s1[t], err[t]);
         }
@@ -542,8 +546,12 @@ __device__ __forceinline__ void tile_eval(const ScreenParams& p, const Piece& pc
 #ifndef LTL_MIN_CTAS_W1
 #define LTL_MIN_CTAS_W1 3
 #endif
+#ifndef LTL_MIN_CTAS_REWRITE
+#define LTL_MIN_CTAS_REWRITE 3  // (4 CTAs -- 64 registers, 4 x 55.5 KB of rings per SM -- measured: 10.3 -> 10.9 ms on config 4)
+#endif
 template <int W, int KIND, bool PAIR = false>
-__global__ void __launch_bounds__(LTL_CTA, (W == 1 ? LTL_MIN_CTAS_W1 : 2)) k_screen(const __grid_constant__ ScreenParams p) {
+__global__ void __launch_bounds__(LTL_CTA, (W == 1 ? (KIND == KIND_REWRITE ? LTL_MIN_CTAS_REWRITE : LTL_MIN_CTAS_W1) : 2))
+    k_screen(const __grid_constant__ ScreenParams p) {
     static_assert(!PAIR || (W == 1 && (KIND == KIND_NH || KIND == KIND_REWRITE)), "half-width rows: one word, NH fingerprint");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int lane = threadIdx.x & 31;
@@ -998,10 +1006,14 @@ __global__ void __launch_bounds__(LTL_CTA, LTL_MATF_MINB) k_materialize_not(cons
     }
     if (valid) {  // file NOT(dst) as candidate not_cbase + (dst - not_i0) of the pass in flight
         const u64 c = (u64)p.not_cbase + (u64)(dst - p.not_i0);
-        if (sp.nsplit > 1 || sp.defer) {  // the pass combines row splits (or GPUs): hand the sums to k_finalize
+        if (sp.nsplit > 1) {  // the pass combines row splits: hand the sums to k_finalize
             atomicAdd(sp.acc + 3 * c, f.s0);
             atomicAdd(sp.acc + 3 * c + 1, f.s1);
             if (f.err) atomicAdd(sp.acc + 3 * c + 2, (u64)f.err);
+        } else if (sp.defer) {  // row shard: this lane folded all local rows of the entry
+            sp.acc[3 * c] = f.s0;
+            sp.acc[3 * c + 1] = f.s1;
+            sp.acc[3 * c + 2] = (u64)f.err;
         } else {
             finish_candidate<true>(sp, c, f.s0, f.s1, f.err);
         }
