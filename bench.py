@@ -407,8 +407,15 @@ def measure_config(config: str, args, *, steps: int, warmup: int, cpu_cost: int 
     roofline = build_roofline(kstats, steps, clocks, config, args.hash, max_cost, sm_count)
 
     # ---- end to end through the public API, host buffers in, formula out
-    pos_c, pos_l = spec.chars[: spec.n_pos].copy(), spec.lengths[: spec.n_pos].copy()
-    neg_c, neg_l = spec.chars[spec.n_pos:].copy(), spec.lengths[spec.n_pos:].copy()
+    # the step's inputs live in PINNED host memory (numpy views of pinned torch tensors): the library's cudaMemcpyAsync then
+    # runs at PCIe speed instead of staging pageable memory (config 4: 134 MB per step)
+    def pinned(a):
+        a = np.ascontiguousarray(a)
+        t = torch.from_numpy(a.view(np.uint8).reshape(-1)).pin_memory()  # (bytes: every torch build pins uint8)
+        return t.numpy().view(a.dtype).reshape(a.shape)
+
+    pos_c, pos_l = pinned(spec.chars[: spec.n_pos]), pinned(spec.lengths[: spec.n_pos])
+    neg_c, neg_l = pinned(spec.chars[spec.n_pos:]), pinned(spec.lengths[spec.n_pos:])
     e2e_parts = {"spec_ms": 0.0, "learn_ms": 0.0}
 
     def e2e_once():

@@ -1420,6 +1420,7 @@ static int plan_materialize(ltl_core* h, const std::vector<Piece>& pieces, i64 t
                                                                             h->d_flagw, h->d_blockoff, h->d_ctl, (u64)total,
                                                                             (i64)n_base, count, h->d_plan_g0, h->d_plan_cnt);
         k_plan_scan<<<1, 1024, 0, h->stream>>>(h->d_plan_cnt, n_seg, h->d_plan_off);
+        h->stats[LTL_K_MISC].launches += 1;  // (two kernels under one timer)
     }
     CK(cudaGetLastError());
     h->plan_in_use = true;
@@ -2961,6 +2962,7 @@ int ltl_core_stage_file(ltl_core* h, const uint64_t* d_tuples, int64_t count, un
         ScopedTimer t(h, LTL_K_RESOLVE, (u64)count, (double)count * 56.0);
         k_file_insert<<<nb, 256, 0, h->stream>>>((const u64*)d_tuples, (u64)count, h->table, h->table_cap - 1, h->offered, h->d_slot);
         k_file_verdict<<<nb, 256, 0, h->stream>>>((const u64*)d_tuples, h->d_slot, (u64)count, h->table, d_win, h->d_ctl);
+        h->stats[LTL_K_RESOLVE].launches += 1;  // (two kernels under one timer)
     }
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h->h_ctl, h->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));
@@ -2997,6 +2999,7 @@ int ltl_core_stage_route(ltl_core* h, const uint64_t* d_fp, int64_t count, uint6
         k_route_count<<<nb, 1024, 0, h->stream>>>((const u64*)d_fp, (u64)count, world, h->d_route_hist, nb);
         k_plan_scan<<<1, 1024, 0, h->stream>>>(h->d_route_hist, (int)cells, h->d_route_off);
         k_route_scatter<<<nb, 1024, 0, h->stream>>>((const u64*)d_fp, (u64)count, world, rank_base, h->d_route_off, nb, (u64*)d_send);
+        h->stats[LTL_K_MISC].launches += 2;  // (three kernels under one timer)
     }
     CK(cudaGetLastError());
     u32 bounds[LTL_MAX_WORLD + 1];
@@ -3025,6 +3028,7 @@ int ltl_core_stage_winners(ltl_core* h, const uint64_t* d_tuples, const unsigned
         k_flag_count<<<nb, RES_CTA, 0, h->stream>>>(h->d_flagw, (u64)count, h->d_blocksum);
         k_scan<<<1, 1024, 0, h->stream>>>(h->d_blocksum, nb, h->d_blockoff, h->d_ctl);
         k_emit_ranks<<<nb, RES_CTA, 0, h->stream>>>(h->d_flagw, h->d_blockoff, (u64)count, (i64)level_lo, (i64*)d_out);
+        h->stats[LTL_K_MISC].launches += 3;  // (four kernels under one timer)
     }
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(h->h_ctl, h->d_ctl, sizeof(Ctl), cudaMemcpyDeviceToHost, h->stream));

@@ -326,7 +326,8 @@ class Enumeration:
             return
         t_scheme = time.perf_counter()
         words = info["words"]
-        rs = resolve_scheme(cfg.hash, spec.lengths, SuffixTable.from_spec(spec, limit=126), words_per_row=words)
+        rs = resolve_scheme(cfg.hash, None, SuffixTable.from_spec(spec, limit=126), words_per_row=words, n_rows=spec.size,
+                            max_len=info["max_len"])
         stats.precise = rs.precise
         t_create = time.perf_counter()
         stats.phase_ms["scheme"] = 1e3 * (t_create - t_scheme)

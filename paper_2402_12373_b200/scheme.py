@@ -58,10 +58,17 @@ def fkp_bits_per_row(n_rows: int) -> int:
     return min(lo, 64)
 
 
-def resolve_scheme(scheme: HashScheme, lengths, suffix_table=None, words_per_row: int = 1) -> ResolvedScheme:
+def resolve_scheme(scheme: HashScheme, lengths, suffix_table=None, words_per_row: int = 1, *, n_rows: int | None = None,
+                   max_len: int | None = None) -> ResolvedScheme:
+    """``n_rows`` / ``max_len`` (with a suffix table): the two facts about the lengths the rule needs, for callers that
+    hold them already (a device-resident specification) -- ``lengths`` is then not touched."""
     import numpy as np
 
-    lengths = np.asarray(lengths, dtype=np.int64).reshape(-1)  # 2^21 traces: no per-element Python work below
+    if suffix_table is not None and n_rows is not None and max_len is not None:
+        lengths = None
+    else:
+        lengths = np.asarray(lengths, dtype=np.int64).reshape(-1)  # 2^21 traces: no per-element Python work below
+        n_rows, max_len = len(lengths), (int(lengths.max()) if len(lengths) else 0)
     if suffix_table is not None:
         if suffix_table.count <= FP_BITS:
             return ResolvedScheme(V_GATHER, tuple(suffix_table.rows), tuple(suffix_table.offsets), mask_k=scheme.mask_bits)
@@ -70,9 +77,9 @@ def resolve_scheme(scheme: HashScheme, lengths, suffix_table=None, words_per_row
         offs = tuple(j for n in lengths for j in range(int(n)))
         return ResolvedScheme(V_GATHER, rows, offs, mask_k=scheme.mask_bits)
     if scheme.variant in ("mueller", "mueller_blocked", "nh"):
-        big = len(lengths) * int(words_per_row) > REFERENCE_WORDS
+        big = n_rows * int(words_per_row) > REFERENCE_WORDS
         nh = scheme.variant == "nh" or (scheme.variant == "mueller" and big)
-        if nh and int(words_per_row) == 1 and (int(lengths.max()) if len(lengths) else 0) <= HALF_WORD:
+        if nh and int(words_per_row) == 1 and max_len <= HALF_WORD:
             return ResolvedScheme(V_NH32, mask_k=scheme.mask_bits)
         return ResolvedScheme(V_NH if nh else V_MUELLER, mask_k=scheme.mask_bits)
-    return ResolvedScheme(V_FKP, fkp_bits=fkp_bits_per_row(len(lengths)), mask_k=scheme.mask_bits)
+    return ResolvedScheme(V_FKP, fkp_bits=fkp_bits_per_row(n_rows), mask_k=scheme.mask_bits)
