@@ -91,7 +91,8 @@ typedef struct ltl_segment {
 #define LTL_K_REHASH 6
 #define LTL_K_PURGE 7
 #define LTL_K_MISC 8        /* import / export / record fix-ups */
-#define LTL_K_COUNT 9
+#define LTL_K_LEVELS 9      /* the first (small) cost levels of a search in one launch: plan + screen + admit + append */
+#define LTL_K_COUNT 10
 
 LTL_API int ltl_abi_version(void);
 

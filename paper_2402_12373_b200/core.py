@@ -26,7 +26,7 @@ V_GATHER, V_MUELLER, V_FKP, V_NH, V_NH32 = 0, 1, 2, 3, 4
 MAX_WORDS_PER_ROW = 16
 
 ERR_ARG, ERR_CUDA, ERR_BUDGET, ERR_DEVICE_OOM, ERR_INVARIANT = -1, -2, -3, -4, -5
-KERNEL_CLASSES = ("screen", "finalize", "resolve", "scan", "emit", "materialize", "rehash", "purge", "misc")
+KERNEL_CLASSES = ("screen", "finalize", "resolve", "scan", "emit", "materialize", "rehash", "purge", "misc", "levels")
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("LTL_CORE_LIB") or os.path.join(_HERE, "csrc", "libltlcore.so")  # override: A/B builds

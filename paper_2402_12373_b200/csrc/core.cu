@@ -22,6 +22,7 @@
 
 #include "../../include/ltl_core.h"
 #include "screen.cuh"
+#include "levels.cuh"
 #include "traces.cuh"
 
 // ------------------------------------------------------------------------------------------------
@@ -845,6 +846,8 @@ struct Arena {
     i64 stage_cap = 0;
     cudaEvent_t sub_ev[2] = {nullptr, nullptr};
     u64* h_solver = nullptr;  // pinned: solver rank as of the end of each of the last two phase-A launches
+    LevelsState* d_lv = nullptr;  // device-resident cost levels (levels.cuh): search state on the device ...
+    LevelsState* h_lv = nullptr;  // ... and its pinned host copy
     std::vector<cudaEvent_t> event_pool;
 
     void destroy_all() {
@@ -855,6 +858,8 @@ struct Arena {
         if (sub_ev[0]) cudaEventDestroy(sub_ev[0]);
         if (sub_ev[1]) cudaEventDestroy(sub_ev[1]);
         cudaFreeHost(h_solver);
+        cudaFree(d_lv);
+        cudaFreeHost(h_lv);
         cms.release();
         rec_op.release();
         rec_lhs.release();
@@ -975,6 +980,10 @@ struct ltl_core : Arena {
     bool plan_in_use = false;
     bool small_screen = true;     // small passes over one-word rows: the compact phase-A kernel (k_screen_small)
     bool small_admit = true;      // passes of <= LTL_SMALL_ADMIT candidates: one bookkeeping kernel instead of four
+    bool device_levels = true;    // run_search: the first (small) cost levels in one launch, planned on the device (levels.cuh)
+    int levels_ctas = LTL_LV_MAX_CLUSTER;  // CTAs of that launch's cluster
+    i64 levels_max_work = (i64)1 << 18;    // candidate-rows per level up to which a level stays in that launch (8 SMs: beyond,
+                                           // the host-driven path with the whole GPU behind it is faster -- measured)
     bool acc_dirty = true;        // the partial-sum arrays may hold something other than zeros
     u64 unstored_from = ~0ull;    // first entry index without a stored matrix
     bool profile = false;
@@ -2513,6 +2522,209 @@ int ltl_core_run_level(ltl_core* h, const ltl_segment* segs, int n_segs, int* st
     return run_units(h, units, true, status, seg_index, li, ri);
 }
 
+// The first cost levels of a search in ONE launch (levels.cuh), while they are small: fills the stats rows of the levels it
+// completed, moves the bucket table and the core's counters on, and returns in *next_cost the level the host-driven loop
+// continues with (with *status == LTL_S_SOLVED: the level that solved).  Declines (next_cost = first_cost, nothing
+// changed) whenever the core is not in the plain state the kernel assumes.
+static int run_levels_device(ltl_core* h, const int32_t op_cost[8], uint32_t op_mask, std::vector<std::pair<i64, i64>>& bucket,
+                             std::vector<char>& known, int first_cost, int ceiling, int store_last_level, ltl_level_stats* rows,
+                             int* n_rows, int* status, int* op, int64_t* li, int64_t* ri, int* next_cost) {
+    *next_cost = first_cost;
+    if (!h->device_levels || !h->small_screen || !h->small_admit || h->W != 1 || h->pair || h->exchange || h->force_split ||
+        h->debug_masks || !h->store_results || h->unstored_from != ~0ull || h->levels_max_work <= 0 || h->blk_base != 0 ||
+        h->chunk_cap < LTL_LV_MAX_TOTAL)
+        return LTL_OK;
+    const int stop_cost = std::min(ceiling, LTL_LV_MAX_COST);
+    if (first_cost >= stop_cost || first_cost < 1) return LTL_OK;
+    int rc;
+    LevelsParams P;
+    memset(&P, 0, sizeof(P));
+    P.sp.R = h->R;
+    P.sp.n = h->n;
+    P.first_cost = first_cost;
+    P.stop_cost = stop_cost;
+    P.nostore_cost = store_last_level ? -1 : ceiling - 1;  // the last level of a search is not stored unless asked for
+    for (int k = 0; k < 8; k++) P.op_cost[k] = op_cost[k];
+    P.op_mask = op_mask;
+    P.max_total = LTL_LV_MAX_TOTAL;
+    P.max_work = h->levels_max_work;
+    const u64 room = h->cap_entries > h->n_entries ? h->cap_entries - h->n_entries : 0;
+    // store mapped ahead of the launch: what the levels it may run can admit, bounded in bytes
+    const u64 ahead = std::min<u64>(room, std::max<u64>(4096, std::min<u64>(4 * (u64)P.max_total, ((u64)256 << 20) / (8 * (u64)h->n))));
+    P.entry_cap = h->n_entries + ahead;
+    {   // is the first level one for the device at all?  (same planner, on the host)
+        static thread_local std::vector<Piece> scratch(LTL_LV_MAX_PIECES);
+        i64 bf[LTL_LV_MAX_COST], be[LTL_LV_MAX_COST];
+        for (int k = 0; k < LTL_LV_MAX_COST; k++) {
+            bf[k] = k < (int)bucket.size() ? bucket[(size_t)k].first : 0;
+            be[k] = k < (int)bucket.size() ? bucket[(size_t)k].second : 0;
+        }
+        int np = 0;
+        i64 total = 0;
+        double bytes = 0;
+        P.table_cap = ~0ull;
+        if (!lv_plan(first_cost, P.op_cost, P.op_mask, bf, be, scratch.data(), LTL_LV_MAX_PIECES, &np, &total, &bytes, 0.0) ||
+            !lv_fits(P, total, h->n_entries, h->keys_upper))
+            return LTL_OK;
+    }
+    if (h->deadline_at > 0 && steady_seconds() > h->deadline_at) {
+        *status = LTL_S_TIMEOUT;
+        return LTL_OK;
+    }
+    if ((rc = flush_materialize(h))) return rc == LTL_ERR_DEVICE_OOM ? LTL_OK : rc;
+    if ((rc = apply_purge(h))) return rc;
+    if ((rc = ensure_table(h, h->keys_upper + 4 * (u64)P.max_total))) return rc == LTL_ERR_DEVICE_OOM ? LTL_OK : rc;
+    if ((rc = ensure_scratch(h, P.max_total))) return rc;
+    if ((rc = ensure_acc(h, P.max_total))) return rc;
+    if ((rc = ensure_entries(h, P.entry_cap))) return rc == LTL_ERR_DEVICE_OOM ? LTL_OK : rc;
+    if (!h->d_lv) {
+        CK(cudaMalloc(&h->d_lv, sizeof(LevelsState)));
+        CK(cudaMallocHost(&h->h_lv, sizeof(LevelsState)));
+    }
+    if (h->R > LTL_SPLIT_ROWS) {
+        // rows in several hash blocks: the blocks' sums meet in the partial-sum array.  `acc_dirty == false` only promises
+        // zeros in the part small host-driven passes use (LTL_SMALL_ADMIT candidates); a level here may be larger, and a
+        // pooled arena remembers the sums of an earlier search beyond that part (found by scripts/levels_diff.py)
+        CK(cudaMemsetAsync(h->d_acc, 0, (size_t)P.max_total * 24, h->stream));
+        if (h->acc_cap <= P.max_total) h->acc_dirty = false;  // (the kernel leaves the sums it consumed zeroed, like k_admit_small)
+    }
+    CK(cudaMemsetAsync(h->d_ctl, 0xFF, sizeof(Ctl), h->stream));
+    LevelsState& S = *h->h_lv;
+    memset(&S, 0, sizeof(S));
+    S.n_entries = h->n_entries;
+    S.offered = h->offered;
+    S.admitted = h->admitted;
+    S.duplicates = h->duplicates;
+    S.keys_upper = h->keys_upper;
+    S.next_cost = first_cost;
+    S.status = LTL_S_DONE;
+    S.unstored_from = ~0ull;
+    for (int k = 0; k < LTL_LV_MAX_COST && k < (int)bucket.size(); k++) {
+        S.bucket_first[k] = bucket[(size_t)k].first;
+        S.bucket_end[k] = bucket[(size_t)k].second;
+        S.known[k] = known[(size_t)k];
+    }
+    CK(cudaMemcpyAsync(h->d_lv, h->h_lv, sizeof(LevelsState), cudaMemcpyHostToDevice, h->stream));
+    h->h2d_bytes += sizeof(LevelsState);
+    P.sp.cms = (const u64*)h->cms.base;
+    P.sp.masks = h->d_masks;
+    P.sp.W = 1;
+    P.sp.n_pos = h->n_pos;
+    P.sp.n_pos_lo = h->n_pos_lo;
+    P.sp.err_max = h->err_max;
+    P.sp.variant = h->variant;
+    P.sp.mask_k = h->mask_k;
+    P.sp.n_dep = h->n_dep;
+    P.sp.deps = h->d_deps;
+    P.sp.mode = MODE_INSERT;
+    P.sp.check_solve = 1;
+    P.sp.table = h->table;
+    P.sp.table_mask = h->table_cap - 1;
+    P.sp.slot = h->d_slot;
+    P.sp.acc = h->d_acc;
+    P.sp.ctl = h->d_ctl;
+    P.sp.owner_world = 1;
+    P.cms_w = (u64*)h->cms.base;
+    P.rec_op = (unsigned char*)h->rec_op.base;
+    P.rec_lhs = (int*)h->rec_lhs.base;
+    P.rec_rhs = (int*)h->rec_rhs.base;
+    P.st = h->d_lv;
+    P.table_cap = h->table_cap;
+    const auto t0 = std::chrono::steady_clock::now();
+    {
+        ScopedTimer t(h, LTL_K_LEVELS, 0, 0.0);
+        cudaLaunchConfig_t cfg;
+        memset(&cfg, 0, sizeof(cfg));
+        cfg.gridDim = dim3((unsigned)h->levels_ctas, 1, 1);
+        cfg.blockDim = dim3(LTL_LV_CTA, 1, 1);
+        cfg.stream = h->stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = (unsigned)h->levels_ctas;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        if (h->variant == VAR_MUELLER) CK(cudaLaunchKernelEx(&cfg, k_levels<KIND_MUELLER>, P));
+        else if (h->variant == VAR_NH) CK(cudaLaunchKernelEx(&cfg, k_levels<KIND_NH>, P));
+        else CK(cudaLaunchKernelEx(&cfg, k_levels<KIND_BITS>, P));
+    }
+    CK(cudaMemcpyAsync(h->h_lv, h->d_lv, sizeof(LevelsState), cudaMemcpyDeviceToHost, h->stream));
+    {
+        HostTimer ht(&h->sync_ms);
+        CK(cudaStreamSynchronize(h->stream));
+    }
+    h->d2h_bytes += sizeof(LevelsState);
+    drain_events(h);
+    const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    if (getenv("LTL_LEVELS_TRACE")) {  // where the launch spent its time (device clock, ns since the level began)
+        for (int k = 0; k < S.n_rows; k++) {
+            const u64* t = S.t_ns[k];
+            fprintf(stderr, "levels: cost %d offered %llu admitted %llu  planned %llu screened %llu admitted %llu booked %llu stored %llu ns\n",
+                    S.rows[k].cost, (unsigned long long)S.rows[k].offered, (unsigned long long)S.rows[k].admitted,
+                    (unsigned long long)(t[1] - t[0]), (unsigned long long)(t[2] - t[0]), (unsigned long long)(t[3] - t[0]),
+                    (unsigned long long)(t[4] - t[0]), (unsigned long long)(t[5] ? t[5] - t[0] : 0));
+        }
+        fprintf(stderr, "levels: launch to state read back %.1f us, next cost %d (stop %d, unstored level %d)\n", 1e3 * ms, S.next_cost,
+                P.stop_cost, P.nostore_cost);
+        if (S.status == LTL_S_DONE && S.next_cost < P.stop_cost) {  // why the hand-over?
+            static thread_local std::vector<Piece> scratch(LTL_LV_MAX_PIECES);
+            int np = 0;
+            i64 total = 0;
+            double bytes = 0;
+            const bool planned = lv_plan(S.next_cost, P.op_cost, P.op_mask, S.bucket_first, S.bucket_end, scratch.data(), LTL_LV_MAX_PIECES,
+                                         &np, &total, &bytes, 0.0);
+            fprintf(stderr, "levels: level %d: planned %d, %d pieces, %lld candidates (max %lld), work %lld (max %lld), entries %llu + total vs cap %llu, keys %llu vs table %llu\n",
+                    S.next_cost, (int)planned, np, (long long)total, (long long)P.max_total, (long long)(total * P.sp.R),
+                    (long long)P.max_work, (unsigned long long)S.n_entries, (unsigned long long)P.entry_cap,
+                    (unsigned long long)S.keys_upper, (unsigned long long)P.table_cap);
+        }
+    }
+    h->stats[LTL_K_LEVELS].units += S.offered - h->offered;
+    h->stats[LTL_K_LEVELS].bytes += S.alg_bytes;
+    u64 admitted_run = h->admitted;
+    for (int k = 0; k < S.n_rows; k++) {
+        const LevelRow& r = S.rows[k];
+        if (r.cost == P.nostore_cost) {  // (what ltl_core_run_search does on entering the last level)
+            h->store_results = false;
+            h->unstored_from = S.unstored_from;
+        }
+        bucket[(size_t)r.cost] = std::make_pair((i64)r.first_entry, (i64)r.end_entry);
+        known[(size_t)r.cost] = 1;
+        admitted_run += r.admitted;
+        ltl_level_stats& row = rows[(*n_rows)++];
+        row.cost = r.cost;
+        row.status = r.status;
+        row.offered = r.offered;
+        row.admitted = r.admitted;
+        row.duplicates = r.duplicates;
+        row.bytes = admitted_run * h->entry_bytes;  // reference _speedups.pyx:260
+        row.first_entry = r.first_entry;
+        row.end_entry = r.end_entry;
+        row.ms = ms / (double)S.n_rows;
+    }
+    h->n_entries = S.n_entries;
+    h->offered = S.offered;
+    h->admitted = S.admitted;
+    h->duplicates = S.duplicates;
+    h->keys_upper = S.keys_upper;
+    *next_cost = S.next_cost;
+    if (S.status == LTL_S_SOLVED) {
+        *status = LTL_S_SOLVED;
+        *op = S.sol_op;
+        *li = S.sol_li;
+        *ri = S.sol_ri;
+        h->pending_purge = S.sol_gbase + S.sol_cut;  // keys filed at or above the cut are not members (run_chunk)
+        if (S.pend_count > 0 && h->store_results) {  // admitted, records written; matrices only if somebody asks for them
+            PendingMat pm;
+            pm.n_base = S.pend_base;
+            pm.count = S.pend_count;
+            h->pending_mat.push_back(std::move(pm));
+        }
+    }
+    return LTL_OK;
+}
+
 // The whole cost-level loop in one call (include/ltl_core.h).  Host work per level is a handful of integer operations
 // here instead of a trip through the caller's interpreter: searches of small levels are bound by exactly that.
 int ltl_core_run_search(ltl_core* h, const int32_t op_cost[8], uint32_t op_mask, const int64_t* bucket_cost,
@@ -2545,7 +2757,15 @@ int ltl_core_run_search(ltl_core* h, const int32_t op_cost[8], uint32_t op_mask,
     }
     std::vector<ltl_segment> segs;
     std::vector<Unit> units;
-    for (int c = first_cost; c < ceiling; c++) {
+    int c_start = first_cost;
+    {   // the small levels a search starts with: one launch (levels.cuh)
+        int rc = run_levels_device(h, op_cost, op_mask, bucket, known, first_cost, ceiling, store_last_level, rows, n_rows, status, op,
+                                   li, ri, &c_start);
+        if (rc) return rc;
+        *end_cost = std::min(c_start, ceiling);
+        if (*status == LTL_S_SOLVED || *status == LTL_S_TIMEOUT) return LTL_OK;
+    }
+    for (int c = c_start; c < ceiling; c++) {
         *end_cost = c;
         const auto t0 = std::chrono::steady_clock::now();
         // begin_level: reference cache.py:144-152
@@ -2826,6 +3046,13 @@ int ltl_core_set_option(ltl_core* h, const char* name, int64_t value) {
         h->small_screen = value != 0;
     } else if (!strcmp(name, "small_admit")) {
         h->small_admit = value != 0;
+    } else if (!strcmp(name, "device_levels")) {
+        h->device_levels = value != 0;
+    } else if (!strcmp(name, "levels_ctas")) {
+        if (value != 1 && value != 2 && value != 4 && value != 8) return h->fail(LTL_ERR_ARG, "levels_ctas must be 1, 2, 4 or 8");
+        h->levels_ctas = (int)value;
+    } else if (!strcmp(name, "levels_max_work")) {
+        h->levels_max_work = std::max<int64_t>(0, value);
     } else if (!strcmp(name, "fuse_not_min")) {
         h->fuse_not_min = value;
     } else if (!strcmp(name, "profile")) {

@@ -712,9 +712,193 @@ __global__ void __launch_bounds__(LTL_CTA, (W == 1 ? (KIND == KIND_REWRITE ? LTL
 // store (consecutive candidates share their left operand and read consecutive right operands), connective chosen by a
 // switch, partial sums combined with atomics like any row-split pass.  Bit-identical results: same connectives
 // (semantics.cuh), same fingerprint definitions as tile_eval, same finish_candidate.
+// one row of a one-word connective chosen at run time
+template <int OP_DUMMY = 0>
+__device__ __forceinline__ u64 small_apply(const int op, const u64 x, const u64 y, const u64 m) {
+    u64 xs[1] = {x}, ys[1] = {y}, ms[1] = {m}, out[1];
+    switch (op) {
+        case OP_NOT: apply_row<OP_NOT, 1>(out, xs, ys, ms); break;
+        case OP_AND: apply_row<OP_AND, 1>(out, xs, ys, ms); break;
+        case OP_OR: apply_row<OP_OR, 1>(out, xs, ys, ms); break;
+        case OP_NEXT: apply_row<OP_NEXT, 1>(out, xs, ys, ms); break;
+        case OP_FINALLY: apply_row<OP_FINALLY, 1>(out, xs, ys, ms); break;
+        case OP_GLOBALLY: apply_row<OP_GLOBALLY, 1>(out, xs, ys, ms); break;
+        case OP_UNTIL: apply_row<OP_UNTIL, 1>(out, xs, ys, ms); break;
+        default: out[0] = x; break;
+    }
+    return out[0];
+}
+
+// rows [r0, r1) of ONE candidate op(x [, y]) over one-word rows: classification errors of those rows and their share of
+// the two fingerprint sums (hash blocks are 64 rows: r0 is a multiple of 64 and r1 - r0 <= 64 or the range is whole
+// blocks).  NC: the operands are read through the non-coherent path (they were written by an earlier launch); the
+// device-resident level loop (levels.cuh) reads matrices written by the running kernel and passes false.
+// U rows are loaded before the first of them is used: a thread walks its rows alone, so the loop is bound by the
+// latency of its loads (L2: every small pass reads matrices the previous launch / phase wrote), not by their number
+template <int KIND, bool NC, int U>
+__device__ __forceinline__ void small_rows(const ScreenParams& p, const int op, const u64* __restrict__ px, const u64* __restrict__ py,
+                                           const int r0, const int r1, u64& s0, u64& s1, u32& err) {
+    constexpr bool NH = KIND == KIND_NH, MUELLER = KIND == KIND_MUELLER, HASHED = NH || MUELLER;
+    u64 h0 = NH ? 0ull : K_SEED0, h1 = NH ? 0ull : K_SEED1;
+    int d = 0;
+    if (KIND == KIND_BITS) {
+        int a = 0, b = p.n_dep;
+        while (a < b) {
+            const int mid = (a + b) >> 1;
+            if (p.deps[mid].k < (u32)r0) a = mid + 1;
+            else b = mid;
+        }
+        d = a;
+    }
+    const bool binary = py != px;
+    for (int rb = r0; rb < r1; rb += U) {
+        u64 xv[U], yv[U], mv[U];
+#pragma unroll
+        for (int k = 0; k < U; k++) {
+            const int r = min(rb + k, r1 - 1);
+            xv[k] = NC ? ld_nc(px + (size_t)r * 32) : __ldcg(px + (size_t)r * 32);
+            yv[k] = !binary ? 0ull : NC ? ld_nc(py + (size_t)r * 32) : __ldcg(py + (size_t)r * 32);
+            mv[k] = ld_nc(p.masks + r);
+        }
+#pragma unroll
+        for (int k = 0; k < U; k++) {
+            const int r = rb + k;
+            if (r >= r1) break;
+            const u64 v = small_apply(op, xv[k], binary ? yv[k] : xv[k], mv[k]);
+            const u32 bit = (u32)(v >> 63);
+            err += r < p.n_pos ? 1u - bit : bit;  // reference _speedups.pyx:327-333
+            if (NH) {  // oracle fp_nh
+                const u32 pk = (u32)r & 63u;
+                const u64 key0 = c_nh.k[pk], key1 = c_nh.k[pk + 1];
+                const u32 xl = (u32)v, xh = (u32)(v >> 32);
+                h0 = mad_wide(xl + (u32)key0, xh + (u32)(key0 >> 32), h0);
+                h1 = mad_wide(xl + (u32)key1, xh + (u32)(key1 >> 32), h1);
+            } else if (MUELLER) {  // reference _speedups.pyx:196-202, blocked
+                const u64 mm = mix64(v ^ (((u64)p.blk_base * 64ull + (u64)r + 1ull) * K_STEP));
+                h0 = (h0 ^ mm) * K_FOLD0;
+                h1 = (h1 ^ ((mm << 32) | (mm >> 32))) * K_FOLD1;
+            } else {  // gather / fkp deposits (reference _speedups.pyx:188-195, 205-222)
+                while (d < p.n_dep && p.deps[d].k <= (u32)r) {
+                    const Deposit dp = p.deps[d];
+                    const u64 w = (v >> dp.rsh) & dp.mask;
+                    if (dp.pos >= 64) s0 += w << (dp.pos - 64);
+                    else {
+                        s1 += w << dp.pos;
+                        if (dp.pos > 0) s0 += w >> (64 - dp.pos);
+                    }
+                    d++;
+                }
+            }
+            if (HASHED && ((((u32)r + 1u) & 63u) == 0 || r + 1 == p.R)) {  // the hash block ends with this word
+                const u32 blk = ((u32)r >> 6) + p.blk_base;
+                if (NH) {
+                    const u64 u = (u64)(blk + 1) * K_STEP;
+                    s0 += mix64(h0 ^ u);
+                    s1 += mix64(h1 + u);
+                    h0 = h1 = 0;
+                } else {
+                    s0 += blk == 0 ? h0 : mix64(h0);
+                    s1 += blk == 0 ? h1 : mix64(h1);
+                    h0 = K_SEED0;
+                    h1 = K_SEED1;
+                }
+            }
+        }
+    }
+}
+
+// NH over ONE hash block (rows [r0, r1), r0 a multiple of 64, r1 <= r0 + 64) by a group of 8 neighbouring lanes: lane `sub`
+// takes rows r0 + sub, r0 + sub + 8, ...  The block's two NH accumulators are sums of products and the error count is a
+// sum, so the lanes' partial sums are combined with three shuffle steps; every lane of the group returns the block's
+// contribution (s0, s1, err) -- bit-identical to small_rows<KIND_NH>.  All 32 lanes of the warp must call it (`valid` false:
+// no loads).  A thread that walks 64 rows alone is bound by the latency of its dependent instructions (~1.5 us per 4 rows
+// measured in the level loop); eight rows per lane leave 1/8 of that chain.
+template <bool NC>
+__device__ __forceinline__ void small_block_nh8(const ScreenParams& p, const int op, const u64* __restrict__ px,
+                                                const u64* __restrict__ py, const int r0, const int r1, const int sub,
+                                                const bool valid, u64& s0, u64& s1, u32& err) {
+    const bool binary = py != px;
+    u64 h0 = 0, h1 = 0;
+    u32 e = 0;
+#pragma unroll
+    for (int half = 0; half < 2; half++) {
+        u64 xv[4], yv[4];
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int r = r0 + sub + 8 * (4 * half + k);
+            const bool in = valid && r < r1;
+            xv[k] = !in ? 0ull : NC ? ld_nc(px + (size_t)r * 32) : __ldcg(px + (size_t)r * 32);
+            yv[k] = !(in && binary) ? 0ull : NC ? ld_nc(py + (size_t)r * 32) : __ldcg(py + (size_t)r * 32);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; k++) {
+            const int r = r0 + sub + 8 * (4 * half + k);
+            if (!(valid && r < r1)) continue;
+            const u64 v = small_apply(op, xv[k], binary ? yv[k] : xv[k], ld_nc(p.masks + r));
+            const u32 bit = (u32)(v >> 63);
+            e += r < p.n_pos ? 1u - bit : bit;  // reference _speedups.pyx:327-333
+            const u32 pk = (u32)r & 63u;  // oracle fp_nh
+            const u64 key0 = c_nh.k[pk], key1 = c_nh.k[pk + 1];
+            const u32 xl = (u32)v, xh = (u32)(v >> 32);
+            h0 = mad_wide(xl + (u32)key0, xh + (u32)(key0 >> 32), h0);
+            h1 = mad_wide(xl + (u32)key1, xh + (u32)(key1 >> 32), h1);
+        }
+    }
+#pragma unroll
+    for (int d = 4; d >= 1; d >>= 1) {
+        h0 += __shfl_xor_sync(0xFFFFFFFFu, h0, d);
+        h1 += __shfl_xor_sync(0xFFFFFFFFu, h1, d);
+        e += __shfl_xor_sync(0xFFFFFFFFu, e, d);
+    }
+    const u64 u = (u64)(((u32)r0 >> 6) + p.blk_base + 1) * K_STEP;
+    s0 = mix64(h0 ^ u);
+    s1 = mix64(h1 + u);
+    err = e;
+}
+
+// k_screen_small for the NH fingerprint: 8 lanes per (candidate, block of 64 rows)
+template <int KIND>  // (KIND_NH only; a template so that every translation unit may see the definition)
+__global__ void __launch_bounds__(256) k_screen_small_nh8(const __grid_constant__ ScreenParams p, const u64 total) {
+    static_assert(KIND == KIND_NH, "the 8-lane split needs a fingerprint that is a sum over rows");
+    const int sub = threadIdx.x & 7;
+    const u64 c = (u64)blockIdx.x * 32 + (threadIdx.x >> 3);
+    bool valid = c < total;
+    int op = 0;
+    i64 i = 0, j = -1;
+    if (valid) {
+        int lo = 0, hi = p.n_pieces - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if ((u64)p.pieces[mid].cbase <= c) lo = mid;
+            else hi = mid - 1;
+        }
+        const Piece& pc = p.pieces[lo];
+        if (pc.ext) valid = false;  // evaluated by phase B of the entries it ranges over (fused NOT)
+        else {
+            piece_unrank(pc, c, &i, &j);
+            op = pc.op;
+        }
+    }
+    const i64 n = p.n;
+    const int r0 = (int)blockIdx.y * LTL_SPLIT_ROWS, r1 = min(p.R, r0 + LTL_SPLIT_ROWS);
+    const u64* __restrict__ px = p.cms + cm_index(i, n, 0);
+    const u64* __restrict__ py = j >= 0 ? p.cms + cm_index(j, n, 0) : px;
+    u64 s0, s1;
+    u32 err;
+    small_block_nh8<true>(p, op, px, py, r0, r1, sub, valid, s0, s1, err);
+    if (!valid || sub != 0) return;
+    if (p.nsplit > 1 || p.defer) {
+        atomicAdd(p.acc + 3 * c, s0);
+        atomicAdd(p.acc + 3 * c + 1, s1);
+        if (err) atomicAdd(p.acc + 3 * c + 2, (u64)err);
+    } else {
+        finish_candidate<true>(p, c, s0, s1, err);
+    }
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(256) k_screen_small(const __grid_constant__ ScreenParams p, const u64 total) {
-    constexpr bool NH = KIND == KIND_NH, MUELLER = KIND == KIND_MUELLER, HASHED = NH || MUELLER;
+    constexpr bool HASHED = KIND == KIND_NH || KIND == KIND_MUELLER;
     const u64 c = (u64)blockIdx.x * 256 + threadIdx.x;
     if (c >= total) return;
     int lo = 0, hi = p.n_pieces - 1;
@@ -727,76 +911,13 @@ __global__ void __launch_bounds__(256) k_screen_small(const __grid_constant__ Sc
     if (pc.ext) return;  // evaluated by phase B of the entries it ranges over (fused NOT)
     i64 i, j;
     piece_unrank(pc, c, &i, &j);
-    const int op = pc.op;
     const i64 n = p.n;
     const int r0 = (int)blockIdx.y * p.rows_per_split, r1 = min(p.R, r0 + p.rows_per_split);
     const u64* __restrict__ px = p.cms + cm_index(i, n, 0);
     const u64* __restrict__ py = j >= 0 ? p.cms + cm_index(j, n, 0) : px;
-    u64 s0 = 0, s1 = 0, h0 = NH ? 0ull : K_SEED0, h1 = NH ? 0ull : K_SEED1;
+    u64 s0 = 0, s1 = 0;
     u32 err = 0;
-    int d = 0;
-    if (KIND == KIND_BITS) {
-        int a = 0, b = p.n_dep;
-        while (a < b) {
-            const int mid = (a + b) >> 1;
-            if (p.deps[mid].k < (u32)r0) a = mid + 1;
-            else b = mid;
-        }
-        d = a;
-    }
-    for (int r = r0; r < r1; r++) {
-        const u64 x = ld_nc(px + (size_t)r * 32), y = ld_nc(py + (size_t)r * 32), m = ld_nc(p.masks + r);
-        u64 xs[1] = {x}, ys[1] = {y}, ms[1] = {m}, out[1];
-        switch (op) {
-            case OP_NOT: apply_row<OP_NOT, 1>(out, xs, ys, ms); break;
-            case OP_AND: apply_row<OP_AND, 1>(out, xs, ys, ms); break;
-            case OP_OR: apply_row<OP_OR, 1>(out, xs, ys, ms); break;
-            case OP_NEXT: apply_row<OP_NEXT, 1>(out, xs, ys, ms); break;
-            case OP_FINALLY: apply_row<OP_FINALLY, 1>(out, xs, ys, ms); break;
-            case OP_GLOBALLY: apply_row<OP_GLOBALLY, 1>(out, xs, ys, ms); break;
-            case OP_UNTIL: apply_row<OP_UNTIL, 1>(out, xs, ys, ms); break;
-            default: out[0] = x; break;
-        }
-        const u64 v = out[0];
-        const u32 bit = (u32)(v >> 63);
-        err += r < p.n_pos ? 1u - bit : bit;  // reference _speedups.pyx:327-333
-        if (NH) {  // oracle fp_nh
-            const u32 pk = (u32)r & 63u;
-            const u64 key0 = c_nh.k[pk], key1 = c_nh.k[pk + 1];
-            const u32 xl = (u32)v, xh = (u32)(v >> 32);
-            h0 = mad_wide(xl + (u32)key0, xh + (u32)(key0 >> 32), h0);
-            h1 = mad_wide(xl + (u32)key1, xh + (u32)(key1 >> 32), h1);
-        } else if (MUELLER) {  // reference _speedups.pyx:196-202, blocked
-            const u64 mm = mix64(v ^ (((u64)p.blk_base * 64ull + (u64)r + 1ull) * K_STEP));
-            h0 = (h0 ^ mm) * K_FOLD0;
-            h1 = (h1 ^ ((mm << 32) | (mm >> 32))) * K_FOLD1;
-        } else {  // gather / fkp deposits (reference _speedups.pyx:188-195, 205-222)
-            while (d < p.n_dep && p.deps[d].k <= (u32)r) {
-                const Deposit dp = p.deps[d];
-                const u64 w = (v >> dp.rsh) & dp.mask;
-                if (dp.pos >= 64) s0 += w << (dp.pos - 64);
-                else {
-                    s1 += w << dp.pos;
-                    if (dp.pos > 0) s0 += w >> (64 - dp.pos);
-                }
-                d++;
-            }
-        }
-        if (HASHED && ((((u32)r + 1u) & 63u) == 0 || r + 1 == p.R)) {  // the hash block ends with this word
-            const u32 blk = ((u32)r >> 6) + p.blk_base;
-            if (NH) {
-                const u64 u = (u64)(blk + 1) * K_STEP;
-                s0 += mix64(h0 ^ u);
-                s1 += mix64(h1 + u);
-                h0 = h1 = 0;
-            } else {
-                s0 += blk == 0 ? h0 : mix64(h0);
-                s1 += blk == 0 ? h1 : mix64(h1);
-                h0 = K_SEED0;
-                h1 = K_SEED1;
-            }
-        }
-    }
+    small_rows<KIND, true, 8>(p, pc.op, px, py, r0, r1, s0, s1, err);
     if (p.nsplit > 1 || p.defer) {
         atomicAdd(p.acc + 3 * c, s0);
         atomicAdd(p.acc + 3 * c + 1, s1);

@@ -50,6 +50,8 @@ extern "C" void LTL_CAT(ltl_launch_screen_w, LTL_W)(const ScreenParams& p, int k
 extern "C" void ltl_launch_screen_small(const ScreenParams& p, int kind, unsigned long long total, cudaStream_t stream) {
     dim3 grid((unsigned)((total + 255) / 256), (unsigned)p.nsplit);
     if (kind == KIND_MUELLER) k_screen_small<KIND_MUELLER><<<grid, 256, 0, stream>>>(p, total);
+    else if (kind == KIND_NH && p.rows_per_split == LTL_SPLIT_ROWS)  // (always: core.cu cuts small passes into hash blocks)
+        k_screen_small_nh8<KIND_NH><<<dim3((unsigned)((total + 31) / 32), (unsigned)p.nsplit), 256, 0, stream>>>(p, total);
     else if (kind == KIND_NH) k_screen_small<KIND_NH><<<grid, 256, 0, stream>>>(p, total);
     else k_screen_small<KIND_BITS><<<grid, 256, 0, stream>>>(p, total);
 }

@@ -100,6 +100,8 @@ while time.time() < t_end:
     desc = f"#{n} props={n_props} P={spec.n_pos} N={spec.n_neg} len={lo}..{hi} planted={planted} {kw}"
     fused_opts = "fuse_not_min=0" + (",chunk_candidates=%d" % int(rng.integers(100, 5000)) if rng.random() < 0.3 else "")
     with_cand2 = rng.random() < 0.3
+    if os.environ.get("SOAK_ONLY") and n > int(os.environ["SOAK_ONLY"]):
+        break
     if os.environ.get("SOAK_ONLY") and n != int(os.environ["SOAK_ONLY"]):
         continue
     if os.environ.get("SOAK_VERBOSE"):
@@ -112,6 +114,14 @@ while time.time() < t_end:
     runs["single"] = [summary(L.learn(spec, None, al, **kw))]
     os.environ["LTL_CORE_OPTIONS"] = fused_opts
     runs["fused"] = [summary(L.learn(spec, None, al, **kw))]
+    # the device-resident first levels (levels.cuh) switched off; and on a smaller cluster, handing over to the
+    # host-driven path at a random point
+    os.environ["LTL_CORE_OPTIONS"] = "device_levels=0"
+    runs["host_levels"] = [summary(L.learn(spec, None, al, **kw))]
+    os.environ["LTL_CORE_OPTIONS"] = "levels_ctas=%d,levels_max_work=%d" % (int(rng.choice([1, 2, 4, 8])), int(rng.choice([1 << 10, 1 << 14, 1 << 18, 1 << 24])))
+    if os.environ.get("SOAK_LEVELS_OPTS"):  # reproduction of one case with chosen options
+        os.environ["LTL_CORE_OPTIONS"] = os.environ["SOAK_LEVELS_OPTS"]
+    runs["levels_hand_over"] = [summary(L.learn(spec, None, al, **kw))]
     # round 2 paths: the level loop driven from Python (one run_level per level) with the big-pass bookkeeping kernels and
     # the phase-B order forced onto every pass (blocks of 32 entries); the specification uploaded as array pairs and
     # checked / packed / searched on the device; the reference's debug invariant on every stored matrix

@@ -206,13 +206,16 @@ def test_transcripts_golden():
         cuda.close()
 
 
-@pytest.mark.parametrize("native_loop,options", [(True, ""), (False, ""), (True, "small_screen=0,small_admit=0")],
-                         ids=["run_search", "run_level", "big_kernels"])
+@pytest.mark.parametrize("native_loop,options", [(True, ""), (False, ""), (True, "small_screen=0,small_admit=0"),
+                                                 (True, "device_levels=0"), (True, "levels_ctas=1"),
+                                                 (True, "levels_max_work=2048")],
+                         ids=["run_search", "run_level", "big_kernels", "host_levels", "levels_one_cta", "levels_hand_over"])
 @pytest.mark.parametrize("case", golden()["learn"], ids=lambda c: c["name"])
 def test_learn_golden_cases(case, native_loop, options, monkeypatch):
     """The product path end to end (learner -> C ABI -> CUDA) against the reference's recorded outcomes, with the
-    cost-level loop inside the library (`ltl_core_run_search`, the default) and with one `run_level` call per level
-    from `learner.py`."""
+    cost-level loop inside the library (`ltl_core_run_search`, the default: the first small levels in one launch planned
+    on the device, `levels.cuh`, the rest host-driven), with that launch switched off, on one CTA, handing over to the
+    host-driven path early, and with one `run_level` call per level from `learner.py`."""
     monkeypatch.setattr(L.Enumeration, "native_loop", native_loop)
     if options:  # small passes through the kernels big passes use (tile phase A, four bookkeeping kernels)
         monkeypatch.setenv("LTL_CORE_OPTIONS", options)
@@ -597,3 +600,43 @@ def test_phase_b_order_matches_oracle(R, W, variant, fuse_not_min):
     assert (plain.export_cms() == cuda.export_cms()).all()
     cuda.close()
     plain.close()
+
+
+@pytest.mark.gpu
+def test_device_levels_match_host_levels(monkeypatch):
+    """The device-resident first levels (`levels.cuh`: one launch, planned on the device) against the host-driven level
+    loop on random specifications -- rows in one and in several hash blocks, every fingerprint variant, masking, noise,
+    a stored and an unstored last level -- for several cluster sizes and hand-over points.  The cases share one process
+    on purpose: cores are built on pooled arenas, and what an earlier search left in them (partial sums beyond the part
+    small passes clear) once leaked into the next one."""
+    from paper_2402_12373_b200.scheme import HashScheme
+
+    def summary(res):
+        lv = [(x["cost"], x["offered"], x["admitted"], x["duplicates"], x["bytes"]) for x in res.stats.levels]
+        return res.status, res.text, res.cost, res.stats.offered, res.stats.admitted, res.stats.duplicates, lv
+
+    for k in range(60):
+        rng = np.random.default_rng(1000 + k)
+        n_props = int(rng.integers(1, 4))
+        n_pos, n_neg = int(rng.integers(1, 300)), int(rng.integers(1, 300))
+        hi = int(rng.choice([5, 20, 45, 64]))
+        lo = int(rng.integers(1, hi + 1))
+        population = 1 << 40 if hi > 12 else sum((1 << n_props) ** length for length in range(lo, hi + 1))
+        if n_pos + n_neg > population // 3:
+            n_pos, n_neg = max(1, population // 8), max(1, population // 8)
+        try:
+            spec, alphabet = random_spec(rng, n_props, n_pos, n_neg, lo, hi)
+        except (RuntimeError, ValueError):
+            continue
+        kw = dict(max_cost=int(rng.integers(4, 8)))
+        if rng.random() < 0.3:
+            kw["noise"] = float(rng.choice([0.02, 0.1]))
+        if rng.random() < 0.6:
+            kw["hash"] = HashScheme(str(rng.choice(["mueller", "nh", "mueller_blocked", "fkp"])), int(rng.choice([0, 0, 20, 90])))
+        if rng.random() < 0.2:
+            kw["store_last_level"] = True
+        monkeypatch.setenv("LTL_CORE_OPTIONS", "device_levels=0")
+        want = summary(L.learn(spec, None, alphabet, **kw))
+        for ctas, max_work in ((8, 1 << 18), (8, 1 << 24), (1, 1 << 24), (4, 1 << 14)):
+            monkeypatch.setenv("LTL_CORE_OPTIONS", f"levels_ctas={ctas},levels_max_work={max_work}")
+            assert summary(L.learn(spec, None, alphabet, **kw)) == want, (k, ctas, max_work, kw)
