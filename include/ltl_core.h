@@ -283,6 +283,16 @@ LTL_API int ltl_core_stream(ltl_core* h, void** stream_out);
  *                matrices are materialised locally from the records when first needed
  *   stage_purge  forget keys filed at or above a global rank (solver / budget cut) */
 LTL_API int ltl_core_level_size(ltl_core* h, const ltl_segment* segs, int n_segs, int64_t* total);
+
+/* The planner of the device-resident cost levels, callable on the host (no GPU, no handle): the pieces of cost level
+ * `cost` in enumeration order -- what ltl_core_run_search's first launch (csrc/levels.cuh) builds for itself on the device
+ * from its bucket table, i.e. the child-cost pairing of reference enumerator.py:254-268 in the dispatch order of 271-296
+ * with triangular segments expanded as _speedups.pyx:364-368 does.  Buckets as for ltl_core_run_search.  Per piece:
+ * op_out, kind_out (0 unary [i0, i1); 1 rectangle [i0, i1) x [j0, j1); 2 triangle i in [i0, i1), j in (i, j1)),
+ * range_out[4] = i0, i1, j0, j1 and count_out.  Returns LTL_ERR_ARG when the level needs more than `cap` pieces. */
+LTL_API int ltl_plan_level(const int32_t op_cost[8], uint32_t op_mask, const int64_t* bucket_cost, const int64_t* bucket_first,
+                           const int64_t* bucket_end, int n_buckets, int cost, int cap, int32_t* op_out, int32_t* kind_out,
+                           int64_t* range_out, int64_t* count_out, int* n_pieces, int64_t* total);
 LTL_API int ltl_core_stage_eval(ltl_core* h, const ltl_segment* segs, int n_segs, int64_t lo, int64_t hi, uint64_t* d_fp,
                         int64_t* solver_rank);
 LTL_API int ltl_core_stage_file(ltl_core* h, const uint64_t* d_tuples, int64_t count, unsigned char* d_win, int64_t* n_win);

@@ -3107,6 +3107,39 @@ int ltl_core_level_size(ltl_core* h, const ltl_segment* segs, int n_segs, int64_
     return LTL_OK;
 }
 
+int ltl_plan_level(const int32_t op_cost[8], uint32_t op_mask, const int64_t* bucket_cost, const int64_t* bucket_first,
+                   const int64_t* bucket_end, int n_buckets, int cost, int cap, int32_t* op_out, int32_t* kind_out,
+                   int64_t* range_out, int64_t* count_out, int* n_pieces, int64_t* total) {
+    if (!op_cost || n_buckets < 0 || (n_buckets && (!bucket_cost || !bucket_first || !bucket_end)) || cap < 0 || !n_pieces || !total ||
+        (cap && (!op_out || !kind_out || !range_out || !count_out)) || cost < 1 || cost > LTL_LV_MAX_COST)
+        return LTL_ERR_ARG;
+    i64 bf[LTL_LV_MAX_COST] = {0}, be[LTL_LV_MAX_COST] = {0};
+    for (int b = 0; b < n_buckets; b++)
+        if (bucket_cost[b] >= 0 && bucket_cost[b] < LTL_LV_MAX_COST) {
+            bf[bucket_cost[b]] = bucket_first[b];
+            be[bucket_cost[b]] = bucket_end[b];
+        }
+    std::vector<Piece> pieces((size_t)std::max(cap, 1));
+    int oc[8];
+    for (int k = 0; k < 8; k++) oc[k] = op_cost[k];
+    int np = 0;
+    i64 tot = 0;
+    double bytes = 0;
+    if (!lv_plan(cost, oc, op_mask, bf, be, pieces.data(), cap, &np, &tot, &bytes, 0.0)) return LTL_ERR_ARG;
+    for (int k = 0; k < np; k++) {
+        op_out[k] = pieces[(size_t)k].op;
+        kind_out[k] = pieces[(size_t)k].kind;
+        range_out[4 * k] = pieces[(size_t)k].i0;
+        range_out[4 * k + 1] = pieces[(size_t)k].i1;
+        range_out[4 * k + 2] = pieces[(size_t)k].j0;
+        range_out[4 * k + 3] = pieces[(size_t)k].j1;
+        count_out[k] = pieces[(size_t)k].count;
+    }
+    *n_pieces = np;
+    *total = tot;
+    return LTL_OK;
+}
+
 int ltl_core_set_row_shard(ltl_core* h, int64_t word_base, int64_t total_words, ltl_exchange_fn fn, void* ctx) {
     ENTER(h);
     if (h->n_entries || h->offered) return h->fail(LTL_ERR_ARG, "set_row_shard: the core is already in use");
