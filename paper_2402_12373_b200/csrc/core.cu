@@ -40,6 +40,11 @@ LTL_DECL_W(9) LTL_DECL_W(10) LTL_DECL_W(11) LTL_DECL_W(12) LTL_DECL_W(13) LTL_DE
 extern "C" void ltl_launch_screen_w1p(const ScreenParams&, int, dim3, cudaStream_t);
 extern "C" void ltl_launch_screen_small(const ScreenParams&, int, unsigned long long, cudaStream_t);
 extern "C" void ltl_launch_materialize_w1p(const MaterializeParams&, const ScreenParams&, int, dim3, cudaStream_t);
+// small NH passes over rows of 2 / 4 / 8 / 16 words
+extern "C" void ltl_launch_screen_small_w2(const ScreenParams&, unsigned long long, cudaStream_t);
+extern "C" void ltl_launch_screen_small_w4(const ScreenParams&, unsigned long long, cudaStream_t);
+extern "C" void ltl_launch_screen_small_w8(const ScreenParams&, unsigned long long, cudaStream_t);
+extern "C" void ltl_launch_screen_small_w16(const ScreenParams&, unsigned long long, cudaStream_t);
 
 static const screen_launch_fn SCREEN_FN[LTL_MAX_W + 1] = {
     nullptr, ltl_launch_screen_w1, ltl_launch_screen_w2, ltl_launch_screen_w3, ltl_launch_screen_w4,
@@ -1480,9 +1485,11 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     p.total_tiles = tiles;
     choose_split(h, tiles, &p.nsplit, &p.rows_per_split);
     // small passes over one-word rows go through the compact kernel: blocks of 64 rows per thread
-    const bool small_screen = h->small_screen && h->W == 1 && !h->pair && mode != MODE_REWRITE && total <= LTL_SMALL_SCREEN &&
-                              (i64)total * (i64)h->R <= ((i64)1 << 24) && h->force_split == 0 && !h->exchange &&
-                              h->R <= 65535 * LTL_SPLIT_ROWS;
+    // (rows of 2 / 4 / 8 / 16 words tile the 64-word hash blocks: k_screen_small_rows, NH only)
+    const bool small_rows_w = (h->W == 2 || h->W == 4 || h->W == 8 || h->W == 16) && h->variant == VAR_NH;
+    const bool small_screen = h->small_screen && (h->W == 1 || small_rows_w) && !h->pair && mode != MODE_REWRITE &&
+                              total <= LTL_SMALL_SCREEN && (i64)total * h->n <= ((i64)1 << (h->W == 1 ? 24 : 22)) && h->force_split == 0 &&
+                              !h->exchange && h->R <= 65535 * LTL_SPLIT_ROWS;
     if (small_screen) {
         p.rows_per_split = LTL_SPLIT_ROWS;
         p.nsplit = (h->R + LTL_SPLIT_ROWS - 1) / LTL_SPLIT_ROWS;
@@ -1503,7 +1510,7 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     p.defer = h->exchange ? 1 : 0;
     p.owner_world = h->exchange ? h->table_shards : 1;
     p.owner_rank = h->table_shard;
-    const bool acc_path = p.nsplit > 1 || p.defer;
+    const bool acc_path = p.nsplit > 1 || p.defer || (small_screen && h->W > 1);  // (the multi-word small kernel always sums blocks)
     if (acc_path) {
         if ((rc = ensure_acc(h, total))) return rc;
         p.acc = h->d_acc;
@@ -1528,7 +1535,11 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
         ScopedTimer t(h, LTL_K_SCREEN, (u64)total, screen_bytes(h, pieces));
         issued_units = (u64)total;
         issued_bytes = screen_bytes(h, pieces);
-        ltl_launch_screen_small(p, screen_kind, (unsigned long long)total, h->stream);
+        if (h->W == 1) ltl_launch_screen_small(p, screen_kind, (unsigned long long)total, h->stream);
+        else if (h->W == 2) ltl_launch_screen_small_w2(p, (unsigned long long)total, h->stream);
+        else if (h->W == 4) ltl_launch_screen_small_w4(p, (unsigned long long)total, h->stream);
+        else if (h->W == 8) ltl_launch_screen_small_w8(p, (unsigned long long)total, h->stream);
+        else ltl_launch_screen_small_w16(p, (unsigned long long)total, h->stream);
         CK(cudaGetLastError());
     } else if (p.defer) {
         // Row shards: every shard adds its partial sums, then all of them complete identical candidates.  The pass is cut
@@ -1731,6 +1742,7 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
         pm.count = count;
         // per-record gathers waste most of each sector once matrices are long and buckets small; with short
         // matrices and dense winners the record form reads less (losers are never evaluated) -- measured both ways
+        // (also for a few hundred winners: per-record phase B of BASELINE config 3's cost levels 2-4 measured slower)
         pm.tiled = h->tiled_materialize == 1 || (h->tiled_materialize < 0 && h->n >= 4096);
         if (pm.tiled) {
             pm.pieces = pieces;

@@ -927,6 +927,84 @@ __global__ void __launch_bounds__(256) k_screen_small(const __grid_constant__ Sc
     }
 }
 
+// Small passes over rows of W = 2, 4, 8 or 16 words (NH fingerprint): one lane per (candidate, row).  The row is the unit
+// of the connectives (carries run through its W words), the 64-word hash block the unit of the fingerprint: a block is
+// 64 / W whole rows, i.e. 64 / W neighbouring lanes, which combine their sums with shuffles; the blocks' sums meet in the
+// partial-sum array like the row splits of any pass.  (The tile kernel spent 0.1-0.2 ms on each of the first five cost
+// levels of BASELINE config 3 -- a dozen to a few thousand candidates -- whatever the work.)
+template <int W>
+__global__ void __launch_bounds__(256) k_screen_small_rows(const __grid_constant__ ScreenParams p, const u64 total) {
+    static_assert(W > 1 && W <= 16 && 64 % W == 0, "rows must tile the 64-word hash blocks");
+    constexpr int LPB = 64 / W;  // lanes (rows) per hash block
+    const int l = threadIdx.x & 63;
+    const u64 c = (u64)blockIdx.x * 4 + (threadIdx.x >> 6);
+    bool valid = c < total;
+    int op = 0;
+    i64 i = 0, j = -1;
+    if (valid) {
+        int lo = 0, hi = p.n_pieces - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if ((u64)p.pieces[mid].cbase <= c) lo = mid;
+            else hi = mid - 1;
+        }
+        const Piece& pc = p.pieces[lo];
+        if (pc.ext) valid = false;
+        else {
+            piece_unrank(pc, c, &i, &j);
+            op = pc.op;
+        }
+    }
+    const int r = (int)blockIdx.y * LTL_SPLIT_ROWS + l;
+    const bool in = valid && r < p.R;
+    const size_t kb = (size_t)r * W;
+    u64 h0 = 0, h1 = 0;
+    u32 e = 0;
+    if (in) {
+        const i64 n = p.n;
+        const u64* __restrict__ px = p.cms + cm_index(i, n, 0);
+        const u64* __restrict__ py = j >= 0 ? p.cms + cm_index(j, n, 0) : px;
+        u64 x[W], y[W], m[W], out[W];
+#pragma unroll
+        for (int w = 0; w < W; w++) {
+            x[w] = ld_nc(px + (kb + w) * 32);
+            y[w] = j >= 0 ? ld_nc(py + (kb + w) * 32) : 0ull;
+            m[w] = ld_nc(p.masks + kb + w);
+        }
+        switch (op) {
+            case OP_NOT: apply_row<OP_NOT, W>(out, x, y, m); break;
+            case OP_AND: apply_row<OP_AND, W>(out, x, y, m); break;
+            case OP_OR: apply_row<OP_OR, W>(out, x, y, m); break;
+            case OP_NEXT: apply_row<OP_NEXT, W>(out, x, y, m); break;
+            case OP_FINALLY: apply_row<OP_FINALLY, W>(out, x, y, m); break;
+            case OP_GLOBALLY: apply_row<OP_GLOBALLY, W>(out, x, y, m); break;
+            case OP_UNTIL: apply_row<OP_UNTIL, W>(out, x, y, m); break;
+            default: apply_row<OP_IDENT, W>(out, x, y, m); break;
+        }
+        const u32 bit = (u32)(out[0] >> 63);
+        e = r < p.n_pos ? 1u - bit : bit;  // reference _speedups.pyx:327-333
+        const u32 pk0 = (u32)kb & 63u;     // the row lies inside one hash block: no wrap of the key index
+#pragma unroll
+        for (int w = 0; w < W; w++) {  // oracle fp_nh
+            const u64 key0 = c_nh.k[pk0 + w], key1 = c_nh.k[pk0 + w + 1];
+            const u32 xl = (u32)out[w], xh = (u32)(out[w] >> 32);
+            h0 = mad_wide(xl + (u32)key0, xh + (u32)(key0 >> 32), h0);
+            h1 = mad_wide(xl + (u32)key1, xh + (u32)(key1 >> 32), h1);
+        }
+    }
+#pragma unroll
+    for (int d = LPB / 2; d >= 1; d >>= 1) {
+        h0 += __shfl_xor_sync(0xFFFFFFFFu, h0, d);
+        h1 += __shfl_xor_sync(0xFFFFFFFFu, h1, d);
+        e += __shfl_xor_sync(0xFFFFFFFFu, e, d);
+    }
+    if (!in || (l & (LPB - 1))) return;  // the block's first row speaks for it (rows ascend: it is valid if any is)
+    const u64 u = (u64)((u32)(kb >> 6) + p.blk_base + 1) * K_STEP;
+    atomicAdd(p.acc + 3 * c, mix64(h0 ^ u));
+    atomicAdd(p.acc + 3 * c + 1, mix64(h1 + u));
+    if (e) atomicAdd(p.acc + 3 * c + 2, (u64)e);
+}
+
 // ------------------------------------------------------------------------------------------------
 // phase B kernel
 

@@ -57,6 +57,13 @@ extern "C" void ltl_launch_screen_small(const ScreenParams& p, int kind, unsigne
 }
 #endif
 
+#if LTL_W == 2 || LTL_W == 4 || LTL_W == 8 || LTL_W == 16
+// small NH passes over rows of 2 / 4 / 8 / 16 words (screen.cuh: k_screen_small_rows); sums go to p.acc
+extern "C" void LTL_CAT(ltl_launch_screen_small_w, LTL_W)(const ScreenParams& p, unsigned long long total, cudaStream_t stream) {
+    k_screen_small_rows<LTL_W><<<dim3((unsigned)((total + 3) / 4), (unsigned)p.nsplit), 256, 0, stream>>>(p, total);
+}
+#endif
+
 // fuse_kind != 0 (one-word rows only; the host never asks otherwise): phase B that also screens NOT(new entry)
 extern "C" void LTL_CAT(ltl_launch_materialize_w, LTL_W)(const MaterializeParams& p, const ScreenParams& sp, int fuse_kind,
                                                           dim3 grid, cudaStream_t stream) {
