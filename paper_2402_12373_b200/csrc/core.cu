@@ -804,6 +804,7 @@ struct PendingEvent {
 struct PendingMat {
     u64 n_base = 0, count = 0;
     bool tiled = false;
+    bool small_rows = false;  // multi-word rows, a small pass: one lane per (entry, row) (k_materialize_small_rows)
     int n_seg = 0;  // > 0: the phase-B order of this range is in the core's plan buffers
     std::vector<Piece> pieces;
     i64 total = 0, tiles = 0;
@@ -1744,6 +1745,10 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
         // matrices and dense winners the record form reads less (losers are never evaluated) -- measured both ways
         // (also for a few hundred winners: per-record phase B of BASELINE config 3's cost levels 2-4 measured slower)
         pm.tiled = h->tiled_materialize == 1 || (h->tiled_materialize < 0 && h->n >= 4096);
+        if (small_screen && h->W > 1 && h->tiled_materialize < 0) {  // (a few hundred winners: neither tiles nor warps per 32 entries)
+            pm.tiled = false;
+            pm.small_rows = true;
+        }
         if (pm.tiled) {
             pm.pieces = pieces;
             pm.total = total;
@@ -1875,6 +1880,16 @@ static int flush_materialize(ltl_core* h, const ScreenParams* sp, int fuse_kind,
             m.seg_g0 = h->d_plan_g0;
             m.seg_goff = h->d_plan_off;
             h->plan_in_use = false;  // (the launch below is the last reader; later plans are written behind it in stream order)
+        }
+        if (pm.small_rows) {
+            ScopedTimer t(h, LTL_K_MATERIALIZE, count, bytes);
+            const dim3 grid((unsigned)((count + 3) / 4), (unsigned)((h->R + LTL_SPLIT_ROWS - 1) / LTL_SPLIT_ROWS));
+            if (h->W == 2) k_materialize_small_rows<2><<<grid, 256, 0, h->stream>>>(m);
+            else if (h->W == 4) k_materialize_small_rows<4><<<grid, 256, 0, h->stream>>>(m);
+            else if (h->W == 8) k_materialize_small_rows<8><<<grid, 256, 0, h->stream>>>(m);
+            else k_materialize_small_rows<16><<<grid, 256, 0, h->stream>>>(m);
+            CK(cudaGetLastError());
+            continue;
         }
         const i64 groups = (i64)((n_base + count + 31) / 32 - n_base / 32);
         choose_split(h, groups, &m.nsplit, &m.rows_per_split);

@@ -1005,6 +1005,42 @@ __global__ void __launch_bounds__(256) k_screen_small_rows(const __grid_constant
     if (e) atomicAdd(p.acc + 3 * c + 2, (u64)e);
 }
 
+// Phase B of a small pass over multi-word rows: one lane per (new entry, row), from the entry's record.  (The tile-shaped
+// phase B has the tile kernel's ~50 us minimum; BASELINE config 3 paid it on each of its first four cost levels.)
+template <int W>
+__global__ void __launch_bounds__(256) k_materialize_small_rows(const __grid_constant__ MaterializeParams p) {
+    const i64 k = (i64)blockIdx.x * 4 + (threadIdx.x >> 6);
+    const int r = (int)blockIdx.y * LTL_SPLIT_ROWS + (threadIdx.x & 63);
+    if (k >= p.count || r >= p.R) return;
+    const i64 dst = p.n_base + k;
+    const int op = (int)p.rec_op[dst];
+    const i64 lhs = p.rec_lhs[dst], rhs = p.rec_rhs[dst];
+    const i64 n = p.n;
+    const size_t kb = (size_t)r * W;
+    const u64* __restrict__ px = p.cms + cm_index(lhs, n, 0);
+    const u64* __restrict__ py = p.cms + cm_index(rhs >= 0 ? rhs : lhs, n, 0);
+    u64* __restrict__ po = p.cms + cm_index(dst, n, 0);
+    u64 x[W], y[W], m[W], out[W];
+#pragma unroll
+    for (int w = 0; w < W; w++) {
+        x[w] = ld_nc(px + (kb + w) * 32);
+        y[w] = rhs >= 0 ? ld_nc(py + (kb + w) * 32) : 0ull;
+        m[w] = ld_nc(p.masks + kb + w);
+    }
+    switch (op) {
+        case OP_NOT: apply_row<OP_NOT, W>(out, x, y, m); break;
+        case OP_AND: apply_row<OP_AND, W>(out, x, y, m); break;
+        case OP_OR: apply_row<OP_OR, W>(out, x, y, m); break;
+        case OP_NEXT: apply_row<OP_NEXT, W>(out, x, y, m); break;
+        case OP_FINALLY: apply_row<OP_FINALLY, W>(out, x, y, m); break;
+        case OP_GLOBALLY: apply_row<OP_GLOBALLY, W>(out, x, y, m); break;
+        case OP_UNTIL: apply_row<OP_UNTIL, W>(out, x, y, m); break;
+        default: apply_row<OP_IDENT, W>(out, x, y, m); break;
+    }
+#pragma unroll
+    for (int w = 0; w < W; w++) po[(kb + w) * 32] = out[w];
+}
+
 // ------------------------------------------------------------------------------------------------
 // phase B kernel
 
