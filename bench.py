@@ -322,7 +322,8 @@ def build_roofline(kstats, steps, clocks, config, hash_name, max_cost, sm_count)
         m = {"bound": "hbm", "kernel": "k_materialize_not + k_materialize", "achieved": mat_bytes / (mat_ms / 1e3) / 1e9,
              "peak": peak, "unit": "GB/s", "frac": mat_bytes / (mat_ms / 1e3) / 1e9 / peak,
              "note": "algorithmic bytes = admitted entries x (stored matrix bytes + 16 + 9) written (SURVEY 8d) + 16 per fused "
-                     "NOT candidate; the operand matrices it re-reads are not counted"}
+                     "NOT candidate; the operand matrices it re-reads are not counted; a fused launch whose store gate was closed "
+                     "(the level solved: DESIGN.md 4, gated store) is booked as the NOT pass it was, entries x (matrix bytes + 16)"}
         if entry and entry.get("k_materialize_dram_bytes_per_step"):
             mt = entry["k_materialize_dram_bytes_per_step"]
             m["dram"] = {"achieved": mt * steps / (mat_ms / 1e3) / 1e9, "unit": "GB/s",

@@ -255,7 +255,9 @@ LTL_API int ltl_core_set_table_shard(ltl_core* h, int shard, int n_shards);
  * events on the launching stream), "max_split" (cap on row splits), "force_split" (tests),
  * "store_results" (0: from now on admitted entries keep fingerprint + record but their matrices are not
  * written -- for the last cost level of a search, whose entries are never operands; counters, records and
- * statuses are unaffected, get_cm / export_cms of such entries fail with LTL_ERR_ARG). */
+ * statuses are unaffected, get_cm / export_cms of such entries fail with LTL_ERR_ARG),
+ * "gate_store" (default 1: the phase B that also screens NOT(new entry) is issued behind the level's phase A and writes
+ * the matrices only if that found no solver; 0: always write first, the order of round 1). */
 LTL_API int ltl_core_set_option(ltl_core* h, const char* name, int64_t value);
 /* Accumulated per kernel class since creation / the last reset: launches, device milliseconds (profile
  * mode only), algorithmic bytes and candidates / entries processed. */
@@ -315,7 +317,8 @@ LTL_API int ltl_core_host_times(ltl_core* h, double out[3]);
 LTL_API int ltl_core_transfer_stats(ltl_core* h, uint64_t out[2]);
 /* out[0..5] = effective entry capacity, device bytes mapped for matrices, table slots, chunk candidates,
  * bit 0: the store uses virtual-memory growth, bit 1: an S_OOM status came from exhausted DEVICE memory rather
- * than from the logical budget; words per matrix */
+ * than from the logical budget, bits 8..: conditional phase-B launches that skipped their store because the pass they
+ * were issued behind had found a solver (option "gate_store"); words per matrix */
 LTL_API int ltl_core_info(ltl_core* h, uint64_t out[6]);
 
 #ifdef __cplusplus

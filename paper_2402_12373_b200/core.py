@@ -691,7 +691,7 @@ class CudaCore:
         self._check(self._L.ltl_core_info(self._h, _u64(out)))
         keys = ("capacity_entries", "matrix_bytes_mapped", "table_slots", "chunk_candidates", "flags", "words_per_matrix")
         d = {k: int(v) for k, v in zip(keys, out)}
-        d["vmm"], d["device_oom"] = bool(d["flags"] & 1), bool(d["flags"] & 2)
+        d["vmm"], d["device_oom"], d["gated_skips"] = bool(d["flags"] & 1), bool(d["flags"] & 2), d["flags"] >> 8
         return d
 
 

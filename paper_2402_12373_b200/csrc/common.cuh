@@ -100,7 +100,8 @@ struct Ctl {
     u64 total;         // winners below the solver cutoff
     u64 fp_hi, fp_lo;  // MODE_FP_ONLY / MODE_LOOKUP result for single-candidate queries
     u64 found;
-    u64 pad[2];
+    u64 gate;          // solver_c as it stood when the conditional phase B of this pass was issued (MaterializeParams::store_gate)
+    u64 pad;
 };
 
 struct ScreenParams {
@@ -157,6 +158,10 @@ struct MaterializeParams {
     int n_pos_lo;  // as in ScreenParams (half-width store)
     i64 not_cbase, not_i0;
     u32 blk_base;  // as in ScreenParams
+    // Conditional store (fused NOT only): non-null => the matrices are written only if *store_gate == ~0, i.e. if the
+    // pass that is being screened had found no solver when this launch was issued.  A search that ends in this pass never
+    // reads the newest level's matrices: only NOT(entry), evaluated here from registers, was needed of them.
+    const u64* store_gate;
     // Processing order of the 32-entry groups ("phase B order"): n_seg == 0: group k of the launch is group
     // n_base/32 + k; else the launch walks n_seg runs of groups, run s = groups seg_g0[s] .. of length seg_goff[s+1] -
     // seg_goff[s], ordered so that the runs reading the same block of right operands follow one another

@@ -963,7 +963,9 @@ struct ltl_core : Arena {
     ltl_exchange_fn exchange = nullptr;
     void* exchange_ctx = nullptr;
     bool fuse_not = true;  // phase B of a level also screens NOT(new entry) for the next level (k_materialize_not)
-    i64 fuse_not_min = 32768;  // ... when it writes at least this many entries: the fused kernel folds all rows of an
+    bool gate_store = true;  // ... and writes the matrices only if the pass it is issued behind found no solver (run_chunk)
+    i64 fuse_not_min = 32768;
+    u64 gated_skips = 0;  // conditional phase-B launches that found the gate closed (statistics)  // ... when it writes at least this many entries: the fused kernel folds all rows of an
                                // entry in one lane (no row split), which is slow on a launch that cannot fill the SMs
     int tiled_materialize = -1;  // phase B over phase A's tiles instead of per record: 1 always, 0 never, -1 by size
     bool device_oom = false;      // an S_OOM came from the device, not from the logical budget
@@ -1087,7 +1089,9 @@ static int ensure_table(ltl_core* h, u64 need_keys) {
     return LTL_OK;
 }
 
-static int flush_materialize(ltl_core* h, const ScreenParams* sp = nullptr, int fuse_kind = 0, i64 not_cbase = 0, i64 not_i0 = 0);
+static int flush_materialize(ltl_core* h, const ScreenParams* sp = nullptr, int fuse_kind = 0, i64 not_cbase = 0, i64 not_i0 = 0,
+                             const u64* store_gate = nullptr);
+static int check_masks(ltl_core* h, u64 first, u64 count);
 
 static int ensure_scratch(ltl_core* h, i64 total) {
     if (total <= h->scratch_cap) return LTL_OK;
@@ -1528,10 +1532,19 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     double issued_bytes = 0;
     const bool mueller = h->variant == VAR_MUELLER || h->variant == VAR_NH;  // hashed variants: two 64-bit sums
     const int screen_kind = h->variant == VAR_MUELLER ? KIND_MUELLER : h->variant == VAR_NH ? KIND_NH : KIND_BITS;
-    if (fused_not >= 0) {
+    // Phase B of the newest level with this level's NOT fused in.  Nothing else of this pass reads those matrices (binary
+    // connectives pair cheaper operands), so when the solver rank is final once phase A has run -- no partial sums to
+    // combine afterwards -- the launch goes out BEHIND phase A and stores only if phase A found no solver: the search
+    // that solves here (BASELINE config 2: 2.56 M entries, 21 GB) never writes the largest level it admitted.
+    const bool gated = fused_not >= 0 && h->gate_store && !p.defer && !acc_path;
+    const size_t n_pending_before = h->pending_mat.size();
+    if (fused_not >= 0 && !gated) {
         const Piece& fp = pieces[(size_t)fused_not];
         if ((rc = flush_materialize(h, &p, screen_kind, fp.cbase, fp.i0))) return rc;
     }
+    if (gated)  // room for the matrices is mapped before anything is filed: running out of device memory ends the level cleanly
+        for (auto& pm : h->pending_mat)
+            if ((rc = ensure_entries(h, pm.n_base + pm.count))) return rc;
     if (small_screen) {
         ScopedTimer t(h, LTL_K_SCREEN, (u64)total, screen_bytes(h, pieces));
         issued_units = (u64)total;
@@ -1641,6 +1654,11 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
         }
         CK(cudaGetLastError());
     }
+    if (gated) {
+        const Piece& fp = pieces[(size_t)fused_not];
+        CK(cudaMemcpyAsync(&h->d_ctl->gate, &h->d_ctl->solver_c, sizeof(u64), cudaMemcpyDeviceToDevice, h->stream));
+        if ((rc = flush_materialize(h, &p, screen_kind, fp.cbase, fp.i0, &h->d_ctl->gate))) return rc;
+    }
     if (acc_path && !small) {
         ScopedTimer t(h, LTL_K_FINALIZE, (u64)total, (double)total * 36.0);
         if (mueller) k_finalize<true><<<(unsigned)((total + 255) / 256), 256, 0, h->stream>>>(p, (u64)total);
@@ -1730,6 +1748,23 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     const u64 winners = h->h_ctl->total;
     const u64 oom_c = h->h_ctl->oom_c;
     drain_events(h);
+    if (gated) {
+        if (h->h_ctl->gate == ~0ull) {  // the gate was open: the pending ranges are written
+            if (h->debug_masks)
+                for (size_t k = 0; k < n_pending_before; k++)
+                    if ((rc = check_masks(h, h->pending_mat[k].n_base, h->pending_mat[k].count))) {
+                        h->pending_mat.clear();
+                        return rc;
+                    }
+            h->pending_mat.erase(h->pending_mat.begin(), h->pending_mat.begin() + (std::ptrdiff_t)n_pending_before);
+        } else {  // closed: they stay pending (read-backs write them), and the launch is booked as the NOT pass it was
+            for (size_t k = 0; k < n_pending_before; k++) {
+                h->pending_mat[k].n_seg = 0;  // (the plan arrays may be reused by then: entry order)
+                h->stats[LTL_K_MATERIALIZE].bytes -= (double)h->pending_mat[k].count * 25.0;
+            }
+            h->gated_skips++;
+        }
+    }
     const bool oom = winners > room;
     const u64 count = oom ? room : winners;
     if (oom && oom_c == ~0ull) return h->fail(LTL_ERR_CUDA, "internal: overflow rank missing");
@@ -1823,7 +1858,9 @@ static int check_masks(ltl_core* h, u64 first, u64 count) {
 
 // Phase B for every admitted-but-unwritten range.  With `sp` (the admission pass being issued) and fuse_kind != 0 it
 // also screens NOT(entry) for every entry it writes: candidate not_cbase + (entry - not_i0) of that pass.
-static int flush_materialize(ltl_core* h, const ScreenParams* sp, int fuse_kind, i64 not_cbase, i64 not_i0) {
+// With `store_gate` (fused launches only) the store is conditional (MaterializeParams::store_gate) and the ranges stay
+// pending: the caller drops them once it knows the gate was open.
+static int flush_materialize(ltl_core* h, const ScreenParams* sp, int fuse_kind, i64 not_cbase, i64 not_i0, const u64* store_gate) {
     int rc;
     for (auto& pm : h->pending_mat) {
         const u64 n_base = pm.n_base, count = pm.count;
@@ -1903,6 +1940,7 @@ static int flush_materialize(ltl_core* h, const ScreenParams* sp, int fuse_kind,
             m.n_pos_lo = h->n_pos_lo;
             m.not_cbase = not_cbase;
             m.not_i0 = not_i0;
+            m.store_gate = store_gate;
             fk = fuse_kind;
         }
         ScopedTimer t(h, LTL_K_MATERIALIZE, count, bytes + (fk ? (double)count * 16.0 : 0.0));
@@ -1910,6 +1948,7 @@ static int flush_materialize(ltl_core* h, const ScreenParams* sp, int fuse_kind,
         (h->pair ? ltl_launch_materialize_w1p : MATERIALIZE_FN[h->W])(m, fk ? *sp : none, fk, grid, h->stream);
         CK(cudaGetLastError());
     }
+    if (store_gate) return LTL_OK;
     if (h->debug_masks)
         for (auto& pm : h->pending_mat)
             if ((rc = check_masks(h, pm.n_base, pm.count))) {
@@ -3059,6 +3098,8 @@ int ltl_core_set_option(ltl_core* h, const char* name, int64_t value) {
         h->fuse_unary = value != 0;
     } else if (!strcmp(name, "fuse_not")) {
         h->fuse_not = value != 0;
+    } else if (!strcmp(name, "gate_store")) {
+        h->gate_store = value != 0;
     } else if (!strcmp(name, "debug_masks")) {
         h->debug_masks = value != 0;
     } else if (!strcmp(name, "exchange_parts")) {
@@ -3415,7 +3456,7 @@ int ltl_core_info(ltl_core* h, uint64_t out[6]) {
     out[1] = h->cms.mapped;
     out[2] = h->table_cap;
     out[3] = (u64)h->chunk_cap;
-    out[4] = (h->cms.vmm ? 1 : 0) | (h->device_oom ? 2 : 0);
+    out[4] = (h->cms.vmm ? 1 : 0) | (h->device_oom ? 2 : 0) | (h->gated_skips << 8);
     out[5] = (u64)h->n_api;
     return LTL_OK;
 }

@@ -1174,8 +1174,8 @@ struct NotFold {
 };
 
 template <int OP, int FK, bool PAIR>
-__device__ __forceinline__ void mat_rows_not(const MaterializeParams& p, const bool mine, const i64 dst, const int lhs,
-                                             const int rhs, NotFold<FK>& f) {
+__device__ __forceinline__ void mat_rows_not(const MaterializeParams& p, const bool mine, const bool store, const i64 dst,
+                                             const int lhs, const int rhs, NotFold<FK>& f) {
     constexpr bool BIN = !(OP == OP_IDENT || OP == OP_NOT || OP == OP_NEXT || OP == OP_FINALLY || OP == OP_GLOBALLY);
     if (!mine) return;
     const i64 n = p.n;
@@ -1191,7 +1191,7 @@ __device__ __forceinline__ void mat_rows_not(const MaterializeParams& p, const b
         y[0] = BIN ? ld_nc(py + (size_t)r * 32) : 0ull;
         m[0] = ld_nc(pm + r);
         apply_row<OP, 1, PAIR>(out, x, y, m);
-        __stcs(po + (size_t)r * 32, out[0]);  // streaming store: keeps the operand blocks in L2
+        if (store) __stcs(po + (size_t)r * 32, out[0]);  // streaming store: keeps the operand blocks in L2
         f.template word<PAIR>(~out[0] & m[0], kbase + (u32)r, pk, r < n_pos, r < n_pos_lo);
     };
     constexpr int UNROLL = LTL_MATF_UNROLL;
@@ -1218,6 +1218,8 @@ __global__ void __launch_bounds__(LTL_CTA, LTL_MATF_MINB) k_materialize_not(cons
     const int op = valid ? (int)p.rec_op[dst] : -1;
     const int lhs = valid ? p.rec_lhs[dst] : 0;
     const int rhs = valid ? p.rec_rhs[dst] : 0;
+    // (the gate is a snapshot taken before this launch: candidates filed here may lower ctl->solver_c, never the gate)
+    const bool store = p.store_gate == nullptr || ld_nc(p.store_gate) == ~0ull;
     NotFold<FK> f;
     f.s0 = f.s1 = 0;
     f.err = 0;
@@ -1228,14 +1230,14 @@ __global__ void __launch_bounds__(LTL_CTA, LTL_MATF_MINB) k_materialize_not(cons
         const bool mine = valid && op == cur;
         remaining &= ~__ballot_sync(0xFFFFFFFFu, mine);
         switch (cur) {
-            case OP_NOT: mat_rows_not<OP_NOT, FK, PAIR>(p, mine, dst, lhs, rhs, f); break;
-            case OP_AND: mat_rows_not<OP_AND, FK, PAIR>(p, mine, dst, lhs, rhs, f); break;
-            case OP_OR: mat_rows_not<OP_OR, FK, PAIR>(p, mine, dst, lhs, rhs, f); break;
-            case OP_NEXT: mat_rows_not<OP_NEXT, FK, PAIR>(p, mine, dst, lhs, rhs, f); break;
-            case OP_FINALLY: mat_rows_not<OP_FINALLY, FK, PAIR>(p, mine, dst, lhs, rhs, f); break;
-            case OP_GLOBALLY: mat_rows_not<OP_GLOBALLY, FK, PAIR>(p, mine, dst, lhs, rhs, f); break;
-            case OP_UNTIL: mat_rows_not<OP_UNTIL, FK, PAIR>(p, mine, dst, lhs, rhs, f); break;
-            default: mat_rows_not<OP_IDENT, FK, PAIR>(p, mine, dst, lhs, rhs, f); break;
+            case OP_NOT: mat_rows_not<OP_NOT, FK, PAIR>(p, mine, store, dst, lhs, rhs, f); break;
+            case OP_AND: mat_rows_not<OP_AND, FK, PAIR>(p, mine, store, dst, lhs, rhs, f); break;
+            case OP_OR: mat_rows_not<OP_OR, FK, PAIR>(p, mine, store, dst, lhs, rhs, f); break;
+            case OP_NEXT: mat_rows_not<OP_NEXT, FK, PAIR>(p, mine, store, dst, lhs, rhs, f); break;
+            case OP_FINALLY: mat_rows_not<OP_FINALLY, FK, PAIR>(p, mine, store, dst, lhs, rhs, f); break;
+            case OP_GLOBALLY: mat_rows_not<OP_GLOBALLY, FK, PAIR>(p, mine, store, dst, lhs, rhs, f); break;
+            case OP_UNTIL: mat_rows_not<OP_UNTIL, FK, PAIR>(p, mine, store, dst, lhs, rhs, f); break;
+            default: mat_rows_not<OP_IDENT, FK, PAIR>(p, mine, store, dst, lhs, rhs, f); break;
         }
         __syncwarp();
     }
