@@ -477,6 +477,7 @@ def test_fused_not_levels_match_unfused(R, err_max, budget_entries, chunk, varia
     kw = {} if chunk is None else {"chunk_candidates": chunk}
     a, b, c = (CudaCore(masks, R // 2, err_max, variant, budget_bytes=budget, **kw) for _ in range(3))
     a.set_option("fuse_not_min", 0)  # by default only launches that fill the device are fused
+    a.set_option("gate_store", 1)
     c.set_option("fuse_not_min", 0)
     c.set_option("gate_store", 0)
     b.set_option("fuse_not", 0)
