@@ -100,7 +100,7 @@ while time.time() < t_end:
     desc = f"#{n} props={n_props} P={spec.n_pos} N={spec.n_neg} len={lo}..{hi} planted={planted} {kw}"
     fused_opts = "fuse_not_min=0" + (",chunk_candidates=%d" % int(rng.integers(100, 5000)) if rng.random() < 0.3 else "")
     # the fused launch behind phase A with its store gated on the solver (needs passes without row split), or round 1's order
-    fused_opts += str(rng.choice([",small_screen=0,max_split=1", ",max_split=1", "", ",gate_store=0"]))
+    fused_opts += str(rng.choice([",gate_store=1,small_screen=0,max_split=1", ",gate_store=1,max_split=1", ",gate_store=1", ",gate_store=0"]))
     with_cand2 = rng.random() < 0.3
     if os.environ.get("SOAK_ONLY") and n > int(os.environ["SOAK_ONLY"]):
         break
