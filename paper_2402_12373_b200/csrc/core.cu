@@ -1532,12 +1532,33 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
     double issued_bytes = 0;
     const bool mueller = h->variant == VAR_MUELLER || h->variant == VAR_NH;  // hashed variants: two 64-bit sums
     const int screen_kind = h->variant == VAR_MUELLER ? KIND_MUELLER : h->variant == VAR_NH ? KIND_NH : KIND_BITS;
-    // Phase B of the newest level with this level's NOT fused in.  Nothing else of this pass reads those matrices (binary
-    // connectives pair cheaper operands), so when the solver rank is final once phase A has run -- no partial sums to
-    // combine afterwards -- the launch goes out BEHIND phase A and stores only if phase A found no solver: the search
-    // that solves here (BASELINE config 2: 2.56 M entries, 21 GB) never writes the largest level it admitted.
-    const bool gated = fused_not >= 0 && h->gate_store && !p.defer && !acc_path;
+    // Phase B of the newest level with this level's NOT fused in.  The pieces in front of the first one that reads those
+    // matrices -- the level's AND / OR candidates: binary connectives pair cheaper operands -- do not need them, so when the
+    // solver rank of a tile is final once the tile has run (no partial sums to combine afterwards) the launch goes out
+    // BEHIND their tiles and stores only if they found no solver: the search that solves there (BASELINE config 2: 2.56 M
+    // entries, 21 GB) never writes the largest level it admitted.  Tiles behind the gate are launched after it in stream
+    // order: either the matrices are there by then, or a solver below them is known and they return at once.
+    const bool gated = fused_not >= 0 && h->gate_store && !p.defer && !acc_path && !small_screen;
     const size_t n_pending_before = h->pending_mat.size();
+    i64 gate_tile = tiles;  // first tile of the first piece that reads a pending entry
+    if (gated) {
+        const i64 pend0 = (i64)h->pending_mat.front().n_base;
+        for (size_t k = 0; k < pieces.size(); k++) {
+            const Piece& pc = pieces[k];
+            if (pc.ext || !pc.owns_tiles || (int)k == fused_not) continue;
+            if (pc.i1 > pend0 || (pc.kind != PIECE_UNARY && pc.j1 > pend0)) {
+                gate_tile = pc.tile_base;
+                break;
+            }
+        }
+    }
+    bool gate_issued = false;
+    auto issue_gate = [&]() -> int {
+        const Piece& fp = pieces[(size_t)fused_not];
+        gate_issued = true;
+        CK(cudaMemcpyAsync(&h->d_ctl->gate, &h->d_ctl->solver_c, sizeof(u64), cudaMemcpyDeviceToDevice, h->stream));
+        return flush_materialize(h, &p, screen_kind, fp.cbase, fp.i0, &h->d_ctl->gate);
+    };
     if (fused_not >= 0 && !gated) {
         const Piece& fp = pieces[(size_t)fused_not];
         if ((rc = flush_materialize(h, &p, screen_kind, fp.cbase, fp.i0))) return rc;
@@ -1621,8 +1642,10 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
             issued_bytes = 0;
             u64 known_solver = ~0ull;
             int k = 0;
-            for (i64 t0 = 0; t0 < tiles; t0 += per, k++) {
-                const i64 t1 = std::min(tiles, t0 + per);
+            for (i64 t0 = 0, t1 = 0; t0 < tiles; t0 = t1, k++) {
+                if (gated && !gate_issued && t0 >= gate_tile && (rc = issue_gate())) return rc;
+                t1 = std::min(tiles, t0 + per);
+                if (gated && !gate_issued && t1 > gate_tile) t1 = gate_tile;  // (t0 < gate_tile here)
                 if (per < tiles) {
                     if (k >= 2) {
                         HostTimer ht(&h->sync_ms);
@@ -1654,11 +1677,7 @@ static int run_chunk(ltl_core* h, std::vector<Piece>& pieces, i64 total, i64 til
         }
         CK(cudaGetLastError());
     }
-    if (gated) {
-        const Piece& fp = pieces[(size_t)fused_not];
-        CK(cudaMemcpyAsync(&h->d_ctl->gate, &h->d_ctl->solver_c, sizeof(u64), cudaMemcpyDeviceToDevice, h->stream));
-        if ((rc = flush_materialize(h, &p, screen_kind, fp.cbase, fp.i0, &h->d_ctl->gate))) return rc;
-    }
+    if (gated && !gate_issued && (rc = issue_gate())) return rc;  // (no tile behind the gate, or phase A stopped at a solver)
     if (acc_path && !small) {
         ScopedTimer t(h, LTL_K_FINALIZE, (u64)total, (double)total * 36.0);
         if (mueller) k_finalize<true><<<(unsigned)((total + 255) / 256), 256, 0, h->stream>>>(p, (u64)total);
