@@ -963,7 +963,7 @@ struct ltl_core : Arena {
     ltl_exchange_fn exchange = nullptr;
     void* exchange_ctx = nullptr;
     bool fuse_not = true;  // phase B of a level also screens NOT(new entry) for the next level (k_materialize_not)
-    bool gate_store = false;  // (off until verified on the GPU) ... and writes the matrices only if the pass it is issued behind found no solver (run_chunk)
+    bool gate_store = true;  // ... and writes the matrices only if the pass it is issued behind found no solver (run_chunk)
     i64 fuse_not_min = 32768;
     u64 gated_skips = 0;  // conditional phase-B launches that found the gate closed (statistics)  // ... when it writes at least this many entries: the fused kernel folds all rows of an
                                // entry in one lane (no row split), which is slow on a launch that cannot fill the SMs
