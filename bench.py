@@ -78,13 +78,16 @@ def sources_digest() -> str:
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region: the sampler runs from before the warm-up
+    (nvidia-smi needs ~0.2 s to produce its first line), `mark()` is called when the timed region starts, and only lines
+    that arrived after it count.  A region shorter than the 100 ms period may see none: then the last line before it --
+    taken under the same load, during the warm-up -- is reported with `"samples": 0, "nearest": true`."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
     def __init__(self, index: int):
-        self.index, self.rows, self.proc = index, [], None
+        self.index, self.rows, self.proc, self.t_mark = index, [], None, 0.0
 
     def start(self):
         try:
@@ -96,7 +99,10 @@ class ClockSampler:
 
     def _pump(self):
         for line in self.proc.stdout:
-            self.rows.append([c.strip() for c in line.split(",")])
+            self.rows.append((time.perf_counter(), [c.strip() for c in line.split(",")]))
+
+    def mark(self):
+        self.t_mark = time.perf_counter()
 
     def stop(self) -> dict:
         if self.proc is None:
@@ -105,7 +111,11 @@ class ClockSampler:
         self.proc.terminate()
         sm, smax, reasons = [], [], set()
         names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
-        for r in self.rows:
+        rows = [r for t, r in self.rows if t >= self.t_mark]
+        nearest = not rows and bool(self.rows)
+        if nearest:
+            rows = [self.rows[-1][1]]
+        for r in rows:
             try:
                 sm.append(float(r[0]))
                 smax.append(float(r[1]))
@@ -114,8 +124,11 @@ class ClockSampler:
                         reasons.add(n)
             except Exception:
                 pass
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+        out = {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+               "samples": 0 if nearest else len(sm), "reasons": sorted(reasons)}
+        if nearest:
+            out["nearest"] = True
+        return out
 
 
 # ------------------------------------------------------------------------------------------------ CPU arm
@@ -324,7 +337,8 @@ def build_roofline(kstats, steps, clocks, config, hash_name, max_cost, sm_count)
              "note": "algorithmic bytes = admitted entries x (stored matrix bytes + 16 + 9) written (SURVEY 8d) + 16 per fused "
                      "NOT candidate; the operand matrices it re-reads are not counted; a fused launch whose store gate was closed "
                      "(the level solved: DESIGN.md 4, gated store) is booked as the NOT pass it was, entries x (matrix bytes + 16)"}
-        if entry and entry.get("k_materialize_dram_bytes_per_step"):
+        # (the DRAM bytes of phase B are only quoted from a pass over this very build: its launches are what changes)
+        if entry and entry.get("build_digest") == sources_digest() and entry.get("k_materialize_dram_bytes_per_step"):
             mt = entry["k_materialize_dram_bytes_per_step"]
             m["dram"] = {"achieved": mt * steps / (mat_ms / 1e3) / 1e9, "unit": "GB/s",
                          "frac": mt * steps / (mat_ms / 1e3) / 1e9 / peak, "bytes_per_step": mt,
@@ -361,6 +375,8 @@ def measure_config(config: str, args, *, steps: int, warmup: int, cpu_cost: int 
         return en
 
     # ---- warm-up (also validates the answer)
+    sampler = ClockSampler(local_rank)
+    sampler.start()
     res = None
     for _ in range(max(warmup, 3)):
         en = resident_search(False)
@@ -375,12 +391,11 @@ def measure_config(config: str, args, *, steps: int, warmup: int, cpu_cost: int 
     # ---- timed: device-resident inputs.  Per step the core is created and the atoms are admitted OUTSIDE the
     # timed region (inputs resident in HBM), the cost-level loop runs INSIDE it, bracketed by CUDA events and a
     # device synchronize on both sides; the K timed intervals are summed.
-    sampler = ClockSampler(local_rank)
     kstats, host_times, close_ms = [], [], 0.0
     launches = 0
     dev_ms = wall = 0.0
     torch.cuda.synchronize()
-    sampler.start()
+    sampler.mark()
     for _ in range(steps):
         en = resident_search(True)
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)

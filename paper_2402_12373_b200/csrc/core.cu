@@ -1966,6 +1966,7 @@ static int flush_materialize(ltl_core* h, const ScreenParams* sp, int fuse_kind,
         dim3 grid((unsigned)((groups + LTL_WARPS_PER_CTA - 1) / LTL_WARPS_PER_CTA), (unsigned)m.nsplit);
         (h->pair ? ltl_launch_materialize_w1p : MATERIALIZE_FN[h->W])(m, fk ? *sp : none, fk, grid, h->stream);
         CK(cudaGetLastError());
+        if (fk && store_gate) h->stats[LTL_K_MATERIALIZE].launches += 1;  // (the storing kernel and its evaluate-only twin)
     }
     if (store_gate) return LTL_OK;
     if (h->debug_masks)

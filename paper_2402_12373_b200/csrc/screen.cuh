@@ -1131,6 +1131,14 @@ __global__ void __launch_bounds__(LTL_CTA) k_materialize(const __grid_constant__
 #ifndef LTL_MATF_MINB
 #define LTL_MATF_MINB 2
 #endif
+// the evaluate-only twin (closed store gate): nothing is written, so the launch is bound by issue and latency, not by HBM
+// writes -- more resident warps, shorter unroll
+#ifndef LTL_MATF_EVAL_UNROLL
+#define LTL_MATF_EVAL_UNROLL 8
+#endif
+#ifndef LTL_MATF_EVAL_MINB
+#define LTL_MATF_EVAL_MINB 3
+#endif
 
 template <int FK>
 struct NotFold {
@@ -1173,8 +1181,8 @@ struct NotFold {
     }
 };
 
-template <int OP, int FK, bool PAIR>
-__device__ __forceinline__ void mat_rows_not(const MaterializeParams& p, const bool mine, const bool store, const i64 dst,
+template <int OP, int FK, bool PAIR, bool STORE>
+__device__ __forceinline__ void mat_rows_not(const MaterializeParams& p, const bool mine, const i64 dst,
                                              const int lhs, const int rhs, NotFold<FK>& f) {
     constexpr bool BIN = !(OP == OP_IDENT || OP == OP_NOT || OP == OP_NEXT || OP == OP_FINALLY || OP == OP_GLOBALLY);
     if (!mine) return;
@@ -1191,10 +1199,10 @@ __device__ __forceinline__ void mat_rows_not(const MaterializeParams& p, const b
         y[0] = BIN ? ld_nc(py + (size_t)r * 32) : 0ull;
         m[0] = ld_nc(pm + r);
         apply_row<OP, 1, PAIR>(out, x, y, m);
-        if (store) __stcs(po + (size_t)r * 32, out[0]);  // streaming store: keeps the operand blocks in L2
+        if (STORE) __stcs(po + (size_t)r * 32, out[0]);  // streaming store: keeps the operand blocks in L2
         f.template word<PAIR>(~out[0] & m[0], kbase + (u32)r, pk, r < n_pos, r < n_pos_lo);
     };
-    constexpr int UNROLL = LTL_MATF_UNROLL;
+    constexpr int UNROLL = STORE ? LTL_MATF_UNROLL : LTL_MATF_EVAL_UNROLL;
     for (int rb = 0; rb < R; rb += 64) {
         f.begin_block();
         if (rb + 64 <= R) {
@@ -1207,9 +1215,12 @@ __device__ __forceinline__ void mat_rows_not(const MaterializeParams& p, const b
     }
 }
 
-template <int FK, bool PAIR = false>
-__global__ void __launch_bounds__(LTL_CTA, LTL_MATF_MINB) k_materialize_not(const __grid_constant__ MaterializeParams p,
-                                                                            const __grid_constant__ ScreenParams sp) {
+// STORE = false: the evaluate-only twin.  A gated pass launches both; each returns at once unless the gate is its way.
+template <int FK, bool PAIR = false, bool STORE = true>
+__global__ void __launch_bounds__(LTL_CTA, STORE ? LTL_MATF_MINB : LTL_MATF_EVAL_MINB)
+    k_materialize_not(const __grid_constant__ MaterializeParams p, const __grid_constant__ ScreenParams sp) {
+    // (the gate is a snapshot taken before this launch: candidates filed here may lower ctl->solver_c, never the gate)
+    if (p.store_gate != nullptr && (ld_nc(p.store_gate) == ~0ull) != STORE) return;
     const int lane = threadIdx.x & 31;
     const i64 g = mat_group(p, (i64)blockIdx.x * LTL_WARPS_PER_CTA + (threadIdx.x >> 5));
     const i64 dst = g * 32 + lane;
@@ -1218,8 +1229,6 @@ __global__ void __launch_bounds__(LTL_CTA, LTL_MATF_MINB) k_materialize_not(cons
     const int op = valid ? (int)p.rec_op[dst] : -1;
     const int lhs = valid ? p.rec_lhs[dst] : 0;
     const int rhs = valid ? p.rec_rhs[dst] : 0;
-    // (the gate is a snapshot taken before this launch: candidates filed here may lower ctl->solver_c, never the gate)
-    const bool store = p.store_gate == nullptr || ld_nc(p.store_gate) == ~0ull;
     NotFold<FK> f;
     f.s0 = f.s1 = 0;
     f.err = 0;
@@ -1230,14 +1239,14 @@ __global__ void __launch_bounds__(LTL_CTA, LTL_MATF_MINB) k_materialize_not(cons
         const bool mine = valid && op == cur;
         remaining &= ~__ballot_sync(0xFFFFFFFFu, mine);
         switch (cur) {
-            case OP_NOT: mat_rows_not<OP_NOT, FK, PAIR>(p, mine, store, dst, lhs, rhs, f); break;
-            case OP_AND: mat_rows_not<OP_AND, FK, PAIR>(p, mine, store, dst, lhs, rhs, f); break;
-            case OP_OR: mat_rows_not<OP_OR, FK, PAIR>(p, mine, store, dst, lhs, rhs, f); break;
-            case OP_NEXT: mat_rows_not<OP_NEXT, FK, PAIR>(p, mine, store, dst, lhs, rhs, f); break;
-            case OP_FINALLY: mat_rows_not<OP_FINALLY, FK, PAIR>(p, mine, store, dst, lhs, rhs, f); break;
-            case OP_GLOBALLY: mat_rows_not<OP_GLOBALLY, FK, PAIR>(p, mine, store, dst, lhs, rhs, f); break;
-            case OP_UNTIL: mat_rows_not<OP_UNTIL, FK, PAIR>(p, mine, store, dst, lhs, rhs, f); break;
-            default: mat_rows_not<OP_IDENT, FK, PAIR>(p, mine, store, dst, lhs, rhs, f); break;
+            case OP_NOT: mat_rows_not<OP_NOT, FK, PAIR, STORE>(p, mine, dst, lhs, rhs, f); break;
+            case OP_AND: mat_rows_not<OP_AND, FK, PAIR, STORE>(p, mine, dst, lhs, rhs, f); break;
+            case OP_OR: mat_rows_not<OP_OR, FK, PAIR, STORE>(p, mine, dst, lhs, rhs, f); break;
+            case OP_NEXT: mat_rows_not<OP_NEXT, FK, PAIR, STORE>(p, mine, dst, lhs, rhs, f); break;
+            case OP_FINALLY: mat_rows_not<OP_FINALLY, FK, PAIR, STORE>(p, mine, dst, lhs, rhs, f); break;
+            case OP_GLOBALLY: mat_rows_not<OP_GLOBALLY, FK, PAIR, STORE>(p, mine, dst, lhs, rhs, f); break;
+            case OP_UNTIL: mat_rows_not<OP_UNTIL, FK, PAIR, STORE>(p, mine, dst, lhs, rhs, f); break;
+            default: mat_rows_not<OP_IDENT, FK, PAIR, STORE>(p, mine, dst, lhs, rhs, f); break;
         }
         __syncwarp();
     }

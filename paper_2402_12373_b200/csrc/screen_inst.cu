@@ -25,8 +25,12 @@ extern "C" void ltl_launch_screen_w1p(const ScreenParams& p, int kind, dim3 grid
 }
 extern "C" void ltl_launch_materialize_w1p(const MaterializeParams& p, const ScreenParams& sp, int fuse_kind, dim3 grid,
                                            cudaStream_t stream) {
-    if (fuse_kind == KIND_NH) k_materialize_not<KIND_NH, true><<<grid, LTL_CTA, 0, stream>>>(p, sp);
-    else k_materialize<1, true><<<grid, LTL_CTA, 0, stream>>>(p);
+    if (fuse_kind == KIND_NH) {
+        k_materialize_not<KIND_NH, true><<<grid, LTL_CTA, 0, stream>>>(p, sp);
+        if (p.store_gate) k_materialize_not<KIND_NH, true, false><<<grid, LTL_CTA, 0, stream>>>(p, sp);
+    } else {
+        k_materialize<1, true><<<grid, LTL_CTA, 0, stream>>>(p);
+    }
 }
 #else
 
@@ -68,12 +72,15 @@ extern "C" void LTL_CAT(ltl_launch_screen_small_w, LTL_W)(const ScreenParams& p,
 extern "C" void LTL_CAT(ltl_launch_materialize_w, LTL_W)(const MaterializeParams& p, const ScreenParams& sp, int fuse_kind,
                                                           dim3 grid, cudaStream_t stream) {
 #if LTL_W == 1
+    // (a gated pass launches the storing kernel and its evaluate-only twin: the gate lets exactly one of them run)
     if (fuse_kind == KIND_NH) {
         k_materialize_not<KIND_NH><<<grid, LTL_CTA, 0, stream>>>(p, sp);
+        if (p.store_gate) k_materialize_not<KIND_NH, false, false><<<grid, LTL_CTA, 0, stream>>>(p, sp);
         return;
     }
     if (fuse_kind == KIND_MUELLER) {
         k_materialize_not<KIND_MUELLER><<<grid, LTL_CTA, 0, stream>>>(p, sp);
+        if (p.store_gate) k_materialize_not<KIND_MUELLER, false, false><<<grid, LTL_CTA, 0, stream>>>(p, sp);
         return;
     }
 #endif

@@ -13,7 +13,7 @@ for v in "$@"; do
 done
 wait
 for n in "${names[@]}"; do
-  objs="build/core.o variants/screen_w1_$n.o"
+  objs="build/core.o build/traces.o build/screen_w1p.o variants/screen_w1_$n.o"
   for w in $(seq 2 16); do objs="$objs build/screen_w$w.o"; done
   nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o variants/libltlcore_$n.so $objs
   echo -n "$n: "; cuobjdump -res-usage variants/screen_w1_$n.o | grep -A1 "k_materialize" | grep -o "REG:[0-9]* STACK:[0-9]*" | tr '\n' ' '; echo
