@@ -25,6 +25,7 @@ for f in gpurun_out/${tag}_sanitize_*.log; do
   { echo "# $(basename $f)"; grep -E "COMPUTE-SANITIZER|SUMMARY|^exit|smoke ok|^rowsplit|^budget|^halfwidth|^traces |Race reported|and (Read|Write) access" "$f" | cut -c1-220 | sort | uniq -c | sort -rn | head -14; } 
 done > profiles/${tag}_sanitizer.txt
 scripts/sass_excerpt.sh paper_2402_12373_b200/csrc/build/screen_w1.o '_Z8k_screenILi1ELi3ELb0EEv12ScreenParams' > profiles/${tag}_sass_k_screen_w1_nh.txt
-scripts/sass_excerpt.sh paper_2402_12373_b200/csrc/build/screen_w1.o '_Z17k_materialize_notILi3ELb0EEv17MaterializeParams12ScreenParams' > profiles/${tag}_sass_k_materialize_not_nh.txt
+scripts/sass_excerpt.sh paper_2402_12373_b200/csrc/build/screen_w1.o '_Z17k_materialize_notILi3ELb0ELb1EEv17MaterializeParams12ScreenParams' > profiles/${tag}_sass_k_materialize_not_nh.txt
+scripts/sass_excerpt.sh paper_2402_12373_b200/csrc/build/screen_w1.o '_Z17k_materialize_notILi3ELb0ELb0EEv17MaterializeParams12ScreenParams' > profiles/${tag}_sass_k_materialize_not_nh_evalonly.txt
 scripts/sass_excerpt.sh paper_2402_12373_b200/csrc/build/screen_w1p.o 'k_screenILi1ELi3ELb1EE' > profiles/${tag}_sass_k_screen_w1_halfwidth.txt
 ls -la profiles | tail -40
