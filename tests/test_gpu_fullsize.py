@@ -136,3 +136,31 @@ def test_config4_full_size_row_split_properties():
     core._real_close()
     planted = L.learn(spec, None, alphabet, max_cost=Wl.CONFIGS["c4_many"]["max_cost"], budget_bytes=4 << 40)
     assert planted.status == "solved" and Wl.error_count(planted.formula, spec, alphabet) == 0
+
+
+def test_config2_solves_behind_a_closed_gate(monkeypatch):
+    """BASELINE config 2 ends among the AND candidates of cost level 11, in front of the first piece that reads a matrix
+    of level 10: the fused phase B of level 10 finds its store gate closed ("gated store") and only screens
+    NOT(entry).  Same outcome as a core that always stores (`gate_store=0`) -- the fixture test above holds both to the
+    oracle -- and matrices of the level left pending read back identical afterwards."""
+    from helpers import LearnerConfig
+
+    spec, alphabet = _workload("c2_planted", False)
+    want = FIXTURE["c2_planted"]
+    runs = {}
+    for gate in (1, 0):
+        monkeypatch.setenv("LTL_CORE_OPTIONS", f"gate_store={gate}")
+        cfg = LearnerConfig(ceiling=want["max_cost"] + 1, budget_bytes=int(want["budget_bytes"]), hash=HashScheme(want["hash"]))
+        en = L.Enumeration(spec, alphabet, cfg)
+        en.keep_core = True
+        out = en.run()
+        s, e = en.cache._buckets[10]
+        picks = [s, s + 1, (s + e) // 2, e - 1]  # entries of cost level 10: written only if the gate was open
+        runs[gate] = (type(out).__name__, out.cost, out.stats.offered, out.stats.admitted, out.stats.duplicates,
+                      en.core.info()["gated_skips"], (int(s), int(e)), [en.core.get_cm(i).copy() for i in picks])
+        en.core.close()
+    assert runs[1][:5] == runs[0][:5] == ("Solved", want["cost"], want["offered"], want["admitted"], want["duplicates"])
+    assert runs[1][5] == 1 and runs[0][5] == 0
+    assert runs[1][6] == runs[0][6]
+    for a, b in zip(runs[1][7], runs[0][7]):
+        assert (a == b).all()
